@@ -1,0 +1,219 @@
+/* gbopt_b200 -- B200-native (sm_100a) FP64 gray-box NN oracle, C ABI.
+ *
+ * Drop-in for the reference's network C interface (reference
+ * proj/include/gbopt.h:1-81, proj/src/capi.cpp:31-178) with the same
+ * conventions:
+ *   - every fallible call returns a gbopt_status (0 = OK);
+ *   - on failure the thread-local message from gbopt_last_error() says why;
+ *   - out-pointers / out-buffers are written only on GBOPT_OK;
+ *   - opaque handles are released by their _free function;
+ *   - caller-owned buffers carry explicit lengths; a null pointer or a
+ *     length that does not match the network is GBOPT_ERR_ARGUMENT;
+ *   - exceptions never cross this boundary;
+ *   - a handle is not thread-safe by itself; distinct handles may be used
+ *     from distinct threads.
+ *
+ * Layouts chosen by this ABI (the reference returns Eigen column-major):
+ *   J (m x n) is ROW-major: J[i*n + j] = dNN_i/dx_j (the order the
+ *   reduced-space callback writes, reference formulations.cpp:320-331);
+ *   H (n x n) is the full symmetric matrix, row-major;
+ *   weights passed to gbopt_net_from_layers are row-major (GBNN order).
+ *
+ * Activation codes follow GBNN v1 (reference nn_io.cpp:184, nn.hpp:12-17):
+ *   0 linear, 1 tanh, 2 sigmoid, 3 softmax (final layer only),
+ *   4 softplus (extension of this build; the reference rejects code 4).
+ *
+ * Compute entry points (forward ... oracle_batched) run on the GPU the
+ * handle is bound to; there is no CPU fallback.  Without a usable CUDA
+ * device they return GBOPT_ERR_DEVICE.  Loading, saving, generation and
+ * the accessors are host-side and work without a GPU.
+ */
+#ifndef GBOPT_B200_H
+#define GBOPT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same values as the reference gbopt_status (gbopt.h:19-31) plus
+ * GBOPT_ERR_DEVICE for CUDA failures / no device. */
+typedef enum gbopt_status {
+  GBOPT_OK = 0,
+  GBOPT_ERR_STRUCTURAL = 1,
+  GBOPT_ERR_NUMERIC = 2,
+  GBOPT_ERR_SINGULAR = 3,
+  GBOPT_ERR_IO = 4,
+  GBOPT_ERR_FORMAT = 5,
+  GBOPT_ERR_DIMENSION = 6,
+  GBOPT_ERR_TRUNCATED = 7,
+  GBOPT_ERR_RANGE = 8,
+  GBOPT_ERR_ARGUMENT = 9,
+  GBOPT_ERR_INTERNAL = 10,
+  GBOPT_ERR_DEVICE = 11
+} gbopt_status;
+
+typedef enum gbopt_activation {
+  GBOPT_ACT_LINEAR = 0,
+  GBOPT_ACT_TANH = 1,
+  GBOPT_ACT_SIGMOID = 2,
+  GBOPT_ACT_SOFTMAX = 3,
+  GBOPT_ACT_SOFTPLUS = 4
+} gbopt_activation;
+
+/* Weight initialisers for gbopt_net_random_ex.  UNIFORM_FANIN is the
+ * reference random_net (nn.cpp:336-367): W and b ~ U(+-1/sqrt(fan_in)). */
+typedef enum gbopt_init {
+  GBOPT_INIT_UNIFORM_FANIN = 0,
+  GBOPT_INIT_XAVIER_UNIFORM = 1, /* U(+-sqrt(6/(fan_in+fan_out))) */
+  GBOPT_INIT_XAVIER_NORMAL = 2,  /* N(0, 2/(fan_in+fan_out)) */
+  GBOPT_INIT_NORMAL_FANIN = 3    /* N(0, 1/fan_in) */
+} gbopt_init;
+
+typedef struct gbopt_net gbopt_net;
+typedef struct gbopt_prng gbopt_prng;
+
+/* Thread-local message of the most recent failed call on this thread; never
+ * NULL; empty after a successful call.  (reference gbopt.h:50-53) */
+const char* gbopt_last_error(void);
+
+/* Library version string, e.g. "gbopt_b200 1.0 sm_100a". */
+const char* gbopt_version(void);
+
+/* ---- devices ------------------------------------------------------------ */
+
+/* Number of CUDA devices visible (0 when none / no driver). */
+int gbopt_device_count(void);
+
+/* ---- seeded generation (reference prng.hpp:11-23) ------------------------
+ * mt19937_64; uniform01 = (raw >> 11) * 2^-53.  Normals are Box-Muller on
+ * two uniforms (u1 mapped to (0,1]), both values of each pair used. */
+gbopt_status gbopt_prng_new(uint64_t seed, gbopt_prng** out);
+void gbopt_prng_free(gbopt_prng* rng);
+gbopt_status gbopt_prng_raw(gbopt_prng* rng, uint64_t* buf, size_t n);
+gbopt_status gbopt_prng_uniform(gbopt_prng* rng, double lo, double hi,
+                                double* buf, size_t n);
+gbopt_status gbopt_prng_normal(gbopt_prng* rng, double mean, double stddev,
+                               double* buf, size_t n);
+
+/* ---- networks (reference gbopt.h:59-81) --------------------------------- */
+
+/* GBNN v1 binary, or the JSON mirror when the path ends in ".json"
+ * (reference nn_io.cpp:144-247). */
+gbopt_status gbopt_net_load(const char* path, gbopt_net** out);
+gbopt_status gbopt_net_save(const gbopt_net* net, const char* path);
+
+/* Reference random_net (nn.cpp:336-367); activations by name: linear,
+ * tanh, sigmoid, softmax, softplus. */
+gbopt_status gbopt_net_random(const int64_t* widths, size_t n_widths,
+                              const char* hidden_activation,
+                              const char* final_activation, uint64_t seed,
+                              gbopt_net** out);
+
+/* Seeded net drawn from an existing generator stream: for each layer in
+ * order, W row-major then b (the draw order of nn.cpp:354-362).  Biases
+ * are U(bias_lo, bias_hi); bias_lo == bias_hi gives constant biases and
+ * draws nothing.  For GBOPT_INIT_UNIFORM_FANIN the biases use the fan-in
+ * bound exactly as random_net and bias_lo/hi are ignored. */
+gbopt_status gbopt_net_random_ex(gbopt_prng* rng, const int64_t* widths,
+                                 size_t n_widths, int hidden_activation,
+                                 int final_activation, int init,
+                                 double bias_lo, double bias_hi,
+                                 gbopt_net** out);
+
+/* "Load MLP weights and activations" from memory: n_layers layers, widths
+ * has n_layers+1 entries, weights[l] is row-major widths[l+1] x widths[l],
+ * biases[l] has widths[l+1] entries.  Validates like the reference
+ * NeuralNet constructor (nn.cpp:74-103). */
+gbopt_status gbopt_net_from_layers(size_t n_layers, const int64_t* widths,
+                                   const int32_t* activations,
+                                   const double* const* weights,
+                                   const double* const* biases,
+                                   gbopt_net** out);
+
+void gbopt_net_free(gbopt_net* net);
+
+int64_t gbopt_net_input_dim(const gbopt_net* net);
+int64_t gbopt_net_output_dim(const gbopt_net* net);
+int64_t gbopt_net_param_count(const gbopt_net* net);
+int64_t gbopt_net_layer_count(const gbopt_net* net);
+
+/* Shape/activation of layer l and a row-major copy of its parameters
+ * (w: rows*cols, b: rows; either may be NULL when not wanted). */
+gbopt_status gbopt_net_layer_info(const gbopt_net* net, int64_t l,
+                                  int64_t* rows, int64_t* cols,
+                                  int32_t* activation);
+gbopt_status gbopt_net_layer_copy(const gbopt_net* net, int64_t l, double* w,
+                                  size_t w_len, double* b, size_t b_len);
+
+/* Binds the handle to CUDA device `ordinal` and uploads the weights into
+ * HBM in kernel layout (idempotent).  Compute calls on an unbound handle
+ * bind it to the calling thread's current CUDA device. */
+gbopt_status gbopt_net_bind_device(gbopt_net* net, int ordinal);
+/* Device the handle is bound to, or -1. */
+int gbopt_net_device(const gbopt_net* net);
+
+/* ---- oracle calls (reference nn.hpp:58-74) -------------------------------
+ * All synchronous: results are in the caller's host buffers on return. */
+
+/* y = NN(x).  (reference gbopt.h:78-81, nn.cpp:113-125) */
+gbopt_status gbopt_net_forward(const gbopt_net* net, const double* x,
+                               size_t n, double* y, size_t m);
+
+/* J = dy/dx, m x n row-major, jac_len == m*n.  (nn.cpp:148-170) */
+gbopt_status gbopt_net_jacobian(const gbopt_net* net, const double* x,
+                                size_t n, double* jac, size_t jac_len);
+
+/* g = grad_x(lambda^T NN(x)), length n.  (nn.cpp:172-196) */
+gbopt_status gbopt_net_lagrangian_gradient(const gbopt_net* net,
+                                           const double* x, size_t n,
+                                           const double* lambda, size_t m,
+                                           double* g, size_t g_len);
+
+/* H = sum_i lambda_i Hess NN_i(x), n x n symmetric, hess_len == n*n.
+ * (nn.cpp:198-292) */
+gbopt_status gbopt_net_lagrangian_hessian(const gbopt_net* net,
+                                          const double* x, size_t n,
+                                          const double* lambda, size_t m,
+                                          double* hess, size_t hess_len);
+
+/* Fused evaluation at one point: y (m), J (m*n), H (n*n) from one forward
+ * pass.  Any of y / jac / hess may be NULL when not wanted (its length is
+ * then ignored).  lambda may be NULL only when hess is NULL. */
+gbopt_status gbopt_net_oracle(const gbopt_net* net, const double* x,
+                              size_t n, const double* lambda, size_t m,
+                              double* y, double* jac, double* hess);
+
+/* Batched fused evaluation of B independent points with the shared
+ * weights: X is B x n, Lambda is B x m (row-major), outputs Y (B x m),
+ * J (B x m x n), H (B x n x n).  Output pointers may be NULL. */
+gbopt_status gbopt_net_oracle_batched(const gbopt_net* net, size_t batch,
+                                      const double* X, size_t n,
+                                      const double* Lambda, size_t m,
+                                      double* Y, double* J, double* H);
+
+/* Same as gbopt_net_oracle_batched on DEVICE pointers of the bound device,
+ * enqueued on `stream` (a cudaStream_t, or NULL for the legacy default
+ * stream) and NOT synchronised: the caller orders work on `stream`.  This
+ * is the entry the multi-GPU driver uses so results can be gathered with
+ * NCCL without a host round trip. */
+gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net,
+                                             size_t batch, const double* dX,
+                                             size_t n, const double* dLambda,
+                                             size_t m, double* dY, double* dJ,
+                                             double* dH, void* stream);
+
+/* Number of kernels the most recent oracle call on this handle launched
+ * (graph replays count their kernel nodes). */
+int64_t gbopt_net_last_launch_count(const gbopt_net* net);
+
+/* Enables/disables CUDA-graph capture of the oracle sequence (default on). */
+gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* GBOPT_B200_H */

@@ -1,0 +1,332 @@
+// C ABI of gbopt_b200 (include/gbopt_b200.h).
+//
+// Conventions restated from the reference C interface (proj/src/capi.cpp):
+// status mapping most-derived-first (capi.cpp:37-59), `guarded` so no
+// exception crosses the ABI and the thread-local message is set or cleared
+// (capi.cpp:61-74), argument checks before any work (capi.cpp:163-172).
+#include "gbopt_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device_net.hpp"
+#include "net.hpp"
+
+struct gbopt_net {
+  std::unique_ptr<gbb::Net> net;
+};
+
+struct gbopt_prng {
+  gbb::Prng rng;
+};
+
+namespace {
+
+thread_local std::string t_last_error;
+
+gbopt_status to_status(const std::exception_ptr& ep) noexcept {
+  try {
+    std::rethrow_exception(ep);
+  } catch (const gbb::FormatError&) {
+    return GBOPT_ERR_FORMAT;
+  } catch (const gbb::DimensionError&) {
+    return GBOPT_ERR_DIMENSION;
+  } catch (const gbb::TruncatedError&) {
+    return GBOPT_ERR_TRUNCATED;
+  } catch (const gbb::IoError&) {
+    return GBOPT_ERR_IO;
+  } catch (const gbb::RangeError&) {
+    return GBOPT_ERR_RANGE;
+  } catch (const gbb::NumericError&) {
+    return GBOPT_ERR_NUMERIC;
+  } catch (const gbb::StructuralError&) {
+    return GBOPT_ERR_STRUCTURAL;
+  } catch (const gbb::DeviceError&) {
+    return GBOPT_ERR_DEVICE;
+  } catch (const std::bad_alloc&) {
+    return GBOPT_ERR_INTERNAL;
+  } catch (...) {
+    return GBOPT_ERR_INTERNAL;
+  }
+}
+
+template <typename F>
+gbopt_status guarded(F&& body) noexcept {
+  try {
+    body();
+    t_last_error.clear();
+    return GBOPT_OK;
+  } catch (const std::exception& e) {
+    t_last_error = e.what();
+    return to_status(std::current_exception());
+  } catch (...) {
+    t_last_error = "unknown failure";
+    return GBOPT_ERR_INTERNAL;
+  }
+}
+
+gbopt_status fail_argument(const char* msg) noexcept {
+  t_last_error = msg;
+  return GBOPT_ERR_ARGUMENT;
+}
+
+bool dims_ok(const gbopt_net* net, size_t n, size_t m) {
+  return static_cast<int64_t>(n) == net->net->input_dim() && static_cast<int64_t>(m) == net->net->output_dim();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gbopt_last_error(void) { return t_last_error.c_str(); }
+
+const char* gbopt_version(void) { return "gbopt_b200 1.0 sm_100a"; }
+
+int gbopt_device_count(void) { return gbb::device_count(); }
+
+/* ---- prng --------------------------------------------------------------- */
+
+gbopt_status gbopt_prng_new(uint64_t seed, gbopt_prng** out) {
+  if (!out) return fail_argument("gbopt_prng_new: out must be non-null");
+  return guarded([&] { *out = new gbopt_prng{gbb::Prng(seed)}; });
+}
+
+void gbopt_prng_free(gbopt_prng* rng) { delete rng; }
+
+gbopt_status gbopt_prng_raw(gbopt_prng* rng, uint64_t* buf, size_t n) {
+  if (!rng || (!buf && n)) return fail_argument("gbopt_prng_raw: null argument");
+  return guarded([&] {
+    for (size_t i = 0; i < n; ++i) buf[i] = rng->rng.raw();
+  });
+}
+
+gbopt_status gbopt_prng_uniform(gbopt_prng* rng, double lo, double hi, double* buf, size_t n) {
+  if (!rng || (!buf && n)) return fail_argument("gbopt_prng_uniform: null argument");
+  return guarded([&] {
+    for (size_t i = 0; i < n; ++i) buf[i] = rng->rng.uniform(lo, hi);
+  });
+}
+
+gbopt_status gbopt_prng_normal(gbopt_prng* rng, double mean, double stddev, double* buf, size_t n) {
+  if (!rng || (!buf && n)) return fail_argument("gbopt_prng_normal: null argument");
+  return guarded([&] {
+    for (size_t i = 0; i < n; ++i) buf[i] = rng->rng.normal(mean, stddev);
+  });
+}
+
+/* ---- networks ----------------------------------------------------------- */
+
+gbopt_status gbopt_net_load(const char* path, gbopt_net** out) {
+  if (path == nullptr || out == nullptr) return fail_argument("gbopt_net_load: path and out must be non-null");
+  return guarded([&] {
+    auto h = std::make_unique<gbopt_net>();
+    h->net = gbb::load_weights(path);
+    *out = h.release();
+  });
+}
+
+gbopt_status gbopt_net_save(const gbopt_net* net, const char* path) {
+  if (net == nullptr || path == nullptr) return fail_argument("gbopt_net_save: net and path must be non-null");
+  return guarded([&] { gbb::save_weights(*net->net, path); });
+}
+
+gbopt_status gbopt_net_random(const int64_t* widths, size_t n_widths, const char* hidden_activation,
+                              const char* final_activation, uint64_t seed, gbopt_net** out) {
+  if (widths == nullptr || out == nullptr || hidden_activation == nullptr || final_activation == nullptr)
+    return fail_argument("gbopt_net_random: pointer arguments must be non-null");
+  return guarded([&] {
+    std::vector<int64_t> w(widths, widths + n_widths);
+    auto h = std::make_unique<gbopt_net>();
+    h->net = gbb::random_net(w, gbb::act_from_name(hidden_activation), gbb::act_from_name(final_activation), seed);
+    *out = h.release();
+  });
+}
+
+gbopt_status gbopt_net_random_ex(gbopt_prng* rng, const int64_t* widths, size_t n_widths, int hidden_activation,
+                                 int final_activation, int init, double bias_lo, double bias_hi, gbopt_net** out) {
+  if (rng == nullptr || widths == nullptr || out == nullptr)
+    return fail_argument("gbopt_net_random_ex: pointer arguments must be non-null");
+  if (hidden_activation < 0 || hidden_activation > gbb::kMaxActCode || final_activation < 0 ||
+      final_activation > gbb::kMaxActCode)
+    return fail_argument("gbopt_net_random_ex: invalid activation code");
+  return guarded([&] {
+    std::vector<int64_t> w(widths, widths + n_widths);
+    auto h = std::make_unique<gbopt_net>();
+    h->net = gbb::random_net_ex(rng->rng, w, hidden_activation, final_activation, init, bias_lo, bias_hi);
+    *out = h.release();
+  });
+}
+
+gbopt_status gbopt_net_from_layers(size_t n_layers, const int64_t* widths, const int32_t* activations,
+                                   const double* const* weights, const double* const* biases, gbopt_net** out) {
+  if (out == nullptr || (n_layers > 0 && (widths == nullptr || activations == nullptr || weights == nullptr ||
+                                          biases == nullptr)))
+    return fail_argument("gbopt_net_from_layers: pointer arguments must be non-null");
+  for (size_t l = 0; l < n_layers; ++l)
+    if (weights[l] == nullptr || biases[l] == nullptr)
+      return fail_argument("gbopt_net_from_layers: null layer buffer");
+  return guarded([&] {
+    std::vector<gbb::HostLayer> layers(n_layers);
+    for (size_t l = 0; l < n_layers; ++l) {
+      gbb::HostLayer& lay = layers[l];
+      lay.rows = widths[l + 1];
+      lay.cols = widths[l];
+      lay.act = activations[l];
+      if (lay.rows <= 0 || lay.cols <= 0)
+        throw gbb::StructuralError("NeuralNet: layer " + std::to_string(l) + " has an empty weight matrix");
+      lay.w.assign(weights[l], weights[l] + lay.rows * lay.cols);
+      lay.b.assign(biases[l], biases[l] + lay.rows);
+    }
+    auto h = std::make_unique<gbopt_net>();
+    h->net = std::make_unique<gbb::Net>(std::move(layers));
+    *out = h.release();
+  });
+}
+
+void gbopt_net_free(gbopt_net* net) {
+  if (!net) return;
+  try {
+    delete net;
+  } catch (...) {
+  }
+}
+
+int64_t gbopt_net_input_dim(const gbopt_net* net) { return net == nullptr ? 0 : net->net->input_dim(); }
+int64_t gbopt_net_output_dim(const gbopt_net* net) { return net == nullptr ? 0 : net->net->output_dim(); }
+int64_t gbopt_net_param_count(const gbopt_net* net) { return net == nullptr ? 0 : net->net->param_count(); }
+int64_t gbopt_net_layer_count(const gbopt_net* net) { return net == nullptr ? 0 : net->net->layer_count(); }
+
+gbopt_status gbopt_net_layer_info(const gbopt_net* net, int64_t l, int64_t* rows, int64_t* cols,
+                                  int32_t* activation) {
+  if (net == nullptr) return fail_argument("gbopt_net_layer_info: net must be non-null");
+  if (l < 0 || l >= net->net->layer_count()) return fail_argument("gbopt_net_layer_info: layer index out of range");
+  return guarded([&] {
+    const auto& lay = net->net->layer(l);
+    if (rows) *rows = lay.rows;
+    if (cols) *cols = lay.cols;
+    if (activation) *activation = lay.act;
+  });
+}
+
+gbopt_status gbopt_net_layer_copy(const gbopt_net* net, int64_t l, double* w, size_t w_len, double* b,
+                                  size_t b_len) {
+  if (net == nullptr) return fail_argument("gbopt_net_layer_copy: net must be non-null");
+  if (l < 0 || l >= net->net->layer_count()) return fail_argument("gbopt_net_layer_copy: layer index out of range");
+  const auto& lay = net->net->layer(l);
+  if ((w && static_cast<int64_t>(w_len) != lay.rows * lay.cols) || (b && static_cast<int64_t>(b_len) != lay.rows))
+    return fail_argument("gbopt_net_layer_copy: buffer lengths do not match the layer shape");
+  return guarded([&] {
+    if (w) std::memcpy(w, lay.w.data(), sizeof(double) * lay.w.size());
+    if (b) std::memcpy(b, lay.b.data(), sizeof(double) * lay.b.size());
+  });
+}
+
+gbopt_status gbopt_net_bind_device(gbopt_net* net, int ordinal) {
+  if (net == nullptr) return fail_argument("gbopt_net_bind_device: net must be non-null");
+  if (ordinal < 0) return fail_argument("gbopt_net_bind_device: ordinal must be >= 0");
+  return guarded([&] { net->net->device(ordinal); });
+}
+
+int gbopt_net_device(const gbopt_net* net) { return net == nullptr ? -1 : net->net->bound_ordinal(); }
+
+gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled) {
+  if (net == nullptr) return fail_argument("gbopt_net_set_graphs: net must be non-null");
+  return guarded([&] { net->net->use_graphs = enabled != 0; });
+}
+
+int64_t gbopt_net_last_launch_count(const gbopt_net* net) {
+  if (net == nullptr || net->net->device_if_bound() == nullptr) return 0;
+  return net->net->device_if_bound()->last_launches();
+}
+
+/* ---- oracle calls ------------------------------------------------------- */
+
+gbopt_status gbopt_net_forward(const gbopt_net* net, const double* x, size_t n, double* y, size_t m) {
+  if (net == nullptr || x == nullptr || y == nullptr)
+    return fail_argument("gbopt_net_forward: pointer arguments must be non-null");
+  if (!dims_ok(net, n, m))
+    return fail_argument("gbopt_net_forward: buffer lengths do not match the network dimensions");
+  return guarded([&] {
+    std::vector<double> tmp(m);
+    net->net->device().evaluate_host(1, x, nullptr, tmp.data(), nullptr, nullptr, nullptr);
+    std::memcpy(y, tmp.data(), sizeof(double) * m);
+  });
+}
+
+gbopt_status gbopt_net_jacobian(const gbopt_net* net, const double* x, size_t n, double* jac, size_t jac_len) {
+  if (net == nullptr || x == nullptr || jac == nullptr)
+    return fail_argument("gbopt_net_jacobian: pointer arguments must be non-null");
+  const int64_t m = net->net->output_dim();
+  if (static_cast<int64_t>(n) != net->net->input_dim() || static_cast<int64_t>(jac_len) != m * static_cast<int64_t>(n))
+    return fail_argument("gbopt_net_jacobian: buffer lengths do not match the network dimensions");
+  return guarded([&] {
+    std::vector<double> tmp(jac_len);
+    net->net->device().evaluate_host(1, x, nullptr, nullptr, tmp.data(), nullptr, nullptr);
+    std::memcpy(jac, tmp.data(), sizeof(double) * jac_len);
+  });
+}
+
+gbopt_status gbopt_net_lagrangian_gradient(const gbopt_net* net, const double* x, size_t n, const double* lambda,
+                                           size_t m, double* g, size_t g_len) {
+  if (net == nullptr || x == nullptr || lambda == nullptr || g == nullptr)
+    return fail_argument("gbopt_net_lagrangian_gradient: pointer arguments must be non-null");
+  if (!dims_ok(net, n, m) || g_len != n)
+    return fail_argument("gbopt_net_lagrangian_gradient: buffer lengths do not match the network dimensions");
+  return guarded([&] {
+    std::vector<double> tmp(n);
+    net->net->device().evaluate_host(1, x, lambda, nullptr, nullptr, nullptr, tmp.data());
+    std::memcpy(g, tmp.data(), sizeof(double) * n);
+  });
+}
+
+gbopt_status gbopt_net_lagrangian_hessian(const gbopt_net* net, const double* x, size_t n, const double* lambda,
+                                          size_t m, double* hess, size_t hess_len) {
+  if (net == nullptr || x == nullptr || lambda == nullptr || hess == nullptr)
+    return fail_argument("gbopt_net_lagrangian_hessian: pointer arguments must be non-null");
+  if (!dims_ok(net, n, m) || hess_len != n * n)
+    return fail_argument("gbopt_net_lagrangian_hessian: buffer lengths do not match the network dimensions");
+  return guarded([&] {
+    std::vector<double> tmp(hess_len);
+    net->net->device().evaluate_host(1, x, lambda, nullptr, nullptr, tmp.data(), nullptr);
+    std::memcpy(hess, tmp.data(), sizeof(double) * hess_len);
+  });
+}
+
+gbopt_status gbopt_net_oracle(const gbopt_net* net, const double* x, size_t n, const double* lambda, size_t m,
+                              double* y, double* jac, double* hess) {
+  return gbopt_net_oracle_batched(net, 1, x, n, lambda, m, y, jac, hess);
+}
+
+gbopt_status gbopt_net_oracle_batched(const gbopt_net* net, size_t batch, const double* X, size_t n,
+                                      const double* Lambda, size_t m, double* Y, double* J, double* H) {
+  if (net == nullptr || X == nullptr) return fail_argument("gbopt_net_oracle: net and x must be non-null");
+  if (H != nullptr && Lambda == nullptr) return fail_argument("gbopt_net_oracle: lambda is required for the Hessian");
+  if (!dims_ok(net, n, m)) return fail_argument("gbopt_net_oracle: lengths do not match the network dimensions");
+  if (batch == 0) return fail_argument("gbopt_net_oracle: batch must be positive");
+  if (batch > (1u << 30)) return fail_argument("gbopt_net_oracle: batch too large");
+  return guarded([&] {
+    net->net->device().evaluate_host(static_cast<int>(batch), X, Lambda, Y, J, H, nullptr);
+  });
+}
+
+gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net, size_t batch, const double* dX, size_t n,
+                                             const double* dLambda, size_t m, double* dY, double* dJ, double* dH,
+                                             void* stream) {
+  if (net == nullptr || dX == nullptr) return fail_argument("gbopt_net_oracle_batched_device: null argument");
+  if (dH != nullptr && dLambda == nullptr)
+    return fail_argument("gbopt_net_oracle_batched_device: lambda is required for the Hessian");
+  if (!dims_ok(net, n, m))
+    return fail_argument("gbopt_net_oracle_batched_device: lengths do not match the network dimensions");
+  if (batch == 0) return fail_argument("gbopt_net_oracle_batched_device: batch must be positive");
+  return guarded([&] {
+    net->net->device().evaluate_device(static_cast<int>(batch), dX, dLambda, dY, dJ, dH,
+                                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

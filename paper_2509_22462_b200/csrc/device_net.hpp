@@ -1,0 +1,122 @@
+// Device-resident network (weights in HBM in kernel layout), its workspace
+// and the oracle launch sequence.  See oracle.cu and DESIGN.md.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "net.hpp"
+
+namespace gbb {
+namespace dev {
+struct NtParams;
+}
+
+void cuda_check(cudaError_t e, const char* what);
+int device_count();
+
+// Restores the caller's current device on scope exit.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int ordinal) {
+    if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+    cuda_check(cudaSetDevice(ordinal), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev_ >= 0) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = -1;
+};
+
+struct DevLayer {
+  int64_t rows = 0, cols = 0, ldw = 0;
+  int act = 0;
+  double* w = nullptr;  // [rows][ldw]
+  double* b = nullptr;  // [rows]
+  CUtensorMap tm_w;     // TMA view of w, box 16 x kBN (B operand)
+};
+
+struct Workspace {
+  std::vector<double*> z, y, s1, s2, ybar, gz, d;  // per layer [cap][ld[l]]
+  std::vector<int64_t> ld;
+  int64_t ld_in = 0, ld_lam = 0;
+  double *x = nullptr, *lam = nullptr, *grad = nullptr, *mid = nullptr;
+  int adj_chunks_max = 0;
+  int64_t ld_part = 0;
+  double* adj_part = nullptr;
+  double* t[2] = {nullptr, nullptr};
+  std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer l & 1)
+  int64_t ldh = 0;
+  double* h = nullptr;
+  double* syrk_part = nullptr;
+  int sk_chunks = 0;
+  double *u = nullptr, *sk_part = nullptr;
+  double *y_out = nullptr, *j_out = nullptr, *h_out = nullptr, *g_out = nullptr;
+};
+
+struct Outputs {
+  double* y = nullptr;  // [nb][m]
+  double* j = nullptr;  // [nb][m][n]
+  double* h = nullptr;  // [nb][n][n]
+  double* g = nullptr;  // [nb][n]
+};
+
+class DeviceNet {
+ public:
+  DeviceNet(const Net& net, int ordinal);
+  ~DeviceNet();
+  DeviceNet(const DeviceNet&) = delete;
+  DeviceNet& operator=(const DeviceNet&) = delete;
+
+  int ordinal() const { return ordinal_; }
+  int64_t last_launches() const { return last_launches_; }
+
+  // Host buffers in/out (synchronous).  Any output may be null.
+  void evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess, double* grad);
+  // Device buffers, ordered on `user` stream, asynchronous.
+  void evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
+                       cudaStream_t user);
+
+ private:
+  using GraphKey = std::tuple<int, double*, double*, double*, double*>;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+  };
+
+  void ensure_workspace(int batch);
+  void free_workspace();
+  void drop_graphs();
+  double* ws_alloc(size_t n_doubles);
+  int syrk_split(int points) const;
+  void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
+  void enqueue(cudaStream_t st, int nb, const Outputs& o);
+  void run(cudaStream_t st, int nb, const Outputs& o);
+
+  const Net& net_;
+  int ordinal_ = 0;
+  int sm_count_ = 148;
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
+  int64_t n_ = 0, m_ = 0, L_ = 0, n_pad_ = 0;
+  std::vector<DevLayer> layers_;
+  double* t0_ = nullptr;  // W_0^T [n_pad][ldt0_]
+  int64_t ldt0_ = 0, ldt_ = 0;
+  CUtensorMap tm_t0_a_, tm_t0_b_;
+  int2* syrk_tiles_ = nullptr;
+  int n_syrk_tiles_ = 0;
+  Workspace ws_;
+  int ws_cap_ = 0;
+  std::vector<void*> ws_allocs_;
+  std::map<GraphKey, GraphEntry> graphs_;
+  int64_t launches_ = 0, last_launches_ = 0;
+};
+
+}  // namespace gbb

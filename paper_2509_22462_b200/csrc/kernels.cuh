@@ -1,0 +1,698 @@
+// sm_100a kernels of the FP64 gray-box oracle.
+//
+// The reference computes everything with Eigen on one CPU core
+// (reference src/nn.cpp:113-292).  Here the same quantities are produced by:
+//
+//   fwd_rows_kernel     z_l = W_l y_{l-1} + b_l, epilogue sigma, sigma',
+//                       sigma'' (nn.cpp:43-72, 113-146).  HBM-bound GEMV,
+//                       one warp per weight row, 16-B coalesced loads.
+//   adj_cols_kernel +   ybar_{l-1} = W_l^T (ybar_l .* sigma'_l)
+//   adj_reduce_kernel   (nn.cpp:172-196).  HBM-bound column sums with a
+//                       deterministic split reduction that also emits the
+//                       next layer's gz and d = ybar .* sigma''.
+//   nt_mma_kernel       C = A diag(s) B^T on FP64 DMMA.8x8x4 tensor cores:
+//                       TMA (cp.async.bulk.tensor, 128B swizzle) -> smem
+//                       ring guarded by mbarriers, one producer warp, eight
+//                       consumer warps.  Used for the tangent chain
+//                       T_{l+1} = T_l diag(sigma'_l) W_{l+1}^T (the forward
+//                       tangents of nn.cpp:219-236, transposed) and for the
+//                       Hessian SYRK H += T_l diag(ybar_l .* sigma''_l) T_l^T
+//                       that replaces the reverse-tangent sweep of
+//                       nn.cpp:242-282 (scale applied in registers, the
+//                       scaled copy is never materialised).
+//   skinny_nt_kernel    the final layer's m <= 16 outputs (tall-skinny).
+//   small-K / softmax / symmetrise helpers.
+//
+// Layout conventions:
+//   W_l      row-major [n_l][kp(n_{l-1})], kp(x) = round_up(x, 16)
+//   T_l      dz_l/dx transposed: row j = tangent of input direction j,
+//            [B * n_pad][kp(n_l)], n_pad = round_up(n, 112)
+//   vectors  [B][kp(n_l)], zero padded.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gbb {
+namespace dev {
+
+// ---------------------------------------------------------------------------
+// Tiling constants of the DMMA NT kernel.
+// ---------------------------------------------------------------------------
+constexpr int kBM = 112;              // tile rows  (7 x 16; 784 = 7 x 112)
+constexpr int kBN = 128;              // tile cols
+constexpr int kBK = 16;               // k per stage = one 128-byte swizzle row
+constexpr int kStages = 6;            // smem ring depth
+constexpr int kConsumerWarps = 8;     // 2 (M) x 4 (N)
+constexpr int kWarpM = 56;            // 7 DMMA row blocks
+constexpr int kWarpN = 32;            // 4 DMMA col blocks
+constexpr int kMI = kWarpM / 8;       // 7
+constexpr int kNJ = kWarpN / 8;       // 4
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kABytes = kBM * kBK * 8;  // 14336 (14 x 1024)
+constexpr int kBBytes = kBN * kBK * 8;  // 16384
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+
+__host__ __device__ constexpr int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// Activations: reference nn.cpp:43-72 (+ softplus, builder extension).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void act_eval(int act, double z, double& y, double& d1, double& d2) {
+  switch (act) {
+    case 1: {  // tanh
+      const double t = tanh(z);
+      y = t;
+      d1 = 1.0 - t * t;
+      d2 = -2.0 * t * (1.0 - t * t);
+      return;
+    }
+    case 2: {  // sigmoid = 0.5 tanh(z/2) + 0.5
+      const double s = 0.5 * tanh(0.5 * z) + 0.5;
+      const double sp = s * (1.0 - s);
+      y = s;
+      d1 = sp;
+      d2 = sp * (1.0 - 2.0 * s);
+      return;
+    }
+    case 4: {  // softplus
+      const double s = 0.5 * tanh(0.5 * z) + 0.5;
+      y = fmax(z, 0.0) + log1p(exp(-fabs(z)));
+      d1 = s;
+      d2 = s * (1.0 - s);
+      return;
+    }
+    default:  // linear (softmax rows are finished by softmax_kernel)
+      y = z;
+      d1 = 1.0;
+      d2 = 0.0;
+      return;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier, TMA, DMMA.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+// 2-D tiled TMA load: box lands in smem (128B-swizzled), completion counted
+// on `bar` in bytes.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c_inner,
+                                            int c_outer) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c_inner), "r"(c_outer)
+      : "memory");
+}
+// D = A(8x4, row) * B(4x8, col) + D on the FP64 tensor pipe (DMMA.8x8x4).
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+// Element (r, k) of a 128B-swizzled [rows][16 doubles] TMA box (TMA's
+// SWIZZLE_128B: 16-byte chunk index XOR (row & 7)).  `base` must point into
+// shared memory via the __shared__ array so the compiler emits LDS.
+__device__ __forceinline__ double lds_swz(const char* base, int r, int k) {
+  const int off = r * 128 + ((((k >> 1) ^ (r & 7)) << 4) | ((k & 1) << 3));
+  return *reinterpret_cast<const double*>(base + off);
+}
+
+// ---------------------------------------------------------------------------
+// NT MMA kernel:  C[r][c] (+)= sum_k A[r][k] * s[k] * B[c][k]
+// ---------------------------------------------------------------------------
+enum NtMode : int { kStore = 0, kAccum = 1, kPartial = 2 };
+
+struct NtParams {
+  // Tile enumeration.  For a dense GEMM (tiles == nullptr) the tile id is
+  // decoded as (point, tm, tn) with grouped rasterisation over (tm, tn);
+  // for the SYRK a host-built list gives (tm, tn) per point.
+  const int2* tiles;     // SYRK tile list (tm, tn) or nullptr
+  int n_tiles;           // tiles per point in the list
+  int tiles_m;           // M tiles per point
+  int tiles_n;           // N tiles per point
+  int points;            // batch
+  int split;             // split-K factor (kPartial when > 1)
+  int k_blocks;          // ceil(K / 16)
+  // Operand row offsets (rows of the TMA tensors).
+  int64_t a_point_rows;  // A row offset per point (0 = broadcast)
+  int64_t b_point_rows;  // B row offset per point (0 = shared weights)
+  int b_rows_valid;      // rows of B valid per point (cols of C)
+  int m_rows_valid;      // rows of C valid per point
+  // Per-k scale on B (nullable): s + point * s_stride.
+  const double* scale;
+  int64_t s_stride;
+  // Output.
+  double* c;
+  int64_t c_point_stride;  // elements
+  int64_t ldc;
+  int mode;
+  double* partial;  // [split][points * n_tiles][kBM][kBN] for kPartial
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    nt_mma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const NtParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte alignment for the 128B swizzle, derived from the __shared__
+  // array itself so loads stay in the shared window (LDS, not generic LD).
+  char* smem = reinterpret_cast<char*>(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- decode tile ----
+  int bid = blockIdx.x;
+  const int split_idx = bid % p.split;
+  bid /= p.split;
+  int point, tm, tn;
+  if (p.tiles != nullptr) {
+    point = bid / p.n_tiles;
+    const int2 t = p.tiles[bid % p.n_tiles];
+    tm = t.x;
+    tn = t.y;
+  } else {
+    // grouped raster: GROUP_M consecutive M tiles sweep all N tiles.
+    const int per_point = p.tiles_m * p.tiles_n;
+    point = bid / per_point;
+    const int local = bid % per_point;
+    constexpr int kGroupM = 8;
+    const int group = local / (kGroupM * p.tiles_n);
+    const int first_m = group * kGroupM;
+    const int gsize = min(p.tiles_m - first_m, kGroupM);
+    const int in_group = local % (kGroupM * p.tiles_n);
+    tm = first_m + in_group % gsize;
+    tn = in_group / gsize;
+  }
+  const int kb_begin = static_cast<int>((static_cast<int64_t>(p.k_blocks) * split_idx) / p.split);
+  const int kb_end = static_cast<int>((static_cast<int64_t>(p.k_blocks) * (split_idx + 1)) / p.split);
+  const int nkb = kb_end - kb_begin;
+
+  const int a_row0 = static_cast<int>(p.a_point_rows * point) + tm * kBM;
+  const int b_row0 = static_cast<int>(p.b_point_rows * point) + tn * kBN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ===== producer warp: one elected lane issues the TMA ring =====
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
+        char* sa = smem + s * kStageBytes;
+        char* sb = sa + kABytes;
+        mbar_arrive_expect_tx(&full[s], kStageBytes);
+        const int kc = (kb_begin + i) * kBK;
+        tma_load_2d(sa, &tmA, &full[s], kc, a_row0);
+        tma_load_2d(sb, &tmB, &full[s], kc, b_row0);
+      }
+    }
+    return;
+  }
+
+  // ===== consumer warps =====
+  const int wm = warp >> 2;  // 0..1
+  const int wn = warp & 3;   // 0..3
+  const int g = lane >> 2;   // DMMA group (row of A / col of B)
+  const int t = lane & 3;    // thread in group (k)
+  double acc[kMI][kNJ][2];
+#pragma unroll
+  for (int i = 0; i < kMI; ++i)
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const double* sp = p.scale ? p.scale + p.s_stride * point : nullptr;
+  const int ra = wm * kWarpM + g;  // base row in A box
+  const int rb = wn * kWarpN + g;  // base row in B box
+
+  double sc_next[4];
+  if (sp && nkb > 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sc_next[q] = __ldg(sp + kb_begin * kBK + 4 * q + t);
+  }
+  for (int i = 0; i < nkb; ++i) {
+    const int s = i % kStages;
+    double sc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sc[q] = sp ? sc_next[q] : 1.0;
+    if (sp && i + 1 < nkb) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sc_next[q] = __ldg(sp + (kb_begin + i + 1) * kBK + 4 * q + t);
+    }
+    mbar_wait(&full[s], (i / kStages) & 1);
+    const char* sa = smem + s * kStageBytes;
+    const char* sb = sa + kABytes;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * q + t;
+      double a[kMI], b[kNJ];
+#pragma unroll
+      for (int mi = 0; mi < kMI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
+#pragma unroll
+      for (int nj = 0; nj < kNJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc[q];
+#pragma unroll
+      for (int mi = 0; mi < kMI; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < kNJ; ++nj) dmma884(acc[mi][nj], a[mi], b[nj]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---- epilogue: thread holds C[8mi+g][8nj+2t .. +1] of its warp tile ----
+  if (p.mode == kPartial) {
+    double* out = p.partial + ((static_cast<int64_t>(split_idx) * p.points * p.n_tiles +
+                                static_cast<int64_t>(blockIdx.x / p.split)) *
+                               kBM * kBN);
+#pragma unroll
+    for (int mi = 0; mi < kMI; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < kNJ; ++nj) {
+        const int r = wm * kWarpM + 8 * mi + g;
+        const int cc = wn * kWarpN + 8 * nj + 2 * t;
+        *reinterpret_cast<double2*>(out + r * kBN + cc) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+      }
+    return;
+  }
+  double* cbase = p.c + p.c_point_stride * point;
+#pragma unroll
+  for (int mi = 0; mi < kMI; ++mi) {
+    const int r = tm * kBM + wm * kWarpM + 8 * mi + g;
+    if (r >= p.m_rows_valid) continue;
+#pragma unroll
+    for (int nj = 0; nj < kNJ; ++nj) {
+      const int cc = tn * kBN + wn * kWarpN + 8 * nj + 2 * t;
+      double* dst = cbase + static_cast<int64_t>(r) * p.ldc + cc;
+      if (cc + 1 < p.b_rows_valid) {
+        double2 v = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+        if (p.mode == kAccum) {
+          const double2 o = *reinterpret_cast<const double2*>(dst);
+          v.x += o.x;
+          v.y += o.y;
+        }
+        *reinterpret_cast<double2*>(dst) = v;
+      } else if (cc < p.b_rows_valid) {
+        dst[0] = (p.mode == kAccum ? dst[0] : 0.0) + acc[mi][nj][0];
+      }
+    }
+  }
+}
+
+// Sum split-K SYRK partials (fixed order: deterministic) into H_ws.
+__global__ void syrk_partial_reduce_kernel(const double* __restrict__ partial, const int2* __restrict__ tiles,
+                                           int n_tiles, int points, int split, double* __restrict__ h,
+                                           int64_t h_point_stride, int64_t ldh, int n_valid) {
+  const int tile_global = blockIdx.y;  // point * n_tiles + tile
+  const int point = tile_global / n_tiles;
+  const int2 t = tiles[tile_global % n_tiles];
+  const int64_t tile_elems = static_cast<int64_t>(kBM) * kBN;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kBM * kBN; e += gridDim.x * blockDim.x) {
+    const int r = t.x * kBM + e / kBN;
+    const int c = t.y * kBN + e % kBN;
+    if (r >= n_valid || c >= n_valid) continue;
+    double sum = 0.0;
+    for (int s = 0; s < split; ++s)
+      sum += partial[(static_cast<int64_t>(s) * points * n_tiles + tile_global) * tile_elems + e];
+    h[h_point_stride * point + static_cast<int64_t>(r) * ldh + c] += sum;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Forward GEMV chain: z = W y + b with the activation epilogue.
+// One warp per output row; NB points per pass, y chunk staged in smem.
+// ---------------------------------------------------------------------------
+constexpr int kFwdWarps = 8;
+
+template <int NB>
+__global__ void __launch_bounds__(kFwdWarps * 32)
+    fwd_rows_kernel(const double* __restrict__ w, int64_t ldw, const double* __restrict__ bias, int rows, int k_dim,
+                    const double* __restrict__ yin, int64_t ld_in, int nb, int act, double* __restrict__ z_out,
+                    double* __restrict__ y_out, double* __restrict__ s1_out, double* __restrict__ s2_out,
+                    int64_t ld_out) {
+  constexpr int kFwdKChunk = 4096 / NB;  // 32 KB of staged inputs
+  __shared__ __align__(16) double ys[NB][kFwdKChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kFwdWarps + warp;
+  const int p0 = blockIdx.y * NB;
+  double acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = 0.0;
+  const double* wr = w + static_cast<int64_t>(row < rows ? row : 0) * ldw;
+  for (int k0 = 0; k0 < k_dim; k0 += kFwdKChunk) {
+    const int kc = min(kFwdKChunk, k_dim - k0);
+    const int kc2 = (kc + 1) & ~1;
+    __syncthreads();
+    for (int b = 0; b < NB; ++b) {
+      const bool live = (p0 + b) < nb;
+      for (int k = threadIdx.x; k < kc2; k += blockDim.x)
+        ys[b][k] = (live && k < kc) ? yin[static_cast<int64_t>(p0 + b) * ld_in + k0 + k] : 0.0;
+    }
+    __syncthreads();
+    if (row < rows) {
+      // weight rows are padded to a multiple of 16 doubles with zeros, so
+      // reading the (kc rounded to 2) tail is safe.
+#pragma unroll 4
+      for (int k = 2 * lane; k < kc2; k += 64) {
+        const double2 wv = __ldg(reinterpret_cast<const double2*>(wr + k0 + k));
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const double2 yv = *reinterpret_cast<const double2*>(&ys[b][k]);
+          acc[b] = fma(wv.x, yv.x, acc[b]);
+          acc[b] = fma(wv.y, yv.y, acc[b]);
+        }
+      }
+    }
+  }
+  if (row >= rows) return;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    double v = acc[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc[b] = v;
+  }
+  if (lane < NB && p0 + lane < nb) {
+    double zz = 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (b == lane) zz = acc[b];
+    zz += bias[row];
+    const int64_t o = static_cast<int64_t>(p0 + lane) * ld_out + row;
+    double yy, d1, d2;
+    act_eval(act, zz, yy, d1, d2);
+    z_out[o] = zz;
+    y_out[o] = yy;
+    s1_out[o] = d1;
+    s2_out[o] = d2;
+  }
+}
+
+// Softmax over each point's final-layer row: nn.cpp:12-17.
+__global__ void softmax_kernel(const double* __restrict__ z, double* __restrict__ y, int m, int64_t ld, int nb) {
+  const int pt = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pt >= nb) return;
+  const double* zr = z + ld * pt;
+  double mx = -INFINITY;
+  for (int i = lane; i < m; i += 32) mx = fmax(mx, zr[i]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double sum = 0.0;
+  for (int i = lane; i < m; i += 32) sum += exp(zr[i] - mx);
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  // deterministic: each lane recomputes its own entries with the same sum
+  for (int i = lane; i < m; i += 32) y[ld * pt + i] = exp(zr[i] - mx) / sum;
+}
+
+// ---------------------------------------------------------------------------
+// Adjoint seed at the output layer: ybar_L = lambda.
+//   elementwise: gz = lambda .* s1, d = lambda .* s2
+//   softmax:     gz = y .* lambda - (y^T lambda) y ;  d unused (dense M)
+// One warp per point.
+// ---------------------------------------------------------------------------
+__global__ void adj_seed_kernel(const double* __restrict__ lam, int64_t ld_lam, const double* __restrict__ y,
+                                const double* __restrict__ s1, const double* __restrict__ s2, int64_t ld, int m,
+                                int nb, int softmax, double* __restrict__ gz, double* __restrict__ d,
+                                double* __restrict__ mid, int64_t ld_mid) {
+  const int pt = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pt >= nb) return;
+  const double* lr = lam + ld_lam * pt;
+  if (!softmax) {
+    for (int i = lane; i < m; i += 32) {
+      gz[ld * pt + i] = lr[i] * s1[ld * pt + i];
+      d[ld * pt + i] = lr[i] * s2[ld * pt + i];
+    }
+    return;
+  }
+  const double* yr = y + ld * pt;
+  double s = 0.0;
+  for (int i = lane; i < m; i += 32) s += yr[i] * lr[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int i = lane; i < m; i += 32) gz[ld * pt + i] = yr[i] * lr[i] - s * yr[i];
+  // M = sum_i lambda_i Hess(softmax_i):
+  //   M_jk = delta_jk y_j (lambda_j - s) - y_j y_k (lambda_j + lambda_k - 2 s)
+  double* mr = mid + ld_mid * pt;
+  for (int e = lane; e < m * m; e += 32) {
+    const int j = e / m, k = e % m;
+    double v = -yr[j] * yr[k] * (lr[j] + lr[k] - 2.0 * s);
+    if (j == k) v += yr[j] * (lr[j] - s);
+    mr[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Adjoint GEMV^T: partial[c][b][k] = sum_{i in chunk c} W[i][k] gz[b][i].
+// Threads own two adjacent k (16-B loads, coalesced along the row).
+// ---------------------------------------------------------------------------
+constexpr int kAdjThreads = 256;
+constexpr int kAdjRows = 128;
+
+template <int NB>
+__global__ void __launch_bounds__(kAdjThreads)
+    adj_cols_kernel(const double* __restrict__ w, int64_t ldw, int rows, int k_dim, const double* __restrict__ gz,
+                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part) {
+  __shared__ double gs[NB][kAdjRows];
+  const int k = 2 * (blockIdx.x * kAdjThreads + threadIdx.x);
+  const int r0 = blockIdx.y * kAdjRows;
+  const int nr = min(kAdjRows, rows - r0);
+  for (int e = threadIdx.x; e < NB * kAdjRows; e += kAdjThreads) {
+    const int b = e / kAdjRows, i = e % kAdjRows;
+    gs[b][i] = (p0 + b < nb && i < nr) ? gz[static_cast<int64_t>(p0 + b) * ld_gz + r0 + i] : 0.0;
+  }
+  __syncthreads();
+  if (k >= k_dim) return;
+  double a0[NB], a1[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0;
+  const double* wp = w + static_cast<int64_t>(r0) * ldw + k;
+#pragma unroll 8
+  for (int i = 0; i < nr; ++i) {
+    const double2 wv = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw));
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      a0[b] = fma(wv.x, gs[b][i], a0[b]);
+      a1[b] = fma(wv.y, gs[b][i], a1[b]);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (p0 + b >= nb) break;
+    double* o = partial + (static_cast<int64_t>(blockIdx.y) * nb + p0 + b) * ld_part + k;
+    o[0] = a0[b];
+    if (k + 1 < k_dim) o[1] = a1[b];
+  }
+}
+
+// ybar[b][k] = sum_c partial[c][b][k] (fixed order), then
+// gz = ybar .* s1 and d = ybar .* s2 for the layer below (nn.cpp:188-193).
+// When s1 == nullptr only ybar is written (the input-gradient).
+__global__ void adj_reduce_kernel(const double* __restrict__ partial, int chunks, int64_t ld_part, int k_dim, int nb,
+                                  const double* __restrict__ s1, const double* __restrict__ s2, int64_t ld,
+                                  double* __restrict__ ybar, double* __restrict__ gz, double* __restrict__ d) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(nb) * k_dim) return;
+  const int b = static_cast<int>(e / k_dim), k = static_cast<int>(e % k_dim);
+  double sum = 0.0;
+  for (int c = 0; c < chunks; ++c) sum += partial[(static_cast<int64_t>(c) * nb + b) * ld_part + k];
+  const int64_t o = static_cast<int64_t>(b) * ld + k;
+  ybar[o] = sum;
+  if (s1) {
+    gz[o] = sum * s1[o];
+    d[o] = sum * s2[o];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Final layer with m <= 16 outputs (tall-skinny NT product):
+//   partial[c][b][j][i] = sum_{k in chunk c} A[b][j][k] s[b][k] W[i][k]
+// A rows j < n_valid of each point; W is the last layer (m x K, row-major).
+// ---------------------------------------------------------------------------
+constexpr int kSkMB = 16;
+constexpr int kSkRows = 16;    // rows j per CTA (2 per warp)
+constexpr int kSkKChunk = 256;
+
+__global__ void __launch_bounds__(256)
+    skinny_nt_kernel(const double* __restrict__ a, int64_t lda, int64_t a_point_rows, int n_valid,
+                     const double* __restrict__ scale, int64_t s_stride, const double* __restrict__ w, int64_t ldw,
+                     int m, int k_dim, double* __restrict__ partial) {
+  __shared__ __align__(16) double ws[kSkMB][kSkKChunk];
+  const int point = blockIdx.z;
+  const int chunk = blockIdx.y;
+  const int k0 = chunk * kSkKChunk;
+  const int kc = min(kSkKChunk, k_dim - k0);
+  const double* sp = scale ? scale + s_stride * point : nullptr;
+  for (int e = threadIdx.x; e < kSkMB * kSkKChunk; e += blockDim.x) {
+    const int i = e / kSkKChunk, k = e % kSkKChunk;
+    double v = 0.0;
+    if (i < m && k < kc) {
+      v = w[static_cast<int64_t>(i) * ldw + k0 + k];
+      if (sp) v *= sp[k0 + k];
+    }
+    ws[i][k] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * kSkRows + warp * 2;
+  double acc[2][kSkMB];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int i = 0; i < kSkMB; ++i) acc[r][i] = 0.0;
+  const double* a0 = a + (a_point_rows * point + j0) * lda + k0;
+  const bool live0 = j0 < n_valid, live1 = j0 + 1 < n_valid;
+  for (int k = 2 * lane; k < kc; k += 64) {
+    const double2 x0 = live0 ? *reinterpret_cast<const double2*>(a0 + k) : make_double2(0.0, 0.0);
+    const double2 x1 = live1 ? *reinterpret_cast<const double2*>(a0 + lda + k) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < kSkMB; ++i) {
+      const double2 wv = *reinterpret_cast<const double2*>(&ws[i][k]);
+      acc[0][i] = fma(x0.x, wv.x, fma(x0.y, wv.y, acc[0][i]));
+      acc[1][i] = fma(x1.x, wv.x, fma(x1.y, wv.y, acc[1][i]));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int i = 0; i < kSkMB; ++i) {
+      double v = acc[r][i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[r][i] = v;
+    }
+  // lane i writes output i of both rows: partial layout [chunk][point][rows_pad][16]
+  const int64_t rows_pad = static_cast<int64_t>(gridDim.x) * kSkRows;
+  const int64_t base = (static_cast<int64_t>(chunk) * gridDim.z + point) * rows_pad;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < kSkMB; ++i)
+      if (i == lane) v = acc[r][i];
+    if (lane < kSkMB) partial[(base + j0 + r) * kSkMB + lane] = v;
+  }
+}
+
+// U[b][j][i] = sum_c partial[c][b][j][i]   (deterministic order)
+__global__ void skinny_reduce_kernel(const double* __restrict__ partial, int chunks, int nb, int rows_pad, int m,
+                                     double* __restrict__ u) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per_point = static_cast<int64_t>(rows_pad) * kSkMB;
+  if (e >= per_point * nb) return;
+  double sum = 0.0;
+  for (int c = 0; c < chunks; ++c) sum += partial[static_cast<int64_t>(c) * nb * per_point + e];
+  u[e] = sum;
+}
+
+// J[b][i][j] from U = dz_L/dx^T (rows j, cols i, pitch ldu):
+//   elementwise final: J_ij = s1_i U_ji
+//   softmax final:     J_ij = y_i U_ji - y_i sum_k y_k U_jk
+__global__ void jacobian_out_kernel(const double* __restrict__ u, int64_t ldu, int64_t u_point_rows,
+                                    const double* __restrict__ s1, const double* __restrict__ y, int64_t ld, int n,
+                                    int m, int nb, int softmax, double* __restrict__ jac) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(nb) * n) return;
+  const int b = static_cast<int>(e / n), j = static_cast<int>(e % n);
+  const double* ur = u + (u_point_rows * b + j) * ldu;
+  double* jb = jac + static_cast<int64_t>(b) * m * n;
+  if (!softmax) {
+    for (int i = 0; i < m; ++i) jb[static_cast<int64_t>(i) * n + j] = s1[ld * b + i] * ur[i];
+  } else {
+    const double* yr = y + ld * b;
+    double dot = 0.0;
+    for (int k = 0; k < m; ++k) dot += yr[k] * ur[k];
+    for (int i = 0; i < m; ++i) jb[static_cast<int64_t>(i) * n + j] = yr[i] * ur[i] - yr[i] * dot;
+  }
+}
+
+// Final-layer curvature with a small K = m:
+//   H[b][r][c] += sum_{i,k} U[r][i] M[i][k] U[c][k]
+// with M = diag(d) (elementwise) or the dense softmax middle.  Only the
+// lower triangle (c <= r) is needed; the symmetrise pass mirrors it.
+__global__ void small_k_syrk_kernel(const double* __restrict__ u, int64_t ldu, int64_t u_point_rows,
+                                    const double* __restrict__ dvec, int64_t ld, const double* __restrict__ mid,
+                                    int64_t ld_mid, int n, int m, int nb, double* __restrict__ h,
+                                    int64_t h_point_stride, int64_t ldh) {
+  const int b = blockIdx.z;
+  const int r = blockIdx.y * blockDim.y + threadIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || c >= n || c > r || b >= nb) return;
+  const double* ur = u + (u_point_rows * b + r) * ldu;
+  const double* uc = u + (u_point_rows * b + c) * ldu;
+  double sum = 0.0;
+  if (mid == nullptr) {
+    const double* dv = dvec + ld * b;
+    for (int i = 0; i < m; ++i) sum += ur[i] * dv[i] * uc[i];
+  } else {
+    const double* mm = mid + ld_mid * b;
+    for (int i = 0; i < m; ++i) {
+      double t = 0.0;
+      for (int k = 0; k < m; ++k) t += mm[i * m + k] * uc[k];
+      sum += ur[i] * t;
+    }
+  }
+  h[h_point_stride * b + static_cast<int64_t>(r) * ldh + c] += sum;
+}
+
+// H_out[b][r][c] = H_ws[b][max(r,c)][min(r,c)]: exactly symmetric output.
+__global__ void symmetrize_out_kernel(const double* __restrict__ hws, int64_t h_point_stride, int64_t ldh, int n,
+                                      int nb, double* __restrict__ out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  if (e >= nn * nb) return;
+  const int b = static_cast<int>(e / nn);
+  const int r = static_cast<int>((e % nn) / n), c = static_cast<int>(e % n);
+  const int hi = r > c ? r : c, lo = r > c ? c : r;
+  out[e] = hws[h_point_stride * b + static_cast<int64_t>(hi) * ldh + lo];
+}
+
+// Strided copy of a [rows][cols] block (pitch src -> pitch dst).
+__global__ void copy_rows_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
+                                 int rows, int cols) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(rows) * cols) return;
+  const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
+  dst[static_cast<int64_t>(r) * ldd + c] = src[static_cast<int64_t>(r) * lds + c];
+}
+
+}  // namespace dev
+}  // namespace gbb

@@ -1,0 +1,607 @@
+// Device-resident network and the oracle launch sequence.
+//
+// One oracle evaluation at B points (shared weights) =
+//   1. forward chain       z_l, y_l, sigma'_l, sigma''_l        (fwd_rows)
+//   2. adjoint chain       ybar_l, gz_l, d_l = ybar_l .* sigma''_l (adj_*)
+//   3. tangent chain       T_0 = W_0^T (constant, uploaded once)
+//                          T_{l+1} = T_l diag(sigma'_l) W_{l+1}^T (nt_mma)
+//      Hessian            H += T_l diag(d_l) T_l^T  per nonlinear layer
+//                          (nt_mma in SYRK mode, lower tiles)
+//   4. final layer         U = dz_L/dx^T (skinny or nt_mma), J, curvature
+//   5. symmetrise          H_out = mirror(lower(H_ws))
+//
+// This restates the reference's lagrangian_hessian (src/nn.cpp:198-292)
+// as H = sum_l (dz_l/dx)^T diag(ybar_l .* sigma''(z_l)) (dz_l/dx) (+ the
+// dense softmax middle on a softmax output layer): the same second
+// derivative, computed as a SYRK on the forward tangents instead of a
+// second (reverse) tangent sweep -- about half the flops, and the
+// asymmetry check of nn.cpp:284-290 is satisfied by construction.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "device_net.hpp"
+#include "kernels.cuh"
+#include "net.hpp"
+
+namespace gbb {
+
+using dev::kBK;
+using dev::kBM;
+using dev::kBN;
+using dev::round_up;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw DeviceError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw DeviceError("cuTensorMapEncodeTiled is unavailable (driver too old?)");
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D FP64 tensor [rows][cols] with row pitch `pitch` doubles; box 16 x box_rows,
+// 128-byte swizzle, out-of-bounds elements read as zero.
+CUtensorMap make_tmap(const double* base, int64_t cols, int64_t rows, int64_t pitch, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch * 8)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// DeviceNet: weights in HBM, workspace, launch sequence.
+// ---------------------------------------------------------------------------
+DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw DeviceError("no CUDA device available");
+  }
+  if (ordinal < 0 || ordinal >= count) throw DeviceError("CUDA device ordinal out of range");
+  DeviceGuard g(ordinal_);
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, ordinal_));
+  if (prop.major != 10) throw DeviceError(std::string("gbopt_b200 needs an sm_100 (B200) device, found ") + prop.name);
+  sm_count_ = prop.multiProcessorCount;
+  CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
+  CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
+
+  n_ = net.input_dim();
+  m_ = net.output_dim();
+  L_ = net.layer_count();
+  n_pad_ = round_up(n_, kBM);
+  const auto& hl = net.layers();
+  for (int64_t l = 0; l < L_; ++l) {
+    const HostLayer& h = hl[static_cast<size_t>(l)];
+    DevLayer d;
+    d.rows = h.rows;
+    d.cols = h.cols;
+    d.act = h.act;
+    d.ldw = round_up(h.cols, 16);
+    CK(cudaMalloc(&d.w, sizeof(double) * d.rows * d.ldw));
+    CK(cudaMemset(d.w, 0, sizeof(double) * d.rows * d.ldw));
+    CK(cudaMemcpy2D(d.w, sizeof(double) * d.ldw, h.w.data(), sizeof(double) * h.cols, sizeof(double) * h.cols,
+                    d.rows, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&d.b, sizeof(double) * d.rows));
+    CK(cudaMemcpy(d.b, h.b.data(), sizeof(double) * d.rows, cudaMemcpyHostToDevice));
+    d.tm_w = make_tmap(d.w, d.cols, d.rows, d.ldw, kBN);
+    layers_.push_back(d);
+  }
+  // T_0 = W_0^T, [n_pad][kp(n_1)], padded rows zero.
+  const HostLayer& h0 = hl[0];
+  ldt0_ = round_up(h0.rows, 16);
+  std::vector<double> t0(static_cast<size_t>(n_pad_ * ldt0_), 0.0);
+  for (int64_t i = 0; i < h0.rows; ++i)
+    for (int64_t j = 0; j < h0.cols; ++j) t0[static_cast<size_t>(j * ldt0_ + i)] = h0.w[static_cast<size_t>(i * h0.cols + j)];
+  CK(cudaMalloc(&t0_, sizeof(double) * t0.size()));
+  CK(cudaMemcpy(t0_, t0.data(), sizeof(double) * t0.size(), cudaMemcpyHostToDevice));
+  tm_t0_a_ = make_tmap(t0_, h0.rows, n_pad_, ldt0_, kBM);
+  tm_t0_b_ = make_tmap(t0_, h0.rows, n_pad_, ldt0_, kBN);
+  // Hidden-layer tangent width (pitch of the ping-pong T buffers).
+  int64_t wmax = 16;
+  for (int64_t l = 0; l < L_; ++l) wmax = std::max(wmax, layers_[static_cast<size_t>(l)].rows);
+  ldt_ = round_up(wmax, 16);
+  // SYRK tile list over an n x n lower triangle with kBM x kBN tiles.
+  std::vector<int2> tiles;
+  for (int tm = 0; tm * kBM < n_; ++tm)
+    for (int tn = 0; tn * kBN < n_; ++tn)
+      if (static_cast<int64_t>(tn) * kBN <= static_cast<int64_t>(tm) * kBM + kBM - 1) tiles.push_back(make_int2(tm, tn));
+  n_syrk_tiles_ = static_cast<int>(tiles.size());
+  CK(cudaMalloc(&syrk_tiles_, sizeof(int2) * tiles.size()));
+  CK(cudaMemcpy(syrk_tiles_, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice));
+}
+
+DeviceNet::~DeviceNet() {
+  DeviceGuard g(ordinal_);
+  free_workspace();
+  for (auto& d : layers_) {
+    cudaFree(d.w);
+    cudaFree(d.b);
+  }
+  cudaFree(t0_);
+  cudaFree(syrk_tiles_);
+  if (stream_) cudaStreamDestroy(stream_);
+  if (ev_in_) cudaEventDestroy(ev_in_);
+  if (ev_out_) cudaEventDestroy(ev_out_);
+}
+
+void DeviceNet::free_workspace() {
+  for (void* p : ws_allocs_) cudaFree(p);
+  ws_allocs_.clear();
+  ws_cap_ = 0;
+  drop_graphs();
+}
+
+void DeviceNet::drop_graphs() {
+  for (auto& kv : graphs_) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  }
+  graphs_.clear();
+}
+
+double* DeviceNet::ws_alloc(size_t n_doubles) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, sizeof(double) * std::max<size_t>(n_doubles, 2)));
+  CK(cudaMemset(p, 0, sizeof(double) * std::max<size_t>(n_doubles, 2)));
+  ws_allocs_.push_back(p);
+  return static_cast<double*>(p);
+}
+
+int DeviceNet::syrk_split(int points) const {
+  const int tiles = points * n_syrk_tiles_;
+  if (tiles >= sm_count_) return 1;
+  return std::max(1, sm_count_ / tiles);
+}
+
+void DeviceNet::ensure_workspace(int batch) {
+  if (batch <= ws_cap_) return;
+  free_workspace();
+  const int cap = batch;
+  Workspace& w = ws_;
+  const size_t L = static_cast<size_t>(L_);
+  w.z.assign(L, nullptr);
+  w.y.assign(L, nullptr);
+  w.s1.assign(L, nullptr);
+  w.s2.assign(L, nullptr);
+  w.ybar.assign(L, nullptr);
+  w.gz.assign(L, nullptr);
+  w.d.assign(L, nullptr);
+  w.ld.assign(L, 0);
+  for (size_t l = 0; l < L; ++l) {
+    const int64_t ld = round_up(layers_[l].rows, 16);
+    w.ld[l] = ld;
+    w.z[l] = ws_alloc(cap * ld);
+    w.y[l] = ws_alloc(cap * ld);
+    w.s1[l] = ws_alloc(cap * ld);
+    w.s2[l] = ws_alloc(cap * ld);
+    w.ybar[l] = ws_alloc(cap * ld);
+    w.gz[l] = ws_alloc(cap * ld);
+    w.d[l] = ws_alloc(cap * ld);
+  }
+  w.ld_in = round_up(n_, 16);
+  w.ld_lam = round_up(m_, 16);
+  w.x = ws_alloc(cap * w.ld_in);
+  w.lam = ws_alloc(cap * w.ld_lam);
+  w.grad = ws_alloc(cap * w.ld_in);
+  w.mid = ws_alloc(layers_[L - 1].act == kSoftmax ? static_cast<size_t>(cap) * m_ * m_ : 1);
+  // adjoint partials: [chunks][cap][ldmax]
+  int64_t rmax = 1;
+  for (auto& d : layers_) rmax = std::max(rmax, d.rows);
+  w.adj_chunks_max = ceil_div(rmax, dev::kAdjRows);
+  w.ld_part = ldt_ > w.ld_in ? ldt_ : w.ld_in;
+  w.adj_part = ws_alloc(static_cast<size_t>(w.adj_chunks_max) * cap * w.ld_part);
+  // tangents (only needed with >= 2 layers)
+  if (L_ >= 2) {
+    w.t[0] = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
+    w.t[1] = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
+    w.tm_t_a.assign(L, CUtensorMap{});
+    w.tm_t_b.assign(L, CUtensorMap{});
+    for (size_t l = 1; l < L; ++l) {
+      const double* buf = w.t[l & 1];
+      w.tm_t_a[l] = make_tmap(buf, layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBM);
+      w.tm_t_b[l] = make_tmap(buf, layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBN);
+    }
+  }
+  // Hessian accumulator [cap][n_pad][n_pad] and split-K partials
+  w.ldh = n_pad_;
+  w.h = ws_alloc(static_cast<size_t>(cap) * n_pad_ * n_pad_);
+  // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
+  w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, n_syrk_tiles_)) * kBM * kBN);
+  // final-layer skinny product: U [cap][n_pad][16], partials [chunks][cap][n_pad][16]
+  const int64_t kfin = layers_[L - 1].cols;
+  w.sk_chunks = ceil_div(kfin, dev::kSkKChunk);
+  w.u = ws_alloc(static_cast<size_t>(cap) * n_pad_ * dev::kSkMB);
+  w.sk_part = ws_alloc(static_cast<size_t>(w.sk_chunks) * cap * n_pad_ * dev::kSkMB);
+  // device-side outputs for the host API
+  w.y_out = ws_alloc(static_cast<size_t>(cap) * m_);
+  w.j_out = ws_alloc(static_cast<size_t>(cap) * m_ * n_);
+  w.h_out = ws_alloc(static_cast<size_t>(cap) * n_ * n_);
+  w.g_out = ws_alloc(static_cast<size_t>(cap) * n_);
+  ws_cap_ = cap;
+}
+
+// --------------------------------------------------------------------------
+// Launch helpers
+// --------------------------------------------------------------------------
+void DeviceNet::launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p,
+                          int grid) {
+  dev::nt_mma_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
+  CK(cudaGetLastError());
+  ++launches_;
+}
+
+// The whole evaluation for `nb` points whose x / lambda already sit in the
+// workspace.  Outputs go to the given device pointers (nullable).
+void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
+  Workspace& w = ws_;
+  const int L = static_cast<int>(L_);
+  const bool softmax_out = layers_[L - 1].act == kSoftmax;
+  const bool want_h = o.h != nullptr;
+  const bool want_j = o.j != nullptr;
+  const bool need_adj = want_h || o.g != nullptr;
+  const bool need_tan = want_h || want_j;
+
+  // ---- 1. forward chain --------------------------------------------------
+  const double* yin = w.x;
+  int64_t ld_in = w.ld_in;
+  for (int l = 0; l < L; ++l) {
+    const DevLayer& d = layers_[static_cast<size_t>(l)];
+    const int nbpass = nb >= 8 ? 8 : (nb >= 4 ? 4 : 1);
+    dim3 grid(ceil_div(d.rows, dev::kFwdWarps), ceil_div(nb, nbpass));
+    const int act = d.act == kSoftmax ? kLinear : d.act;
+    if (nbpass == 8)
+      dev::fwd_rows_kernel<8><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
+                                                                     act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
+    else if (nbpass == 4)
+      dev::fwd_rows_kernel<4><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
+                                                                     act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
+    else
+      dev::fwd_rows_kernel<1><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
+                                                                     act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
+    CK(cudaGetLastError());
+    ++launches_;
+    yin = w.y[l];
+    ld_in = w.ld[l];
+  }
+  if (softmax_out) {
+    dev::softmax_kernel<<<ceil_div(nb, 4), 128, 0, st>>>(w.z[L - 1], w.y[L - 1], static_cast<int>(m_), w.ld[L - 1],
+                                                         nb);
+    CK(cudaGetLastError());
+    ++launches_;
+  }
+  if (o.y) {
+    CK(cudaMemcpy2DAsync(o.y, sizeof(double) * m_, w.y[L - 1], sizeof(double) * w.ld[L - 1], sizeof(double) * m_, nb,
+                         cudaMemcpyDeviceToDevice, st));
+  }
+
+  // ---- 2. adjoint chain --------------------------------------------------
+  if (need_adj) {
+    dev::adj_seed_kernel<<<ceil_div(nb, 4), 128, 0, st>>>(
+        w.lam, w.ld_lam, w.y[L - 1], w.s1[L - 1], w.s2[L - 1], w.ld[L - 1], static_cast<int>(m_), nb,
+        softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
+    CK(cudaGetLastError());
+    ++launches_;
+    const int lstop = o.g ? 0 : 1;
+    for (int l = L - 1; l >= lstop; --l) {
+      const DevLayer& d = layers_[static_cast<size_t>(l)];
+      const int chunks = ceil_div(d.rows, dev::kAdjRows);
+      dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
+      for (int p0 = 0; p0 < nb;) {
+        const int left = nb - p0;
+        if (left >= 8) {
+          dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                     nb, p0, w.adj_part, w.ld_part);
+          p0 += 8;
+        } else if (left >= 4) {
+          dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                     nb, p0, w.adj_part, w.ld_part);
+          p0 += 4;
+        } else {
+          dev::adj_cols_kernel<1><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                     nb, p0, w.adj_part, w.ld_part);
+          p0 += 1;
+        }
+        CK(cudaGetLastError());
+        ++launches_;
+      }
+      const int64_t tot = static_cast<int64_t>(nb) * d.cols;
+      if (l > 0) {
+        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.adj_part, chunks, w.ld_part,
+                                                                   static_cast<int>(d.cols), nb, w.s1[l - 1],
+                                                                   w.s2[l - 1], w.ld[l - 1], w.ybar[l - 1],
+                                                                   w.gz[l - 1], w.d[l - 1]);
+      } else {
+        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.adj_part, chunks, w.ld_part,
+                                                                   static_cast<int>(d.cols), nb, nullptr, nullptr,
+                                                                   w.ld_in, w.grad, nullptr, nullptr);
+      }
+      CK(cudaGetLastError());
+      ++launches_;
+    }
+    if (o.g) {
+      CK(cudaMemcpy2DAsync(o.g, sizeof(double) * n_, w.grad, sizeof(double) * w.ld_in, sizeof(double) * n_, nb,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (!need_tan) return;
+
+  // ---- 3. tangent chain + Hessian SYRK ------------------------------------
+  if (want_h) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, st));
+  const int kfin_layer = L - 1;
+  const bool skinny_final = m_ <= dev::kSkMB;
+  // T_l lives in: l == 0 -> t0_ (broadcast over points), else w.t[l & 1].
+  auto t_ptr = [&](int l) -> const double* { return l == 0 ? t0_ : w.t[l & 1]; };
+  auto t_ld = [&](int l) -> int64_t { return l == 0 ? ldt0_ : ldt_; };
+  auto t_point_rows = [&](int l) -> int64_t { return l == 0 ? 0 : n_pad_; };
+  auto tmap_a = [&](int l) -> const CUtensorMap& { return l == 0 ? tm_t0_a_ : w.tm_t_a[static_cast<size_t>(l)]; };
+  auto tmap_b = [&](int l) -> const CUtensorMap& { return l == 0 ? tm_t0_b_ : w.tm_t_b[static_cast<size_t>(l)]; };
+
+  auto syrk = [&](int l) {
+    const DevLayer& d = layers_[static_cast<size_t>(l)];
+    dev::NtParams p{};
+    p.tiles = syrk_tiles_;
+    p.n_tiles = n_syrk_tiles_;
+    p.points = nb;
+    p.split = syrk_split(nb);
+    p.k_blocks = ceil_div(d.rows, kBK);
+    p.a_point_rows = t_point_rows(l);
+    p.b_point_rows = t_point_rows(l);
+    p.b_rows_valid = static_cast<int>(n_);
+    p.m_rows_valid = static_cast<int>(n_);
+    p.scale = w.d[l];
+    p.s_stride = w.ld[l];
+    p.c = w.h;
+    p.c_point_stride = n_pad_ * n_pad_;
+    p.ldc = n_pad_;
+    p.mode = p.split > 1 ? dev::kPartial : dev::kAccum;
+    p.partial = w.syrk_part;
+    launch_nt(st, tmap_a(l), tmap_b(l), p, nb * n_syrk_tiles_ * p.split);
+    if (p.split > 1) {
+      dim3 grid(8, nb * n_syrk_tiles_);
+      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, st>>>(w.syrk_part, syrk_tiles_, n_syrk_tiles_, nb, p.split, w.h,
+                                                            n_pad_ * n_pad_, n_pad_, static_cast<int>(n_));
+      CK(cudaGetLastError());
+      ++launches_;
+    }
+  };
+
+  for (int l = 0; l + 1 < L; ++l) {
+    // curvature of hidden layer l
+    if (want_h && layers_[static_cast<size_t>(l)].act != kLinear) syrk(l);
+    // propagate the tangents to layer l+1 (unless it is a skinny final)
+    if (l + 1 == kfin_layer && skinny_final) break;
+    const DevLayer& dn = layers_[static_cast<size_t>(l + 1)];
+    dev::NtParams p{};
+    p.tiles = nullptr;
+    p.tiles_m = static_cast<int>(n_pad_ / kBM);
+    p.tiles_n = ceil_div(dn.rows, kBN);
+    p.n_tiles = p.tiles_m * p.tiles_n;
+    p.points = nb;
+    p.split = 1;
+    p.k_blocks = ceil_div(dn.cols, kBK);
+    p.a_point_rows = t_point_rows(l);
+    p.b_point_rows = 0;
+    p.b_rows_valid = static_cast<int>(dn.rows);
+    p.m_rows_valid = static_cast<int>(n_pad_);
+    p.scale = w.s1[l];
+    p.s_stride = w.ld[l];
+    p.c = w.t[(l + 1) & 1];
+    p.c_point_stride = n_pad_ * ldt_;
+    p.ldc = ldt_;
+    p.mode = dev::kStore;
+    launch_nt(st, tmap_a(l), dn.tm_w, p, nb * p.n_tiles);
+  }
+
+  // ---- 4. final layer -------------------------------------------------------
+  const DevLayer& df = layers_[static_cast<size_t>(kfin_layer)];
+  const double* u;
+  int64_t ldu, u_point_rows;
+  if (kfin_layer == 0) {
+    u = t0_;
+    ldu = ldt0_;
+    u_point_rows = 0;
+  } else if (skinny_final) {
+    const int l = kfin_layer - 1;
+    dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
+    dev::skinny_nt_kernel<<<grid, 256, 0, st>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_), w.s1[l],
+                                                w.ld[l], df.w, df.ldw, static_cast<int>(m_),
+                                                static_cast<int>(df.cols), w.sk_part);
+    CK(cudaGetLastError());
+    ++launches_;
+    const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
+    dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.sk_part, w.sk_chunks, nb,
+                                                                  static_cast<int>(n_pad_), static_cast<int>(m_), w.u);
+    CK(cudaGetLastError());
+    ++launches_;
+    u = w.u;
+    ldu = dev::kSkMB;
+    u_point_rows = n_pad_;
+  } else {
+    u = t_ptr(kfin_layer);
+    ldu = ldt_;
+    u_point_rows = n_pad_;
+  }
+  if (want_j) {
+    const int64_t tot = static_cast<int64_t>(nb) * n_;
+    dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, st>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
+                                                                 w.y[kfin_layer], w.ld[kfin_layer],
+                                                                 static_cast<int>(n_), static_cast<int>(m_), nb,
+                                                                 softmax_out ? 1 : 0, o.j);
+    CK(cudaGetLastError());
+    ++launches_;
+  }
+  if (want_h) {
+    if (df.act != kLinear) {
+      if (softmax_out || skinny_final || kfin_layer == 0) {
+        // K = m is small: direct lower-triangle update (dense middle for softmax)
+        dim3 blk(16, 16);
+        dim3 grid(ceil_div(n_, 16), ceil_div(n_, 16), nb);
+        dev::small_k_syrk_kernel<<<grid, blk, 0, st>>>(u, ldu, u_point_rows, w.d[kfin_layer], w.ld[kfin_layer],
+                                                       softmax_out ? w.mid : nullptr, m_ * m_, static_cast<int>(n_),
+                                                       static_cast<int>(m_), nb, w.h, n_pad_ * n_pad_, n_pad_);
+        CK(cudaGetLastError());
+        ++launches_;
+      } else {
+        syrk(kfin_layer);
+      }
+    }
+    const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
+    dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.h, n_pad_ * n_pad_, n_pad_,
+                                                                   static_cast<int>(n_), nb, o.h);
+    CK(cudaGetLastError());
+    ++launches_;
+  }
+}
+
+void DeviceNet::run(cudaStream_t st, int nb, const Outputs& o) {
+  const GraphKey key{nb, o.y, o.j, o.h, o.g};
+  if (!net_.use_graphs) {
+    launches_ = 0;
+    enqueue(st, nb, o);
+    last_launches_ = launches_;
+    return;
+  }
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
+    launches_ = 0;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue(st, nb, o);
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &graph));
+    GraphEntry e;
+    e.launches = launches_;
+    const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(ie);
+    if (graphs_.size() > 16) drop_graphs();
+    it = graphs_.emplace(key, e).first;
+  }
+  CK(cudaGraphLaunch(it->second.exec, st));
+  last_launches_ = it->second.launches;
+}
+
+// Host-buffer entry: copy in, evaluate, copy out, synchronise.
+void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess,
+                              double* grad) {
+  DeviceGuard g(ordinal_);
+  ensure_workspace(nb);
+  Workspace& w = ws_;
+  CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
+                       cudaMemcpyHostToDevice, stream_));
+  if (lam)
+    CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam, sizeof(double) * m_, sizeof(double) * m_, nb,
+                         cudaMemcpyHostToDevice, stream_));
+  Outputs o;
+  o.y = y ? w.y_out : nullptr;
+  o.j = jac ? w.j_out : nullptr;
+  o.h = hess ? w.h_out : nullptr;
+  o.g = grad ? w.g_out : nullptr;
+  run(stream_, nb, o);
+  if (y) CK(cudaMemcpyAsync(y, w.y_out, sizeof(double) * nb * m_, cudaMemcpyDeviceToHost, stream_));
+  if (jac) CK(cudaMemcpyAsync(jac, w.j_out, sizeof(double) * nb * m_ * n_, cudaMemcpyDeviceToHost, stream_));
+  if (hess) CK(cudaMemcpyAsync(hess, w.h_out, sizeof(double) * nb * n_ * n_, cudaMemcpyDeviceToHost, stream_));
+  if (grad) CK(cudaMemcpyAsync(grad, w.g_out, sizeof(double) * nb * n_, cudaMemcpyDeviceToHost, stream_));
+  CK(cudaStreamSynchronize(stream_));
+}
+
+// Device-buffer entry: ordered after / before `user` stream, no host sync.
+void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
+                                cudaStream_t user) {
+  DeviceGuard g(ordinal_);
+  ensure_workspace(nb);
+  Workspace& w = ws_;
+  CK(cudaEventRecord(ev_in_, user));
+  CK(cudaStreamWaitEvent(stream_, ev_in_, 0));
+  CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
+                       cudaMemcpyDeviceToDevice, stream_));
+  if (dlam)
+    CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, dlam, sizeof(double) * m_, sizeof(double) * m_, nb,
+                         cudaMemcpyDeviceToDevice, stream_));
+  Outputs o;
+  o.y = dy;
+  o.j = dj;
+  o.h = dh;
+  o.g = nullptr;
+  run(stream_, nb, o);
+  CK(cudaEventRecord(ev_out_, stream_));
+  CK(cudaStreamWaitEvent(user, ev_out_, 0));
+}
+
+// ---------------------------------------------------------------------------
+// Net <-> DeviceNet glue.
+// ---------------------------------------------------------------------------
+Net::~Net() = default;
+
+DeviceNet& Net::device(int ordinal) {
+  if (dev_) {
+    if (ordinal >= 0 && ordinal != dev_->ordinal())
+      throw StructuralError("network is already bound to CUDA device " + std::to_string(dev_->ordinal()));
+    return *dev_;
+  }
+  if (ordinal < 0) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) {
+      cudaGetLastError();
+      throw DeviceError("no CUDA device available");
+    }
+    ordinal = cur;
+  }
+  dev_ = std::make_unique<DeviceNet>(*this, ordinal);
+  return *dev_;
+}
+
+int Net::bound_ordinal() const { return dev_ ? dev_->ordinal() : -1; }
+
+int device_count() {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+}  // namespace gbb

@@ -1,0 +1,164 @@
+"""GPU parity: the B200 oracle (through the C ABI) against the CPU oracle
+restatement of the reference algorithm (oracle/gbopt_oracle.py, which
+follows proj/src/nn.cpp:113-292 line by line).
+
+Parity metric: per array and per point,
+max|GPU - CPU| / max|CPU| <= 1e-10 (north_star tolerance, FP64).
+"""
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+if has_gpu():
+    import paper_2509_22462_b200 as gb
+    from paper_2509_22462_b200 import configs
+from oracle import gbopt_oracle as orc
+
+
+def to_oracle(net) -> "orc.NeuralNet":
+    layers = []
+    for l in range(net.layer_count):
+        w, b, a = net.layer(l)
+        layers.append(orc.Layer(w, b, a))
+    return orc.NeuralNet(layers)
+
+
+def check_point(net, ref, x, lam, tol=TOL):
+    y, j, h = net.oracle(x, lam)
+    ry = ref.forward(x)
+    rj = ref.jacobian(x)
+    rh = ref.lagrangian_hessian(x, lam)
+    assert orc.rel_err(y, ry) <= tol, ("y", orc.rel_err(y, ry))
+    assert orc.rel_err(j, rj) <= tol, ("J", orc.rel_err(j, rj))
+    if np.abs(rh).max() > 0:
+        assert orc.rel_err(h, rh) <= tol, ("H", orc.rel_err(h, rh))
+    else:
+        assert np.abs(h).max() <= 1e-14
+    assert np.array_equal(h, h.T)  # exactly symmetric (nn.cpp:291)
+    return orc.rel_err(y, ry), orc.rel_err(j, rj), orc.rel_err(h, rh)
+
+
+MIXES = [
+    ([5, 7, 4], "tanh", "tanh", 1234),
+    ([4, 6, 6, 3], "tanh", "softmax", 2),
+    ([4, 6, 6, 3], "sigmoid", "tanh", 3),
+    ([4, 6, 6, 3], "sigmoid", "softmax", 4),
+    ([4, 6, 6, 3], "tanh", "linear", 5),
+    ([4, 6, 6, 3], "linear", "linear", 6),
+    ([5, 8, 7, 4], "sigmoid", "softmax", 999),
+    ([6, 9, 4], "softplus", "sigmoid", 41),
+    ([3, 5], "tanh", "tanh", 1),
+    ([7, 4], "softplus", "softmax", 77),
+    ([9, 33, 17, 40], "tanh", "sigmoid", 8),      # final width > 16 (big final path)
+    ([9, 33, 17, 20], "sigmoid", "softmax", 9),    # softmax wider than 16
+    ([130, 200, 150, 12], "softplus", "linear", 10),  # n_pad > 112, multiple M tiles
+    ([300, 257, 129, 3], "tanh", "tanh", 11),
+]
+
+
+@pytest.mark.parametrize("widths,hid,fin,seed", MIXES)
+def test_small_nets_match_oracle(widths, hid, fin, seed):
+    net = gb.random_net(widths, hid, fin, seed)
+    ref = to_oracle(net)
+    rng = np.random.default_rng(seed)
+    for _ in range(3):
+        x = rng.uniform(-1.5, 1.5, widths[0])
+        lam = rng.uniform(-2, 2, widths[-1])
+        check_point(net, ref, x, lam)
+        g = net.lagrangian_gradient(x, lam)
+        assert orc.rel_err(g, ref.lagrangian_gradient(x, lam)) <= TOL
+
+
+def test_acceptance_criterion1_nets():
+    """acceptance.cpp:86-128: 25 nets, depth 1..5, widths 2..12, final softmax."""
+    rng = np.random.default_rng(2026)
+    hiddens = ["linear", "tanh", "sigmoid"]
+    for k in range(25):
+        depth = 1 + k % 5
+        widths = [int(2 + rng.integers(0, 11)) for _ in range(depth + 1)]
+        net = gb.random_net(widths, hiddens[k % 3], "softmax", 4000 + k)
+        ref = to_oracle(net)
+        x = rng.uniform(-0.9, 0.9, widths[0])
+        lam = rng.uniform(-1, 1, widths[-1])
+        check_point(net, ref, x, lam)
+        # exact linearity in lambda (<= 1e-12)
+        lam2 = rng.uniform(-1, 1, widths[-1])
+        h1 = net.lagrangian_hessian(x, lam)
+        h2 = net.lagrangian_hessian(x, lam2)
+        hm = net.lagrangian_hessian(x, lam + 2.5 * lam2)
+        assert np.abs(hm - (h1 + 2.5 * h2)).max() <= 1e-12
+
+
+def test_known_answers_on_device():
+    """test_nn.cpp:30-94, 151-167, 229-243 on the GPU path."""
+    eye = gb.NeuralNet.from_layers([np.eye(2)], [np.zeros(2)], [gb.LINEAR])
+    x = np.array([0.3, -0.7])
+    assert np.array_equal(eye.forward(x), x)
+    t = gb.NeuralNet.from_layers([np.eye(3)], [np.zeros(3)], [gb.TANH])
+    assert np.abs(t.forward(np.zeros(3))).max() == 0.0
+    assert np.array_equal(t.jacobian(np.zeros(3)), np.eye(3))
+    assert np.abs(t.lagrangian_hessian(np.zeros(3), np.array([1.0, 0, 0]))).max() == 0.0
+    rng = np.random.default_rng(17)
+    w = rng.uniform(-1, 1, (3, 5))
+    lin = gb.NeuralNet.from_layers([w], [rng.uniform(-1, 1, 3)], [gb.LINEAR])
+    assert np.array_equal(lin.jacobian(rng.uniform(-1, 1, 5)), w)
+    sm = gb.NeuralNet.from_layers([np.zeros((4, 4))], [np.zeros(4)], [gb.SOFTMAX])
+    assert np.allclose(sm.forward(rng.uniform(-5, 5, 4)), 0.25, rtol=0, atol=1e-14)
+    s = gb.NeuralNet.from_layers([np.eye(3)], [np.zeros(3)], [gb.SIGMOID])
+    assert np.all(s.forward(np.zeros(3)) == 0.5)
+    assert np.all(s.jacobian(np.zeros(3)) == 0.25 * np.eye(3))
+    # linear net => zero Hessian
+    ln = gb.random_net([4, 5, 3], "linear", "linear", 9)
+    assert np.abs(ln.lagrangian_hessian(rng.uniform(-1, 1, 4), rng.uniform(-1, 1, 3))).max() <= 1e-14
+
+
+def test_determinism_bitwise():
+    net = gb.random_net([6, 8, 4], "tanh", "softmax", 21)
+    x = np.random.default_rng(4).uniform(-1, 1, 6)
+    lam = np.random.default_rng(5).uniform(-1, 1, 4)
+    a = net.oracle(x, lam)
+    b = net.oracle(x, lam)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+
+
+def test_batched_equals_single():
+    net = gb.random_net([20, 40, 30, 5], "sigmoid", "linear", 3)
+    rng = np.random.default_rng(7)
+    X = rng.uniform(-1, 1, (9, 20))
+    L = rng.uniform(-1, 1, (9, 5))
+    Y, J, H = net.oracle_batched(X, L)
+    for b in range(9):
+        y, j, h = net.oracle(X[b], L[b])
+        assert np.array_equal(Y[b], y) and np.array_equal(J[b], j) and np.array_equal(H[b], h)
+
+
+def test_graphs_off_matches_graphs_on():
+    net = gb.random_net([30, 64, 64, 7], "tanh", "softmax", 12)
+    rng = np.random.default_rng(8)
+    x, lam = rng.uniform(-1, 1, 30), rng.uniform(-1, 1, 7)
+    a = net.oracle(x, lam)
+    net.set_graphs(False)
+    b = net.oracle(x, lam)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+
+
+def test_config_c1_parity():
+    wl = configs.make("c1")
+    ref = to_oracle(wl.net)
+    errs = check_point(wl.net, ref, wl.X[0], wl.Lam[0])
+    print("c1 rel errs y/J/H:", errs)
+
+
+@pytest.mark.slow
+def test_config_c2_parity():
+    wl = configs.make("c2")
+    ref = to_oracle(wl.net)
+    errs = check_point(wl.net, ref, wl.X[0], wl.Lam[0])
+    print("c2 rel errs y/J/H:", errs)
