@@ -209,6 +209,19 @@ gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net,
  * (graph replays count their kernel nodes). */
 int64_t gbopt_net_last_launch_count(const gbopt_net* net);
 
+/* Profiling hook used by bench.py's roofline leg: runs one evaluation of
+ * `batch` points (device pointers, as gbopt_net_oracle_batched_device)
+ * eagerly with CUDA events around every kernel on the launching stream and
+ * reports, per launch, its kernel tag, duration (ms), algorithmic FP64
+ * flops and algorithmic HBM bytes.  *count receives the number of launches
+ * (at most cap are written).  Synchronous. */
+gbopt_status gbopt_net_profile(const gbopt_net* net, size_t batch,
+                               const double* dX, const double* dLambda,
+                               int32_t* tags, float* ms, double* flops,
+                               double* bytes, size_t cap, size_t* count);
+/* Name of a kernel tag reported by gbopt_net_profile ("nt_mma.gemm", ...). */
+const char* gbopt_kernel_tag_name(int tag);
+
 /* Enables/disables CUDA-graph capture of the oracle sequence (default on). */
 gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled);
 

@@ -329,4 +329,24 @@ gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net, size_t batch,
   });
 }
 
+gbopt_status gbopt_net_profile(const gbopt_net* net, size_t batch, const double* dX, const double* dLambda,
+                               int32_t* tags, float* ms, double* flops, double* bytes, size_t cap, size_t* count) {
+  if (net == nullptr || dX == nullptr || dLambda == nullptr || count == nullptr)
+    return fail_argument("gbopt_net_profile: null argument");
+  if (batch == 0) return fail_argument("gbopt_net_profile: batch must be positive");
+  return guarded([&] {
+    std::vector<gbb::ProfResult> res;
+    net->net->device().profile(static_cast<int>(batch), dX, dLambda, &res);
+    *count = res.size();
+    for (size_t i = 0; i < res.size() && i < cap; ++i) {
+      if (tags) tags[i] = res[i].tag;
+      if (ms) ms[i] = res[i].ms;
+      if (flops) flops[i] = res[i].flops;
+      if (bytes) bytes[i] = res[i].bytes;
+    }
+  });
+}
+
+const char* gbopt_kernel_tag_name(int tag) { return gbb::kernel_tag_name(tag); }
+
 }  // extern "C"

@@ -61,6 +61,19 @@ struct Workspace {
   double *y_out = nullptr, *j_out = nullptr, *h_out = nullptr, *g_out = nullptr;
 };
 
+enum KernelTag : int {
+  kTagFwd = 0, kTagSoftmax, kTagAdjSeed, kTagAdjCols, kTagAdjReduce, kTagGemm, kTagSyrk, kTagSyrkReduce,
+  kTagSkinny, kTagSkinnyReduce, kTagJacOut, kTagSmallSyrk, kTagSymmetrize, kTagCount
+};
+const char* kernel_tag_name(int tag);
+
+struct ProfResult {
+  int tag;
+  float ms;
+  double flops;  // algorithmic FP64 flops of this launch
+  double bytes;  // algorithmic HBM bytes (weight streams) of this launch
+};
+
 struct Outputs {
   double* y = nullptr;  // [nb][m]
   double* j = nullptr;  // [nb][m][n]
@@ -80,6 +93,8 @@ class DeviceNet {
 
   // Host buffers in/out (synchronous).  Any output may be null.
   void evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess, double* grad);
+  // Eager run with CUDA events around every launch (on the launching stream).
+  void profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out);
   // Device buffers, ordered on `user` stream, asynchronous.
   void evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
                        cudaStream_t user);
@@ -98,6 +113,15 @@ class DeviceNet {
   int syrk_split(int points) const;
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
   void enqueue(cudaStream_t st, int nb, const Outputs& o);
+  void prof_begin(cudaStream_t st, int tag, double flops, double bytes);
+  void after_launch(cudaStream_t st);
+  struct ProfRec {
+    int tag;
+    double flops, bytes;
+    cudaEvent_t e0, e1;
+  };
+  bool profiling_ = false;
+  std::vector<ProfRec> prof_;
   void run(cudaStream_t st, int nb, const Outputs& o);
 
   const Net& net_;

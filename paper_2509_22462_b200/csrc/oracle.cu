@@ -263,8 +263,60 @@ void DeviceNet::ensure_workspace(int batch) {
 void DeviceNet::launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p,
                           int grid) {
   dev::nt_mma_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
+  after_launch(st);
+}
+
+void DeviceNet::prof_begin(cudaStream_t st, int tag, double flops, double bytes) {
+  if (!profiling_) return;
+  ProfRec r;
+  r.tag = tag;
+  r.flops = flops;
+  r.bytes = bytes;
+  CK(cudaEventCreate(&r.e0));
+  CK(cudaEventCreate(&r.e1));
+  CK(cudaEventRecord(r.e0, st));
+  prof_.push_back(r);
+}
+
+void DeviceNet::after_launch(cudaStream_t st) {
   CK(cudaGetLastError());
   ++launches_;
+  if (profiling_) CK(cudaEventRecord(prof_.back().e1, st));
+}
+
+void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out) {
+  DeviceGuard g(ordinal_);
+  ensure_workspace(nb);
+  Workspace& w = ws_;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
+                       cudaMemcpyDeviceToDevice, stream_));
+  CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, dlam, sizeof(double) * m_, sizeof(double) * m_, nb,
+                       cudaMemcpyDeviceToDevice, stream_));
+  Outputs o;
+  o.y = w.y_out;
+  o.j = w.j_out;
+  o.h = w.h_out;
+  profiling_ = true;
+  prof_.clear();
+  launches_ = 0;
+  try {
+    enqueue(stream_, nb, o);
+  } catch (...) {
+    profiling_ = false;
+    throw;
+  }
+  profiling_ = false;
+  CK(cudaStreamSynchronize(stream_));
+  out->clear();
+  for (auto& r : prof_) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    out->push_back(ProfResult{r.tag, ms, r.flops, r.bytes});
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  prof_.clear();
 }
 
 // The whole evaluation for `nb` points whose x / lambda already sit in the
@@ -286,6 +338,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     const int nbpass = nb >= 8 ? 8 : (nb >= 4 ? 4 : 1);
     dim3 grid(ceil_div(d.rows, dev::kFwdWarps), ceil_div(nb, nbpass));
     const int act = d.act == kSoftmax ? kLinear : d.act;
+    prof_begin(st, kTagFwd, 2.0 * d.rows * d.cols * nb, 8.0 * d.rows * d.cols * ceil_div(nb, nbpass));
     if (nbpass == 8)
       dev::fwd_rows_kernel<8><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
@@ -295,16 +348,15 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     else
       dev::fwd_rows_kernel<1><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
     yin = w.y[l];
     ld_in = w.ld[l];
   }
   if (softmax_out) {
+    prof_begin(st, kTagSoftmax, 0, 0);
     dev::softmax_kernel<<<ceil_div(nb, 4), 128, 0, st>>>(w.z[L - 1], w.y[L - 1], static_cast<int>(m_), w.ld[L - 1],
                                                          nb);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
   }
   if (o.y) {
     CK(cudaMemcpy2DAsync(o.y, sizeof(double) * m_, w.y[L - 1], sizeof(double) * w.ld[L - 1], sizeof(double) * m_, nb,
@@ -313,11 +365,11 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
 
   // ---- 2. adjoint chain --------------------------------------------------
   if (need_adj) {
+    prof_begin(st, kTagAdjSeed, 0, 0);
     dev::adj_seed_kernel<<<ceil_div(nb, 4), 128, 0, st>>>(
         w.lam, w.ld_lam, w.y[L - 1], w.s1[L - 1], w.s2[L - 1], w.ld[L - 1], static_cast<int>(m_), nb,
         softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
     const int lstop = o.g ? 0 : 1;
     for (int l = L - 1; l >= lstop; --l) {
       const DevLayer& d = layers_[static_cast<size_t>(l)];
@@ -325,6 +377,8 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
       for (int p0 = 0; p0 < nb;) {
         const int left = nb - p0;
+        const int pass = left >= 8 ? 8 : (left >= 4 ? 4 : 1);
+        prof_begin(st, kTagAdjCols, 2.0 * d.rows * d.cols * pass, 8.0 * d.rows * d.cols);
         if (left >= 8) {
           dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
                                                                      nb, p0, w.adj_part, w.ld_part);
@@ -338,10 +392,10 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
                                                                      nb, p0, w.adj_part, w.ld_part);
           p0 += 1;
         }
-        CK(cudaGetLastError());
-        ++launches_;
+        after_launch(st);
       }
       const int64_t tot = static_cast<int64_t>(nb) * d.cols;
+      prof_begin(st, kTagAdjReduce, 0, 0);
       if (l > 0) {
         dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.adj_part, chunks, w.ld_part,
                                                                    static_cast<int>(d.cols), nb, w.s1[l - 1],
@@ -352,8 +406,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
                                                                    static_cast<int>(d.cols), nb, nullptr, nullptr,
                                                                    w.ld_in, w.grad, nullptr, nullptr);
       }
-      CK(cudaGetLastError());
-      ++launches_;
+      after_launch(st);
     }
     if (o.g) {
       CK(cudaMemcpy2DAsync(o.g, sizeof(double) * n_, w.grad, sizeof(double) * w.ld_in, sizeof(double) * n_, nb,
@@ -392,13 +445,14 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.ldc = n_pad_;
     p.mode = p.split > 1 ? dev::kPartial : dev::kAccum;
     p.partial = w.syrk_part;
+    prof_begin(st, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
     launch_nt(st, tmap_a(l), tmap_b(l), p, nb * n_syrk_tiles_ * p.split);
     if (p.split > 1) {
+      prof_begin(st, kTagSyrkReduce, 0, 0);
       dim3 grid(8, nb * n_syrk_tiles_);
       dev::syrk_partial_reduce_kernel<<<grid, 256, 0, st>>>(w.syrk_part, syrk_tiles_, n_syrk_tiles_, nb, p.split, w.h,
                                                             n_pad_ * n_pad_, n_pad_, static_cast<int>(n_));
-      CK(cudaGetLastError());
-      ++launches_;
+      after_launch(st);
     }
   };
 
@@ -426,6 +480,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.c_point_stride = n_pad_ * ldt_;
     p.ldc = ldt_;
     p.mode = dev::kStore;
+    prof_begin(st, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
     launch_nt(st, tmap_a(l), dn.tm_w, p, nb * p.n_tiles);
   }
 
@@ -440,16 +495,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   } else if (skinny_final) {
     const int l = kfin_layer - 1;
     dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
+    prof_begin(st, kTagSkinny, 2.0 * n_ * m_ * df.cols * nb, 0);
     dev::skinny_nt_kernel<<<grid, 256, 0, st>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_), w.s1[l],
                                                 w.ld[l], df.w, df.ldw, static_cast<int>(m_),
                                                 static_cast<int>(df.cols), w.sk_part);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
     const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
+    prof_begin(st, kTagSkinnyReduce, 0, 0);
     dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.sk_part, w.sk_chunks, nb,
                                                                   static_cast<int>(n_pad_), static_cast<int>(m_), w.u);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
     u = w.u;
     ldu = dev::kSkMB;
     u_point_rows = n_pad_;
@@ -460,12 +515,12 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   }
   if (want_j) {
     const int64_t tot = static_cast<int64_t>(nb) * n_;
+    prof_begin(st, kTagJacOut, 0, 0);
     dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, st>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
                                                                  w.y[kfin_layer], w.ld[kfin_layer],
                                                                  static_cast<int>(n_), static_cast<int>(m_), nb,
                                                                  softmax_out ? 1 : 0, o.j);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
   }
   if (want_h) {
     if (df.act != kLinear) {
@@ -473,20 +528,20 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         // K = m is small: direct lower-triangle update (dense middle for softmax)
         dim3 blk(16, 16);
         dim3 grid(ceil_div(n_, 16), ceil_div(n_, 16), nb);
+        prof_begin(st, kTagSmallSyrk, 0, 0);
         dev::small_k_syrk_kernel<<<grid, blk, 0, st>>>(u, ldu, u_point_rows, w.d[kfin_layer], w.ld[kfin_layer],
                                                        softmax_out ? w.mid : nullptr, m_ * m_, static_cast<int>(n_),
                                                        static_cast<int>(m_), nb, w.h, n_pad_ * n_pad_, n_pad_);
-        CK(cudaGetLastError());
-        ++launches_;
+        after_launch(st);
       } else {
         syrk(kfin_layer);
       }
     }
     const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
+    prof_begin(st, kTagSymmetrize, 0, 0);
     dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.h, n_pad_ * n_pad_, n_pad_,
                                                                    static_cast<int>(n_), nb, o.h);
-    CK(cudaGetLastError());
-    ++launches_;
+    after_launch(st);
   }
 }
 
@@ -594,6 +649,14 @@ DeviceNet& Net::device(int ordinal) {
 }
 
 int Net::bound_ordinal() const { return dev_ ? dev_->ordinal() : -1; }
+
+const char* kernel_tag_name(int tag) {
+  static const char* names[kTagCount] = {"fwd_rows",     "softmax",       "adj_seed",     "adj_cols",
+                                         "adj_reduce",   "nt_mma.gemm",   "nt_mma.syrk",  "syrk_reduce",
+                                         "skinny_nt",    "skinny_reduce", "jacobian_out", "small_k_syrk",
+                                         "symmetrize"};
+  return (tag >= 0 && tag < kTagCount) ? names[tag] : "unknown";
+}
 
 int device_count() {
   int c = 0;

@@ -76,6 +76,9 @@ _net_oracle_batched_device = _fn("gbopt_net_oracle_batched_device", _status, _vp
                                  _vp, _vp)
 _net_last_launch_count = _fn("gbopt_net_last_launch_count", _i64, _vp)
 _net_set_graphs = _fn("gbopt_net_set_graphs", _status, _vp, ctypes.c_int)
+_net_profile = _fn("gbopt_net_profile", _status, _vp, _sz, _vp, _vp, ctypes.POINTER(ctypes.c_int32),
+                   ctypes.POINTER(ctypes.c_float), _dp, _dp, _sz, ctypes.POINTER(_sz))
+_kernel_tag_name = _fn("gbopt_kernel_tag_name", ctypes.c_char_p, ctypes.c_int)
 
 # ---------------------------------------------------------------------------
 # Error taxonomy (reference errors.hpp:10-71; status codes gbopt.h:19-31)
@@ -352,6 +355,20 @@ class NeuralNet:
         enqueued on ``stream`` without a host synchronisation."""
         _check(_net_oracle_batched_device(self._h, batch, dX or None, self.input_dim, dLam or None, self.output_dim,
                                           dY or None, dJ or None, dH or None, stream or None))
+
+
+def profile_launches(net: "NeuralNet", batch: int, dX: int, dLam: int):
+    """Per-launch (kernel, ms, flops, bytes) of one eager evaluation, timed
+    with CUDA events on the launching stream (gbopt_net_profile)."""
+    cap = 4096
+    tags = (ctypes.c_int32 * cap)()
+    ms = (ctypes.c_float * cap)()
+    fl = (ctypes.c_double * cap)()
+    by = (ctypes.c_double * cap)()
+    cnt = _sz()
+    _check(_net_profile(net._h, batch, dX, dLam, tags, ms, fl, by, cap, ctypes.byref(cnt)))
+    return [(_kernel_tag_name(tags[i]).decode(), float(ms[i]), float(fl[i]), float(by[i]))
+            for i in range(min(cnt.value, cap))]
 
 
 def load_weights(path: str) -> NeuralNet:
