@@ -246,7 +246,7 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2509_22462_b200 as gb
-    from paper_2509_22462_b200 import configs
+    from paper_2509_22462_b200 import configs, parallel
 
     name = args.config
     B = args.batch or DEFAULT_BATCH[name]
@@ -277,7 +277,8 @@ def run_b200(args):
                                   stream.cuda_stream)
         if world > 1:
             # result gather to rank 0: the path's only collective
-            torch.cat([Yd.reshape(-1), Jd.reshape(-1), Hd.reshape(-1)], out=flat)
+            # (paper_2509_22462_b200/parallel.py; CPU-tested over gloo)
+            parallel.pack(Yd, Jd, Hd, B, m, n, flat)
             dist.gather(flat, gather_list=gather, dst=0)
 
     peak = measure_fp64_peak(torch, dev) if rank == 0 else None

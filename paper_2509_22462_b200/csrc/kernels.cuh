@@ -77,11 +77,14 @@ __device__ __forceinline__ void act_eval(int act, double z, double& y, double& d
       d2 = sp * (1.0 - 2.0 * s);
       return;
     }
-    case 4: {  // softplus
-      const double s = 0.5 * tanh(0.5 * z) + 0.5;
-      y = fmax(z, 0.0) + log1p(exp(-fabs(z)));
+    case 4: {  // softplus (builder extension), stable on both tails
+      const double e = exp(-fabs(z));
+      const double big = 1.0 / (1.0 + e), small = e / (1.0 + e);
+      const double s = z >= 0.0 ? big : small;      // logistic(z)
+      const double sm = z >= 0.0 ? small : big;     // logistic(-z) = 1 - s
+      y = fmax(z, 0.0) + log1p(e);
       d1 = s;
-      d2 = s * (1.0 - s);
+      d2 = s * sm;
       return;
     }
     default:  // linear (softmax rows are finished by softmax_kernel)

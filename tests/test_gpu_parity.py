@@ -162,3 +162,93 @@ def test_config_c2_parity():
     ref = to_oracle(wl.net)
     errs = check_point(wl.net, ref, wl.X[0], wl.Lam[0])
     print("c2 rel errs y/J/H:", errs)
+
+
+@pytest.mark.slow
+def test_config_c3_batched_parity():
+    """c3: B=64 points of c2's net in one batched call; the first, a middle
+    and the last point are checked against the oracle; every point's H is
+    exactly symmetric."""
+    wl = configs.make("c3")
+    ref = to_oracle(wl.net)
+    Y, J, H = wl.net.oracle_batched(wl.X, wl.Lam)
+    assert Y.shape == (64, 10) and J.shape == (64, 10, 784) and H.shape == (64, 784, 784)
+    for b in (0, 31, 63):
+        assert orc.rel_err(Y[b], ref.forward(wl.X[b])) <= TOL
+        assert orc.rel_err(J[b], ref.jacobian(wl.X[b])) <= TOL
+        assert orc.rel_err(H[b], ref.lagrangian_hessian(wl.X[b], wl.Lam[b])) <= TOL
+    assert np.array_equal(H, H.transpose(0, 2, 1))
+
+
+def test_config_c4_contingency_parity():
+    """c4: K=4096 contingencies (shared 108-[1024]x3-1 net) in one call;
+    a sample of contingencies against the oracle."""
+    wl = configs.make("c4")
+    ref = to_oracle(wl.net)
+    Y, J, H = wl.net.oracle_batched(wl.X, wl.Lam)
+    assert Y.shape == (4096, 1) and J.shape == (4096, 1, 108) and H.shape == (4096, 108, 108)
+    for k in (0, 1, 777, 2048, 4095):
+        assert orc.rel_err(Y[k], ref.forward(wl.X[k])) <= TOL
+        assert orc.rel_err(J[k], ref.jacobian(wl.X[k])) <= TOL
+        assert orc.rel_err(H[k], ref.lagrangian_hessian(wl.X[k], wl.Lam[k])) <= TOL
+
+
+def test_config_c5_deep_chain_parity():
+    wl = configs.make("c5")
+    ref = to_oracle(wl.net)
+    Y, J, H = wl.net.oracle_batched(wl.X, wl.Lam)
+    for b in (0, 15):
+        assert orc.rel_err(Y[b], ref.forward(wl.X[b])) <= TOL
+        assert orc.rel_err(J[b], ref.jacobian(wl.X[b])) <= TOL
+        assert orc.rel_err(H[b], ref.lagrangian_hessian(wl.X[b], wl.Lam[b])) <= TOL
+
+
+@pytest.mark.slow
+def test_c2_full_size_properties():
+    """Size-independent properties at BASELINE's full size (c2): linearity in
+    lambda, gradient = J^T lambda, exact symmetry, batch == single."""
+    wl = configs.make("c2")
+    net = wl.net
+    x = wl.X[0]
+    rng = np.random.default_rng(3)
+    l1, l2 = rng.normal(0, 1, 10), rng.normal(0, 1, 10)
+    a, b = 0.37, -2.25
+    h1 = net.lagrangian_hessian(x, l1)
+    h2 = net.lagrangian_hessian(x, l2)
+    hc = net.lagrangian_hessian(x, a * l1 + b * l2)
+    assert orc.rel_err(hc, a * h1 + b * h2) <= 1e-12
+    assert np.array_equal(hc, hc.T)
+    j = net.jacobian(x)
+    g = net.lagrangian_gradient(x, l1)
+    assert orc.rel_err(g, j.T @ l1) <= 1e-12
+    Y, J, H = net.oracle_batched(np.stack([x, x]), np.stack([l1, l1]))
+    assert np.array_equal(H[0], h1) and np.array_equal(H[1], h1) and np.array_equal(J[0], j)
+
+
+def test_device_pointer_entry_and_launch_count():
+    import torch
+    net = gb.random_net([40, 64, 48, 6], "softplus", "sigmoid", 5).bind_device(0)
+    rng = np.random.default_rng(2)
+    X = rng.uniform(0, 1, (3, 40))
+    L = rng.normal(0, 1, (3, 6))
+    Y, J, H = net.oracle_batched(X, L)
+    dev = torch.device("cuda", 0)
+    Xd, Ld = torch.from_numpy(X).to(dev), torch.from_numpy(L).to(dev)
+    Yd = torch.empty(3, 6, dtype=torch.float64, device=dev)
+    Jd = torch.empty(3, 6, 40, dtype=torch.float64, device=dev)
+    Hd = torch.empty(3, 40, 40, dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream(dev)
+    net.oracle_batched_device(3, Xd.data_ptr(), Ld.data_ptr(), Yd.data_ptr(), Jd.data_ptr(), Hd.data_ptr(),
+                              s.cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(Yd.cpu().numpy(), Y) and np.array_equal(Jd.cpu().numpy(), J)
+    assert np.array_equal(Hd.cpu().numpy(), H)
+    assert net.last_launch_count > 5
+
+
+def test_nonfinite_input_propagates_like_reference():
+    """The reference oracle does not check x (nn.cpp:105-111 checks only the
+    length): a NaN input yields NaN outputs, not an error."""
+    net = gb.random_net([4, 5, 2], "tanh", "linear", 3)
+    y = net.forward(np.array([np.nan, 0, 0, 0]))
+    assert np.isnan(y).all()
