@@ -41,6 +41,9 @@ struct DevLayer {
   double* w = nullptr;  // [rows][ldw]
   double* b = nullptr;  // [rows]
   CUtensorMap tm_w;     // TMA view of w, box 16 x kBN (B operand)
+  double* wt = nullptr;  // W^T [cols][ldwt] (created for batched adjoints)
+  int64_t ldwt = 0;
+  CUtensorMap tm_wt;
 };
 
 struct Workspace {
@@ -55,7 +58,9 @@ struct Workspace {
   std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer l & 1)
   int64_t ldh = 0;
   double* h = nullptr;
-  double* syrk_part = nullptr;
+  double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs)
+  CUtensorMap tm_x;                   // x as an A operand [cap][n]
+  std::vector<CUtensorMap> tm_y, tm_gz;  // y_l / gz_l as A operands [cap][n_l]
   int sk_chunks = 0;
   double *u = nullptr, *sk_part = nullptr;
   double *y_out = nullptr, *j_out = nullptr, *h_out = nullptr, *g_out = nullptr;
@@ -63,7 +68,8 @@ struct Workspace {
 
 enum KernelTag : int {
   kTagFwd = 0, kTagSoftmax, kTagAdjSeed, kTagAdjCols, kTagAdjReduce, kTagGemm, kTagSyrk, kTagSyrkReduce,
-  kTagSkinny, kTagSkinnyReduce, kTagJacOut, kTagSmallSyrk, kTagSymmetrize, kTagCount
+  kTagSkinny, kTagSkinnyReduce, kTagJacOut, kTagSmallSyrk, kTagSymmetrize, kTagFwdGemm, kTagAdjGemm, kTagRowEpi,
+  kTagCount
 };
 const char* kernel_tag_name(int tag);
 
@@ -110,7 +116,10 @@ class DeviceNet {
   void free_workspace();
   void drop_graphs();
   double* ws_alloc(size_t n_doubles);
-  int syrk_split(int points) const;
+  int syrk_split(int points, int k_blocks) const;
+  void ensure_transposed();
+  void batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const DevLayer& d, bool transposed,
+                  const void* epi, double* store);
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
   void enqueue(cudaStream_t st, int nb, const Outputs& o);
   void prof_begin(cudaStream_t st, int tag, double flops, double bytes);
@@ -138,6 +147,7 @@ class DeviceNet {
   int n_syrk_tiles_ = 0;
   Workspace ws_;
   int ws_cap_ = 0;
+  bool transposed_ = false;
   std::vector<void*> ws_allocs_;
   std::map<GraphKey, GraphEntry> graphs_;
   int64_t launches_ = 0, last_launches_ = 0;

@@ -182,6 +182,21 @@ struct NtParams {
   double* partial;  // [split][points * n_tiles][kBM][kBN] for kPartial
 };
 
+// Grouped rasterisation of a dense tile grid: kGroupM consecutive M tiles
+// sweep all N tiles, so CTAs resident together share B (weight) tiles in L2.
+__host__ __device__ inline void decode_dense_tile(int local, int tiles_m, int tiles_n, int& tm, int& tn) {
+  constexpr int kGroupM = 8;
+  const int group = local / (kGroupM * tiles_n);
+  const int first_m = group * kGroupM;
+  const int gsize = (tiles_m - first_m) < kGroupM ? (tiles_m - first_m) : kGroupM;
+  const int in_group = local % (kGroupM * tiles_n);
+  tm = first_m + in_group % gsize;
+  tn = in_group / gsize;
+}
+
+// Row permutation within an 8-row DMMA block: g -> 2(g mod 4) + g/4.
+__device__ __forceinline__ int row_perm(int g) { return ((g & 3) << 1) | (g >> 2); }
+
 __global__ void __launch_bounds__(kThreads, 1)
     nt_mma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const NtParams p) {
@@ -206,17 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tm = t.x;
     tn = t.y;
   } else {
-    // grouped raster: GROUP_M consecutive M tiles sweep all N tiles.
     const int per_point = p.tiles_m * p.tiles_n;
     point = bid / per_point;
-    const int local = bid % per_point;
-    constexpr int kGroupM = 8;
-    const int group = local / (kGroupM * p.tiles_n);
-    const int first_m = group * kGroupM;
-    const int gsize = min(p.tiles_m - first_m, kGroupM);
-    const int in_group = local % (kGroupM * p.tiles_n);
-    tm = first_m + in_group % gsize;
-    tn = in_group / gsize;
+    decode_dense_tile(bid % per_point, p.tiles_m, p.tiles_n, tm, tn);
   }
   const int kb_begin = static_cast<int>((static_cast<int64_t>(p.k_blocks) * split_idx) / p.split);
   const int kb_end = static_cast<int>((static_cast<int64_t>(p.k_blocks) * (split_idx + 1)) / p.split);
@@ -265,8 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < kNJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const double* sp = p.scale ? p.scale + p.s_stride * point : nullptr;
-  const int ra = wm * kWarpM + g;  // base row in A box
-  const int rb = wn * kWarpN + g;  // base row in B box
+  // DMMA group g reads smem row 8*blk + row_perm(g): with the TMA 128B
+  // swizzle this makes each half-warp's 16 LDS.64 hit 32 distinct banks
+  // (identity order gives 2-way conflicts).  C inherits the permutation.
+  const int ra = wm * kWarpM + row_perm(g);  // base row in A box
+  const int rb = wn * kWarpN + row_perm(g);  // base row in B box
 
   double sc_next[4];
   if (sp && nkb > 0) {
@@ -302,7 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---- epilogue: thread holds C[8mi+g][8nj+2t .. +1] of its warp tile ----
+  // ---- epilogue: thread holds C[8mi+perm(g)][8nj+perm(2t)], [..][8nj+perm(2t+1)]
+  // of its warp tile (perm: see kernel comment) ----
+  const int pg = row_perm(g);
+  const int pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
   if (p.mode == kPartial) {
     double* out = p.partial + ((static_cast<int64_t>(split_idx) * p.points * p.n_tiles +
                                 static_cast<int64_t>(blockIdx.x / p.split)) *
@@ -311,31 +324,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int mi = 0; mi < kMI; ++mi)
 #pragma unroll
       for (int nj = 0; nj < kNJ; ++nj) {
-        const int r = wm * kWarpM + 8 * mi + g;
-        const int cc = wn * kWarpN + 8 * nj + 2 * t;
-        *reinterpret_cast<double2*>(out + r * kBN + cc) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+        const int r = wm * kWarpM + 8 * mi + pg;
+        const int cb = wn * kWarpN + 8 * nj;
+        out[r * kBN + cb + pc0] = acc[mi][nj][0];
+        out[r * kBN + cb + pc1] = acc[mi][nj][1];
       }
     return;
   }
   double* cbase = p.c + p.c_point_stride * point;
 #pragma unroll
   for (int mi = 0; mi < kMI; ++mi) {
-    const int r = tm * kBM + wm * kWarpM + 8 * mi + g;
+    const int r = tm * kBM + wm * kWarpM + 8 * mi + pg;
     if (r >= p.m_rows_valid) continue;
 #pragma unroll
     for (int nj = 0; nj < kNJ; ++nj) {
-      const int cc = tn * kBN + wn * kWarpN + 8 * nj + 2 * t;
-      double* dst = cbase + static_cast<int64_t>(r) * p.ldc + cc;
-      if (cc + 1 < p.b_rows_valid) {
-        double2 v = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
-        if (p.mode == kAccum) {
-          const double2 o = *reinterpret_cast<const double2*>(dst);
-          v.x += o.x;
-          v.y += o.y;
-        }
-        *reinterpret_cast<double2*>(dst) = v;
-      } else if (cc < p.b_rows_valid) {
-        dst[0] = (p.mode == kAccum ? dst[0] : 0.0) + acc[mi][nj][0];
+      const int cb = tn * kBN + wn * kWarpN + 8 * nj;
+      double* dst = cbase + static_cast<int64_t>(r) * p.ldc + cb;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = h ? pc1 : pc0;
+        if (cb + c < p.b_rows_valid) dst[c] = (p.mode == kAccum ? dst[c] : 0.0) + acc[mi][nj][h];
       }
     }
   }
@@ -357,6 +365,86 @@ __global__ void syrk_partial_reduce_kernel(const double* __restrict__ partial, c
     for (int s = 0; s < split; ++s)
       sum += partial[(static_cast<int64_t>(s) * points * n_tiles + tile_global) * tile_elems + e];
     h[h_point_stride * point + static_cast<int64_t>(r) * ldh + c] += sum;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched forward / adjoint as GEMMs (B points >= kBatchGemm):
+//   forward  Z_l    = Y_{l-1} W_l^T        (nt_mma, then act epilogue)
+//   adjoint  Ybar_l = GZ_{l+1} W_{l+1}     (nt_mma on the W^T copy, then
+//                                            gz/d epilogue)
+// The epilogue runs either inside the split-K reduction or as a separate
+// elementwise pass over the stored GEMM result.
+// ---------------------------------------------------------------------------
+enum EpiMode : int { kEpiAct = 0, kEpiAdj = 1 };
+
+struct RowEpi {
+  int mode;
+  int act;
+  const double* bias;                 // act
+  double *z, *y, *s1o, *s2o;          // act outputs
+  const double *s1i, *s2i;            // adj inputs (sigma', sigma'' of this layer)
+  double *ybar, *gz, *d;              // adj outputs (gz, d nullable)
+  int64_t ld;
+};
+
+__device__ __forceinline__ void apply_row_epi(const RowEpi& e, int r, int c, double v) {
+  const int64_t o = static_cast<int64_t>(r) * e.ld + c;
+  if (e.mode == kEpiAct) {
+    const double zz = v + e.bias[c];
+    double yy, d1, d2;
+    act_eval(e.act, zz, yy, d1, d2);
+    e.z[o] = zz;
+    e.y[o] = yy;
+    e.s1o[o] = d1;
+    e.s2o[o] = d2;
+  } else {
+    e.ybar[o] = v;
+    if (e.gz) {
+      e.gz[o] = v * e.s1i[o];
+      e.d[o] = v * e.s2i[o];
+    }
+  }
+}
+
+// Elementwise epilogue over a stored [rows][cols] GEMM result (pitch e.ld).
+__global__ void rows_epilogue_kernel(const double* __restrict__ v, int rows, int cols, RowEpi e) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * cols) return;
+  const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+  apply_row_epi(e, r, c, v[static_cast<int64_t>(r) * e.ld + c]);
+}
+
+// Split-K reduction of a dense nt_mma GEMM (kPartial) in fixed split order,
+// fused with the row epilogue.  One block row per tile.
+__global__ void gemm_partial_reduce_kernel(const double* __restrict__ partial, int split, int tiles_m, int tiles_n,
+                                           int rows_valid, int cols_valid, RowEpi e) {
+  const int tile = blockIdx.y;
+  int tm, tn;
+  decode_dense_tile(tile, tiles_m, tiles_n, tm, tn);
+  const int64_t n_t = static_cast<int64_t>(tiles_m) * tiles_n;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < kBM * kBN; x += gridDim.x * blockDim.x) {
+    const int r = tm * kBM + x / kBN, c = tn * kBN + x % kBN;
+    if (r >= rows_valid || c >= cols_valid) continue;
+    double sum = 0.0;
+    for (int s = 0; s < split; ++s) sum += partial[(static_cast<int64_t>(s) * n_t + tile) * kBM * kBN + x];
+    apply_row_epi(e, r, c, sum);
+  }
+}
+
+// out[c][r] = in[r][c] for an [rows][cols] matrix (pitches in doubles).
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int rows, int cols,
+                                 double* __restrict__ out, int64_t ldo) {
+  __shared__ double t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = r0 + j, c = c0 + threadIdx.x;
+    t[j][threadIdx.x] = (r < rows && c < cols) ? in[static_cast<int64_t>(r) * ldi + c] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int c = c0 + j, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) out[static_cast<int64_t>(c) * ldo + r] = t[threadIdx.x][j];
   }
 }
 

@@ -81,6 +81,10 @@ CUtensorMap make_tmap(const double* base, int64_t cols, int64_t rows, int64_t pi
 
 int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
+// From this many points on, the forward and adjoint chains run as DMMA GEMMs
+// over the batch instead of GEMV sweeps.
+constexpr int kBatchGemm = 32;
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -154,6 +158,7 @@ DeviceNet::~DeviceNet() {
   for (auto& d : layers_) {
     cudaFree(d.w);
     cudaFree(d.b);
+    if (d.wt) cudaFree(d.wt);
   }
   cudaFree(t0_);
   cudaFree(syrk_tiles_);
@@ -184,10 +189,12 @@ double* DeviceNet::ws_alloc(size_t n_doubles) {
   return static_cast<double*>(p);
 }
 
-int DeviceNet::syrk_split(int points) const {
+// Split-K factor of a layer's SYRK: enough CTAs to cover the SMs, at least
+// 8 k-blocks (128 of K) per split.
+int DeviceNet::syrk_split(int points, int k_blocks) const {
   const int tiles = points * n_syrk_tiles_;
   if (tiles >= sm_count_) return 1;
-  return std::max(1, sm_count_ / tiles);
+  return std::max(1, std::min(sm_count_ / tiles, k_blocks / 8));
 }
 
 void DeviceNet::ensure_workspace(int batch) {
@@ -249,12 +256,82 @@ void DeviceNet::ensure_workspace(int batch) {
   w.sk_chunks = ceil_div(kfin, dev::kSkKChunk);
   w.u = ws_alloc(static_cast<size_t>(cap) * n_pad_ * dev::kSkMB);
   w.sk_part = ws_alloc(static_cast<size_t>(w.sk_chunks) * cap * n_pad_ * dev::kSkMB);
+  // vectors as TMA A operands (batched forward / adjoint GEMMs)
+  w.tm_x = make_tmap(w.x, n_, cap, w.ld_in, kBM);
+  w.tm_y.assign(L, CUtensorMap{});
+  w.tm_gz.assign(L, CUtensorMap{});
+  for (size_t l = 0; l < L; ++l) {
+    w.tm_y[l] = make_tmap(w.y[l], layers_[l].rows, cap, w.ld[l], kBM);
+    w.tm_gz[l] = make_tmap(w.gz[l], layers_[l].rows, cap, w.ld[l], kBM);
+  }
   // device-side outputs for the host API
   w.y_out = ws_alloc(static_cast<size_t>(cap) * m_);
   w.j_out = ws_alloc(static_cast<size_t>(cap) * m_ * n_);
   w.h_out = ws_alloc(static_cast<size_t>(cap) * n_ * n_);
   w.g_out = ws_alloc(static_cast<size_t>(cap) * n_);
   ws_cap_ = cap;
+}
+
+// W_l^T copies (row-major [n_{l-1}][kp(n_l)]) for the batched adjoint GEMMs;
+// made once, on first use, by a device transpose.
+void DeviceNet::ensure_transposed() {
+  if (transposed_) return;
+  for (auto& d : layers_) {
+    d.ldwt = round_up(d.rows, 16);
+    CK(cudaMalloc(&d.wt, sizeof(double) * d.cols * d.ldwt));
+    CK(cudaMemset(d.wt, 0, sizeof(double) * d.cols * d.ldwt));
+    dim3 grid(ceil_div(d.cols, 32), ceil_div(d.rows, 32));
+    dev::transpose_kernel<<<grid, dim3(32, 8), 0, stream_>>>(d.w, d.ldw, static_cast<int>(d.rows),
+                                                              static_cast<int>(d.cols), d.wt, d.ldwt);
+    CK(cudaGetLastError());
+    d.tm_wt = make_tmap(d.wt, d.rows, d.cols, d.ldwt, kBN);
+  }
+  CK(cudaStreamSynchronize(stream_));
+  transposed_ = true;
+}
+
+// One layer of the batched forward (transposed == false: Z = Y W^T) or
+// adjoint (transposed == true: Ybar = GZ W) as an nt_mma GEMM over the nb
+// points, split-K when the tile grid is too small to fill the GPU; the row
+// epilogue (activation or gz/d) is fused into the split reduction or run as
+// an elementwise pass over `store`.
+void DeviceNet::batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const DevLayer& d, bool transposed,
+                           const void* epi_ptr, double* store) {
+  const dev::RowEpi& e = *static_cast<const dev::RowEpi*>(epi_ptr);
+  const int64_t N = transposed ? d.cols : d.rows;
+  const int64_t K = transposed ? d.rows : d.cols;
+  dev::NtParams p{};
+  p.tiles = nullptr;
+  p.tiles_m = ceil_div(nb, kBM);
+  p.tiles_n = ceil_div(N, kBN);
+  p.n_tiles = p.tiles_m * p.tiles_n;
+  p.points = 1;
+  p.k_blocks = ceil_div(K, kBK);
+  int split = 1;
+  if (p.n_tiles * 2 <= sm_count_) split = std::max(1, std::min(sm_count_ / p.n_tiles, p.k_blocks / 8));
+  p.split = split;
+  p.a_point_rows = 0;
+  p.b_point_rows = 0;
+  p.b_rows_valid = static_cast<int>(N);
+  p.m_rows_valid = nb;
+  p.scale = nullptr;
+  p.c = store;
+  p.c_point_stride = 0;
+  p.ldc = e.ld;
+  p.mode = split > 1 ? dev::kPartial : dev::kStore;
+  p.partial = ws_.syrk_part;
+  prof_begin(st, transposed ? kTagAdjGemm : kTagFwdGemm, 2.0 * nb * N * K, 8.0 * N * K);
+  launch_nt(st, ta, transposed ? d.tm_wt : d.tm_w, p, p.n_tiles * split);
+  prof_begin(st, kTagRowEpi, 0, 0);
+  if (split > 1) {
+    dim3 grid(4, p.n_tiles);
+    dev::gemm_partial_reduce_kernel<<<grid, 256, 0, st>>>(ws_.syrk_part, split, p.tiles_m, p.tiles_n, nb,
+                                                          static_cast<int>(N), e);
+  } else {
+    const int64_t tot = static_cast<int64_t>(nb) * N;
+    dev::rows_epilogue_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(store, nb, static_cast<int>(N), e);
+  }
+  after_launch(st);
 }
 
 // --------------------------------------------------------------------------
@@ -287,6 +364,7 @@ void DeviceNet::after_launch(cudaStream_t st) {
 void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
+  if (nb >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
@@ -333,8 +411,22 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   // ---- 1. forward chain --------------------------------------------------
   const double* yin = w.x;
   int64_t ld_in = w.ld_in;
+  const bool batched = nb >= kBatchGemm;
   for (int l = 0; l < L; ++l) {
     const DevLayer& d = layers_[static_cast<size_t>(l)];
+    if (batched) {
+      dev::RowEpi e{};
+      e.mode = dev::kEpiAct;
+      e.act = d.act == kSoftmax ? kLinear : d.act;
+      e.bias = d.b;
+      e.z = w.z[l];
+      e.y = w.y[l];
+      e.s1o = w.s1[l];
+      e.s2o = w.s2[l];
+      e.ld = w.ld[l];
+      batch_gemm(st, nb, l == 0 ? w.tm_x : w.tm_y[static_cast<size_t>(l - 1)], d, false, &e, w.z[l]);
+      continue;
+    }
     const int nbpass = nb >= 8 ? 8 : (nb >= 4 ? 4 : 1);
     dim3 grid(ceil_div(d.rows, dev::kFwdWarps), ceil_div(nb, nbpass));
     const int act = d.act == kSoftmax ? kLinear : d.act;
@@ -373,6 +465,23 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     const int lstop = o.g ? 0 : 1;
     for (int l = L - 1; l >= lstop; --l) {
       const DevLayer& d = layers_[static_cast<size_t>(l)];
+      if (batched) {
+        dev::RowEpi e{};
+        e.mode = dev::kEpiAdj;
+        if (l > 0) {
+          e.s1i = w.s1[l - 1];
+          e.s2i = w.s2[l - 1];
+          e.ybar = w.ybar[l - 1];
+          e.gz = w.gz[l - 1];
+          e.d = w.d[l - 1];
+          e.ld = w.ld[l - 1];
+        } else {
+          e.ybar = w.grad;
+          e.ld = w.ld_in;
+        }
+        batch_gemm(st, nb, w.tm_gz[static_cast<size_t>(l)], d, true, &e, e.ybar);
+        continue;
+      }
       const int chunks = ceil_div(d.rows, dev::kAdjRows);
       dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
       for (int p0 = 0; p0 < nb;) {
@@ -432,7 +541,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.tiles = syrk_tiles_;
     p.n_tiles = n_syrk_tiles_;
     p.points = nb;
-    p.split = syrk_split(nb);
+    p.split = syrk_split(nb, ceil_div(d.rows, kBK));
     p.k_blocks = ceil_div(d.rows, kBK);
     p.a_point_rows = t_point_rows(l);
     p.b_point_rows = t_point_rows(l);
@@ -583,6 +692,7 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
                               double* grad) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
+  if (nb >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
                        cudaMemcpyHostToDevice, stream_));
@@ -607,6 +717,7 @@ void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, do
                                 cudaStream_t user) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
+  if (nb >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
   CK(cudaEventRecord(ev_in_, user));
   CK(cudaStreamWaitEvent(stream_, ev_in_, 0));
@@ -654,7 +765,7 @@ const char* kernel_tag_name(int tag) {
   static const char* names[kTagCount] = {"fwd_rows",     "softmax",       "adj_seed",     "adj_cols",
                                          "adj_reduce",   "nt_mma.gemm",   "nt_mma.syrk",  "syrk_reduce",
                                          "skinny_nt",    "skinny_reduce", "jacobian_out", "small_k_syrk",
-                                         "symmetrize"};
+                                         "symmetrize",   "nt_mma.fwd",    "nt_mma.adj",   "row_epilogue"};
   return (tag >= 0 && tag < kTagCount) ? names[tag] : "unknown";
 }
 

@@ -221,8 +221,11 @@ def test_c2_full_size_properties():
     j = net.jacobian(x)
     g = net.lagrangian_gradient(x, l1)
     assert orc.rel_err(g, j.T @ l1) <= 1e-12
+    # Batching may change the SYRK's split-K factor (and so the summation
+    # order of H at the rounding level); y and J are batch-invariant bitwise.
     Y, J, H = net.oracle_batched(np.stack([x, x]), np.stack([l1, l1]))
-    assert np.array_equal(H[0], h1) and np.array_equal(H[1], h1) and np.array_equal(J[0], j)
+    assert np.array_equal(J[0], j) and np.array_equal(J[1], j)
+    assert np.array_equal(H[0], H[1]) and orc.rel_err(H[0], h1) <= 1e-13
 
 
 def test_device_pointer_entry_and_launch_count():
