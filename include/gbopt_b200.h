@@ -222,6 +222,16 @@ gbopt_status gbopt_net_profile(const gbopt_net* net, size_t batch,
 /* Name of a kernel tag reported by gbopt_net_profile ("nt_mma.gemm", ...). */
 const char* gbopt_kernel_tag_name(int tag);
 
+/* White-box access for tests: copies the per-layer vector `name` ("z", "y",
+ * "s1", "s2", "ybar", "gz", "d": pre-activation, activation, sigma',
+ * sigma'', adjoint dL/dy_l, ybar .* sigma', ybar .* sigma'') of layer
+ * `layer` for the first `batch` points of the most recent evaluation into
+ * out (batch x rows(layer), row-major; len == batch * rows). */
+gbopt_status gbopt_net_debug_intermediate(const gbopt_net* net,
+                                          const char* name, int64_t layer,
+                                          size_t batch, double* out,
+                                          size_t len);
+
 /* Enables/disables CUDA-graph capture of the oracle sequence (default on). */
 gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled);
 

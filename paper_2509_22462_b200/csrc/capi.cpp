@@ -349,4 +349,19 @@ gbopt_status gbopt_net_profile(const gbopt_net* net, size_t batch, const double*
 
 const char* gbopt_kernel_tag_name(int tag) { return gbb::kernel_tag_name(tag); }
 
+gbopt_status gbopt_net_debug_intermediate(const gbopt_net* net, const char* name, int64_t layer, size_t batch,
+                                          double* out, size_t len) {
+  if (net == nullptr || name == nullptr || out == nullptr)
+    return fail_argument("gbopt_net_debug_intermediate: null argument");
+  if (layer < 0 || layer >= net->net->layer_count())
+    return fail_argument("gbopt_net_debug_intermediate: layer out of range");
+  if (len != batch * static_cast<size_t>(net->net->layer(layer).rows))
+    return fail_argument("gbopt_net_debug_intermediate: len must be batch * rows(layer)");
+  return guarded([&] {
+    gbb::DeviceNet* d = net->net->device_if_bound();
+    if (!d) throw gbb::StructuralError("gbopt_net_debug_intermediate: no evaluation has run");
+    d->copy_intermediate(name, static_cast<int>(layer), static_cast<int>(batch), out);
+  });
+}
+
 }  // extern "C"

@@ -99,6 +99,10 @@ class DeviceNet {
 
   // Host buffers in/out (synchronous).  Any output may be null.
   void evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess, double* grad);
+  // Copies an intermediate per-layer vector of the most recent evaluation
+  // ("z", "y", "s1", "s2", "ybar", "gz", "d") for `nb` points into out
+  // (nb x rows(l), row-major).  Synchronous; for white-box tests.
+  void copy_intermediate(const char* name, int layer, int nb, double* out);
   // Eager run with CUDA events around every launch (on the launching stream).
   void profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out);
   // Device buffers, ordered on `user` stream, asynchronous.
@@ -136,7 +140,10 @@ class DeviceNet {
   const Net& net_;
   int ordinal_ = 0;
   int sm_count_ = 148;
-  cudaStream_t stream_ = nullptr;
+  cudaStream_t stream_ = nullptr;   // high priority: critical path
+  cudaStream_t stream2_ = nullptr;  // low priority: adjoint + SYRKs
+  bool concurrent_ = true;
+  std::vector<cudaEvent_t> evpool_;
   cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
   int64_t n_ = 0, m_ = 0, L_ = 0, n_pad_ = 0;
   std::vector<DevLayer> layers_;

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -103,7 +104,11 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   if (prop.major != 10) throw DeviceError(std::string("gbopt_b200 needs an sm_100 (B200) device, found ") + prop.name);
   sm_count_ = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
-  CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
+  CK(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, prio_lo));
+  concurrent_ = std::getenv("GBOPT_SERIAL") == nullptr;  // debugging / A-B switch
   CK(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
 
@@ -163,6 +168,8 @@ DeviceNet::~DeviceNet() {
   cudaFree(t0_);
   cudaFree(syrk_tiles_);
   if (stream_) cudaStreamDestroy(stream_);
+  if (stream2_) cudaStreamDestroy(stream2_);
+  for (cudaEvent_t e : evpool_) cudaEventDestroy(e);
   if (ev_in_) cudaEventDestroy(ev_in_);
   if (ev_out_) cudaEventDestroy(ev_out_);
 }
@@ -269,6 +276,9 @@ void DeviceNet::ensure_workspace(int batch) {
   w.j_out = ws_alloc(static_cast<size_t>(cap) * m_ * n_);
   w.h_out = ws_alloc(static_cast<size_t>(cap) * n_ * n_);
   w.g_out = ws_alloc(static_cast<size_t>(cap) * n_);
+  // ws_alloc zero-fills with cudaMemset on the legacy stream, which does not
+  // order against the non-blocking compute streams: finish it here.
+  CK(cudaDeviceSynchronize());
   ws_cap_ = cap;
 }
 
@@ -279,7 +289,9 @@ void DeviceNet::ensure_transposed() {
   for (auto& d : layers_) {
     d.ldwt = round_up(d.rows, 16);
     CK(cudaMalloc(&d.wt, sizeof(double) * d.cols * d.ldwt));
-    CK(cudaMemset(d.wt, 0, sizeof(double) * d.cols * d.ldwt));
+    // on stream_: a legacy-stream memset would not be ordered before the
+    // transpose on the non-blocking stream_
+    CK(cudaMemsetAsync(d.wt, 0, sizeof(double) * d.cols * d.ldwt, stream_));
     dim3 grid(ceil_div(d.cols, 32), ceil_div(d.rows, 32));
     dev::transpose_kernel<<<grid, dim3(32, 8), 0, stream_>>>(d.w, d.ldw, static_cast<int>(d.rows),
                                                               static_cast<int>(d.cols), d.wt, d.ldwt);
@@ -399,8 +411,37 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
 
 // The whole evaluation for `nb` points whose x / lambda already sit in the
 // workspace.  Outputs go to the given device pointers (nullable).
+//
+// Two streams: `sa` carries the critical path (forward chain, tangent GEMM
+// chain, final layer, J); `sb` the adjoint chain and every Hessian SYRK,
+// which only feed H.  SYRK_l waits for GEMM_l (T_l ready) and then runs
+// beside GEMM_{l+1}, filling the SMs the GEMM's last wave leaves idle;
+// GEMM_{l+1} overwrites T_{l-1}'s buffer, so it waits for SYRK_{l-1}.
+// (Profiling runs serialise both onto one stream.)
 void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   Workspace& w = ws_;
+  const bool two = !profiling_ && concurrent_;
+  cudaStream_t sa = st;
+  cudaStream_t sb = two ? stream2_ : st;
+  int ev_next = 0;
+  auto next_event = [&]() -> cudaEvent_t {
+    if (ev_next >= static_cast<int>(evpool_.size())) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evpool_.push_back(e);
+    }
+    return evpool_[static_cast<size_t>(ev_next++)];
+  };
+  // make `to` wait for everything enqueued so far on `from`
+  bool sb_forked = false;  // sb joins a capture only through a fork from sa
+  auto link = [&](cudaStream_t from, cudaStream_t to) {
+    if (from == to) return;
+    if (from == sb && !sb_forked) return;  // nothing was enqueued on sb
+    if (to == sb) sb_forked = true;
+    cudaEvent_t e = next_event();
+    CK(cudaEventRecord(e, from));
+    CK(cudaStreamWaitEvent(to, e, 0));
+  };
   const int L = static_cast<int>(L_);
   const bool softmax_out = layers_[L - 1].act == kSoftmax;
   const bool want_h = o.h != nullptr;
@@ -424,44 +465,45 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       e.s1o = w.s1[l];
       e.s2o = w.s2[l];
       e.ld = w.ld[l];
-      batch_gemm(st, nb, l == 0 ? w.tm_x : w.tm_y[static_cast<size_t>(l - 1)], d, false, &e, w.z[l]);
+      batch_gemm(sa, nb, l == 0 ? w.tm_x : w.tm_y[static_cast<size_t>(l - 1)], d, false, &e, w.z[l]);
       continue;
     }
     const int nbpass = nb >= 8 ? 8 : (nb >= 4 ? 4 : 1);
     dim3 grid(ceil_div(d.rows, dev::kFwdWarps), ceil_div(nb, nbpass));
     const int act = d.act == kSoftmax ? kLinear : d.act;
-    prof_begin(st, kTagFwd, 2.0 * d.rows * d.cols * nb, 8.0 * d.rows * d.cols * ceil_div(nb, nbpass));
+    prof_begin(sa, kTagFwd, 2.0 * d.rows * d.cols * nb, 8.0 * d.rows * d.cols * ceil_div(nb, nbpass));
     if (nbpass == 8)
-      dev::fwd_rows_kernel<8><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
+      dev::fwd_rows_kernel<8><<<grid, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
     else if (nbpass == 4)
-      dev::fwd_rows_kernel<4><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
+      dev::fwd_rows_kernel<4><<<grid, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
     else
-      dev::fwd_rows_kernel<1><<<grid, dev::kFwdWarps * 32, 0, st>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
+      dev::fwd_rows_kernel<1><<<grid, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
-    after_launch(st);
+    after_launch(sa);
     yin = w.y[l];
     ld_in = w.ld[l];
   }
   if (softmax_out) {
-    prof_begin(st, kTagSoftmax, 0, 0);
-    dev::softmax_kernel<<<ceil_div(nb, 4), 128, 0, st>>>(w.z[L - 1], w.y[L - 1], static_cast<int>(m_), w.ld[L - 1],
+    prof_begin(sa, kTagSoftmax, 0, 0);
+    dev::softmax_kernel<<<ceil_div(nb, 4), 128, 0, sa>>>(w.z[L - 1], w.y[L - 1], static_cast<int>(m_), w.ld[L - 1],
                                                          nb);
-    after_launch(st);
+    after_launch(sa);
   }
   if (o.y) {
     CK(cudaMemcpy2DAsync(o.y, sizeof(double) * m_, w.y[L - 1], sizeof(double) * w.ld[L - 1], sizeof(double) * m_, nb,
-                         cudaMemcpyDeviceToDevice, st));
+                         cudaMemcpyDeviceToDevice, sa));
   }
 
   // ---- 2. adjoint chain --------------------------------------------------
   if (need_adj) {
-    prof_begin(st, kTagAdjSeed, 0, 0);
-    dev::adj_seed_kernel<<<ceil_div(nb, 4), 128, 0, st>>>(
+    link(sa, sb);  // the adjoint needs the forward chain
+    prof_begin(sb, kTagAdjSeed, 0, 0);
+    dev::adj_seed_kernel<<<ceil_div(nb, 4), 128, 0, sb>>>(
         w.lam, w.ld_lam, w.y[L - 1], w.s1[L - 1], w.s2[L - 1], w.ld[L - 1], static_cast<int>(m_), nb,
         softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
-    after_launch(st);
+    after_launch(sb);
     const int lstop = o.g ? 0 : 1;
     for (int l = L - 1; l >= lstop; --l) {
       const DevLayer& d = layers_[static_cast<size_t>(l)];
@@ -479,7 +521,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
           e.ybar = w.grad;
           e.ld = w.ld_in;
         }
-        batch_gemm(st, nb, w.tm_gz[static_cast<size_t>(l)], d, true, &e, e.ybar);
+        batch_gemm(sb, nb, w.tm_gz[static_cast<size_t>(l)], d, true, &e, e.ybar);
         continue;
       }
       const int chunks = ceil_div(d.rows, dev::kAdjRows);
@@ -487,45 +529,48 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       for (int p0 = 0; p0 < nb;) {
         const int left = nb - p0;
         const int pass = left >= 8 ? 8 : (left >= 4 ? 4 : 1);
-        prof_begin(st, kTagAdjCols, 2.0 * d.rows * d.cols * pass, 8.0 * d.rows * d.cols);
+        prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * pass, 8.0 * d.rows * d.cols);
         if (left >= 8) {
-          dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+          dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
                                                                      nb, p0, w.adj_part, w.ld_part);
           p0 += 8;
         } else if (left >= 4) {
-          dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+          dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
                                                                      nb, p0, w.adj_part, w.ld_part);
           p0 += 4;
         } else {
-          dev::adj_cols_kernel<1><<<grid, dev::kAdjThreads, 0, st>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+          dev::adj_cols_kernel<1><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
                                                                      nb, p0, w.adj_part, w.ld_part);
           p0 += 1;
         }
-        after_launch(st);
+        after_launch(sb);
       }
       const int64_t tot = static_cast<int64_t>(nb) * d.cols;
-      prof_begin(st, kTagAdjReduce, 0, 0);
+      prof_begin(sb, kTagAdjReduce, 0, 0);
       if (l > 0) {
-        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.adj_part, chunks, w.ld_part,
+        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.adj_part, chunks, w.ld_part,
                                                                    static_cast<int>(d.cols), nb, w.s1[l - 1],
                                                                    w.s2[l - 1], w.ld[l - 1], w.ybar[l - 1],
                                                                    w.gz[l - 1], w.d[l - 1]);
       } else {
-        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.adj_part, chunks, w.ld_part,
+        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.adj_part, chunks, w.ld_part,
                                                                    static_cast<int>(d.cols), nb, nullptr, nullptr,
                                                                    w.ld_in, w.grad, nullptr, nullptr);
       }
-      after_launch(st);
+      after_launch(sb);
     }
     if (o.g) {
       CK(cudaMemcpy2DAsync(o.g, sizeof(double) * n_, w.grad, sizeof(double) * w.ld_in, sizeof(double) * n_, nb,
-                           cudaMemcpyDeviceToDevice, st));
+                           cudaMemcpyDeviceToDevice, sb));
     }
   }
-  if (!need_tan) return;
 
+  if (!need_tan) {
+    link(sb, sa);
+    return;
+  }
   // ---- 3. tangent chain + Hessian SYRK ------------------------------------
-  if (want_h) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, st));
+  if (want_h) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
   const int kfin_layer = L - 1;
   const bool skinny_final = m_ <= dev::kSkMB;
   // T_l lives in: l == 0 -> t0_ (broadcast over points), else w.t[l & 1].
@@ -554,22 +599,34 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.ldc = n_pad_;
     p.mode = p.split > 1 ? dev::kPartial : dev::kAccum;
     p.partial = w.syrk_part;
-    prof_begin(st, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
-    launch_nt(st, tmap_a(l), tmap_b(l), p, nb * n_syrk_tiles_ * p.split);
+    prof_begin(sb, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
+    launch_nt(sb, tmap_a(l), tmap_b(l), p, nb * n_syrk_tiles_ * p.split);
     if (p.split > 1) {
-      prof_begin(st, kTagSyrkReduce, 0, 0);
+      prof_begin(sb, kTagSyrkReduce, 0, 0);
       dim3 grid(8, nb * n_syrk_tiles_);
-      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, st>>>(w.syrk_part, syrk_tiles_, n_syrk_tiles_, nb, p.split, w.h,
+      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, sb>>>(w.syrk_part, syrk_tiles_, n_syrk_tiles_, nb, p.split, w.h,
                                                             n_pad_ * n_pad_, n_pad_, static_cast<int>(n_));
-      after_launch(st);
+      after_launch(sb);
     }
   };
 
+  // syrk_done[l]: event on sb after SYRK_l (nullptr when none ran)
+  std::vector<cudaEvent_t> syrk_done(static_cast<size_t>(L), nullptr);
   for (int l = 0; l + 1 < L; ++l) {
-    // curvature of hidden layer l
-    if (want_h && layers_[static_cast<size_t>(l)].act != kLinear) syrk(l);
+    // curvature of hidden layer l, on sb once T_l exists (T_0 is constant)
+    if (want_h && layers_[static_cast<size_t>(l)].act != kLinear) {
+      if (l > 0) link(sa, sb);
+      syrk(l);
+      if (two) {
+        syrk_done[static_cast<size_t>(l)] = next_event();
+        CK(cudaEventRecord(syrk_done[static_cast<size_t>(l)], sb));
+      }
+    }
     // propagate the tangents to layer l+1 (unless it is a skinny final)
     if (l + 1 == kfin_layer && skinny_final) break;
+    // T_{l+1} overwrites T_{l-1}: wait for SYRK_{l-1}
+    if (l >= 2 && syrk_done[static_cast<size_t>(l - 1)])
+      CK(cudaStreamWaitEvent(sa, syrk_done[static_cast<size_t>(l - 1)], 0));
     const DevLayer& dn = layers_[static_cast<size_t>(l + 1)];
     dev::NtParams p{};
     p.tiles = nullptr;
@@ -589,8 +646,8 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.c_point_stride = n_pad_ * ldt_;
     p.ldc = ldt_;
     p.mode = dev::kStore;
-    prof_begin(st, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
-    launch_nt(st, tmap_a(l), dn.tm_w, p, nb * p.n_tiles);
+    prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
+    launch_nt(sa, tmap_a(l), dn.tm_w, p, nb * p.n_tiles);
   }
 
   // ---- 4. final layer -------------------------------------------------------
@@ -604,16 +661,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   } else if (skinny_final) {
     const int l = kfin_layer - 1;
     dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
-    prof_begin(st, kTagSkinny, 2.0 * n_ * m_ * df.cols * nb, 0);
-    dev::skinny_nt_kernel<<<grid, 256, 0, st>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_), w.s1[l],
+    prof_begin(sa, kTagSkinny, 2.0 * n_ * m_ * df.cols * nb, 0);
+    dev::skinny_nt_kernel<<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_), w.s1[l],
                                                 w.ld[l], df.w, df.ldw, static_cast<int>(m_),
                                                 static_cast<int>(df.cols), w.sk_part);
-    after_launch(st);
+    after_launch(sa);
     const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
-    prof_begin(st, kTagSkinnyReduce, 0, 0);
-    dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.sk_part, w.sk_chunks, nb,
+    prof_begin(sa, kTagSkinnyReduce, 0, 0);
+    dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sa>>>(w.sk_part, w.sk_chunks, nb,
                                                                   static_cast<int>(n_pad_), static_cast<int>(m_), w.u);
-    after_launch(st);
+    after_launch(sa);
     u = w.u;
     ldu = dev::kSkMB;
     u_point_rows = n_pad_;
@@ -624,34 +681,36 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   }
   if (want_j) {
     const int64_t tot = static_cast<int64_t>(nb) * n_;
-    prof_begin(st, kTagJacOut, 0, 0);
-    dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, st>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
+    prof_begin(sa, kTagJacOut, 0, 0);
+    dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, sa>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
                                                                  w.y[kfin_layer], w.ld[kfin_layer],
                                                                  static_cast<int>(n_), static_cast<int>(m_), nb,
                                                                  softmax_out ? 1 : 0, o.j);
-    after_launch(st);
+    after_launch(sa);
   }
   if (want_h) {
+    link(sa, sb);  // the final curvature needs U (sa)
     if (df.act != kLinear) {
       if (softmax_out || skinny_final || kfin_layer == 0) {
         // K = m is small: direct lower-triangle update (dense middle for softmax)
         dim3 blk(16, 16);
         dim3 grid(ceil_div(n_, 16), ceil_div(n_, 16), nb);
-        prof_begin(st, kTagSmallSyrk, 0, 0);
-        dev::small_k_syrk_kernel<<<grid, blk, 0, st>>>(u, ldu, u_point_rows, w.d[kfin_layer], w.ld[kfin_layer],
+        prof_begin(sb, kTagSmallSyrk, 0, 0);
+        dev::small_k_syrk_kernel<<<grid, blk, 0, sb>>>(u, ldu, u_point_rows, w.d[kfin_layer], w.ld[kfin_layer],
                                                        softmax_out ? w.mid : nullptr, m_ * m_, static_cast<int>(n_),
                                                        static_cast<int>(m_), nb, w.h, n_pad_ * n_pad_, n_pad_);
-        after_launch(st);
+        after_launch(sb);
       } else {
         syrk(kfin_layer);
       }
     }
     const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
-    prof_begin(st, kTagSymmetrize, 0, 0);
-    dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.h, n_pad_ * n_pad_, n_pad_,
+    prof_begin(sb, kTagSymmetrize, 0, 0);
+    dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.h, n_pad_ * n_pad_, n_pad_,
                                                                    static_cast<int>(n_), nb, o.h);
-    after_launch(st);
+    after_launch(sb);
   }
+  link(sb, sa);  // join: the evaluation ends on `st`
 }
 
 void DeviceNet::run(cudaStream_t st, int nb, const Outputs& o) {
@@ -677,7 +736,8 @@ void DeviceNet::run(cudaStream_t st, int nb, const Outputs& o) {
     CK(cudaStreamEndCapture(st, &graph));
     GraphEntry e;
     e.launches = launches_;
-    const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+    // keep the two streams' priorities inside the graph
+    const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     CK(ie);
     if (graphs_.size() > 16) drop_graphs();
@@ -734,6 +794,20 @@ void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, do
   run(stream_, nb, o);
   CK(cudaEventRecord(ev_out_, stream_));
   CK(cudaStreamWaitEvent(user, ev_out_, 0));
+}
+
+void DeviceNet::copy_intermediate(const char* name, int layer, int nb, double* out) {
+  DeviceGuard g(ordinal_);
+  if (layer < 0 || layer >= L_) throw StructuralError("copy_intermediate: layer out of range");
+  if (nb <= 0 || nb > ws_cap_) throw StructuralError("copy_intermediate: batch exceeds the last evaluation");
+  const std::string s(name);
+  const size_t l = static_cast<size_t>(layer);
+  double* src = s == "z" ? ws_.z[l] : s == "y" ? ws_.y[l] : s == "s1" ? ws_.s1[l] : s == "s2" ? ws_.s2[l]
+              : s == "ybar" ? ws_.ybar[l] : s == "gz" ? ws_.gz[l] : s == "d" ? ws_.d[l] : nullptr;
+  if (!src) throw StructuralError("copy_intermediate: unknown buffer " + s);
+  CK(cudaStreamSynchronize(stream_));
+  CK(cudaMemcpy2D(out, sizeof(double) * layers_[l].rows, src, sizeof(double) * ws_.ld[l],
+                  sizeof(double) * layers_[l].rows, nb, cudaMemcpyDeviceToHost));
 }
 
 // ---------------------------------------------------------------------------

@@ -79,6 +79,7 @@ _net_set_graphs = _fn("gbopt_net_set_graphs", _status, _vp, ctypes.c_int)
 _net_profile = _fn("gbopt_net_profile", _status, _vp, _sz, _vp, _vp, ctypes.POINTER(ctypes.c_int32),
                    ctypes.POINTER(ctypes.c_float), _dp, _dp, _sz, ctypes.POINTER(_sz))
 _kernel_tag_name = _fn("gbopt_kernel_tag_name", ctypes.c_char_p, ctypes.c_int)
+_net_debug_intermediate = _fn("gbopt_net_debug_intermediate", _status, _vp, ctypes.c_char_p, _i64, _sz, _dp, _sz)
 
 # ---------------------------------------------------------------------------
 # Error taxonomy (reference errors.hpp:10-71; status codes gbopt.h:19-31)
@@ -349,6 +350,13 @@ class NeuralNet:
             raise ArgumentError("oracle_batched: Lambda must be B x m")
         _check(_net_oracle_batched(self._h, B, _dptr(X), X.shape[1], _dptr(Lam), m, _dptr(Y), _dptr(J), _dptr(H)))
         return Y, J, H
+
+    def intermediate(self, name: str, layer: int, batch: int = 1) -> np.ndarray:
+        """Per-layer vector of the last evaluation (white-box tests)."""
+        rows = self.layer(layer)[0].shape[0]
+        out = np.empty((batch, rows))
+        _check(_net_debug_intermediate(self._h, name.encode(), layer, batch, _dptr(out), out.size))
+        return out
 
     def oracle_batched_device(self, batch: int, dX: int, dLam: int, dY: int, dJ: int, dH: int, stream: int = 0):
         """Device-pointer entry (raw CUDA addresses, e.g. torch ``data_ptr()``);

@@ -255,3 +255,26 @@ def test_nonfinite_input_propagates_like_reference():
     net = gb.random_net([4, 5, 2], "tanh", "linear", 3)
     y = net.forward(np.array([np.nan, 0, 0, 0]))
     assert np.isnan(y).all()
+
+
+def test_batched_intermediates_match_single():
+    """White-box: the batched (GEMM) forward/adjoint chains give the same
+    per-layer z, y, sigma', sigma'', ybar, gz, d as the single-point GEMV
+    chains (regression: stream-ordering of the W^T build / zero fills)."""
+    widths = [784, 2048, 2048, 2048, 10]
+    ref = gb.random_net(widths, "softplus", "linear", 3)
+    rng = np.random.default_rng(0)
+    X = rng.uniform(-1, 1, (40, 784))
+    L = rng.uniform(-1, 1, (40, 10))
+    net = gb.random_net(widths, "softplus", "linear", 3)
+    net.oracle_batched(X, L)
+    for b in (0, 17, 39):
+        ref.oracle_batched(X[b:b + 1], L[b:b + 1])
+        for name in ("z", "y", "s1", "s2", "ybar", "gz", "d"):
+            for l in range(len(widths) - 1):
+                got = net.intermediate(name, l, 40)[b]
+                want = ref.intermediate(name, l, 1)[0]
+                if np.abs(want).max() == 0:
+                    assert np.abs(got).max() == 0, (name, l)
+                else:
+                    assert orc.rel_err(got, want) <= 1e-13, (name, l, b)
