@@ -386,6 +386,7 @@ struct RowEpi {
   const double *s1i, *s2i;            // adj inputs (sigma', sigma'' of this layer)
   double *ybar, *gz, *d;              // adj outputs (gz, d nullable)
   int64_t ld;
+  int s_div;  // adj: rows r share the sigma' / sigma'' row r / s_div (reverse-mode J seeds); 0 == 1
 };
 
 __device__ __forceinline__ void apply_row_epi(const RowEpi& e, int r, int c, double v) {
@@ -401,8 +402,9 @@ __device__ __forceinline__ void apply_row_epi(const RowEpi& e, int r, int c, dou
   } else {
     e.ybar[o] = v;
     if (e.gz) {
-      e.gz[o] = v * e.s1i[o];
-      e.d[o] = v * e.s2i[o];
+      const int64_t os = e.s_div > 1 ? static_cast<int64_t>(r / e.s_div) * e.ld + c : o;
+      e.gz[o] = v * e.s1i[os];
+      if (e.d) e.d[o] = v * e.s2i[os];
     }
   }
 }
@@ -619,18 +621,41 @@ __global__ void __launch_bounds__(kAdjThreads)
 // When s1 == nullptr only ybar is written (the input-gradient).
 __global__ void adj_reduce_kernel(const double* __restrict__ partial, int chunks, int64_t ld_part, int k_dim, int nb,
                                   const double* __restrict__ s1, const double* __restrict__ s2, int64_t ld,
-                                  double* __restrict__ ybar, double* __restrict__ gz, double* __restrict__ d) {
+                                  double* __restrict__ ybar, double* __restrict__ gz, double* __restrict__ d,
+                                  int s_div) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= static_cast<int64_t>(nb) * k_dim) return;
   const int b = static_cast<int>(e / k_dim), k = static_cast<int>(e % k_dim);
   double sum = 0.0;
   for (int c = 0; c < chunks; ++c) sum += partial[(static_cast<int64_t>(c) * nb + b) * ld_part + k];
   const int64_t o = static_cast<int64_t>(b) * ld + k;
+  // s_div > 1: b indexes reverse-mode seed vectors, s_div per point
+  const int64_t os = static_cast<int64_t>(b / s_div) * ld + k;
   ybar[o] = sum;
   if (s1) {
-    gz[o] = sum * s1[o];
-    d[o] = sum * s2[o];
+    gz[o] = sum * s1[os];
+    if (d) d[o] = sum * s2[os];
   }
+}
+
+// Reverse-mode Jacobian seeds (nn.cpp:148-170): for point p and output i,
+// seed vector v = p*m + i is row i of d y_L / d z_L:
+//   elementwise: e_i * sigma'_L ;  softmax: y_i (e_i - y)
+// written as gz_L[v] (the adjoint chain then yields row i of J at layer 0).
+__global__ void jac_seed_kernel(const double* __restrict__ y, const double* __restrict__ s1, int64_t ld, int m,
+                                int nb, int softmax, double* __restrict__ gz) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(nb) * m * m) return;
+  const int p = static_cast<int>(e / (static_cast<int64_t>(m) * m));
+  const int i = static_cast<int>((e / m) % m), k = static_cast<int>(e % m);
+  double v;
+  if (softmax) {
+    const double yi = y[ld * p + i];
+    v = yi * ((i == k ? 1.0 : 0.0) - y[ld * p + k]);
+  } else {
+    v = i == k ? s1[ld * p + k] : 0.0;
+  }
+  gz[(static_cast<int64_t>(p) * m + i) * ld + k] = v;
 }
 
 // ---------------------------------------------------------------------------

@@ -208,6 +208,7 @@ void DeviceNet::ensure_workspace(int batch) {
   if (batch <= ws_cap_) return;
   free_workspace();
   const int cap = batch;
+  const int64_t vcap = static_cast<int64_t>(cap) * std::max<int64_t>(m_, 1);
   Workspace& w = ws_;
   const size_t L = static_cast<size_t>(L_);
   w.z.assign(L, nullptr);
@@ -225,22 +226,22 @@ void DeviceNet::ensure_workspace(int batch) {
     w.y[l] = ws_alloc(cap * ld);
     w.s1[l] = ws_alloc(cap * ld);
     w.s2[l] = ws_alloc(cap * ld);
-    w.ybar[l] = ws_alloc(cap * ld);
-    w.gz[l] = ws_alloc(cap * ld);
+    w.ybar[l] = ws_alloc(vcap * ld);  // vcap: reverse-mode J runs m vectors per point
+    w.gz[l] = ws_alloc(vcap * ld);
     w.d[l] = ws_alloc(cap * ld);
   }
   w.ld_in = round_up(n_, 16);
   w.ld_lam = round_up(m_, 16);
   w.x = ws_alloc(cap * w.ld_in);
   w.lam = ws_alloc(cap * w.ld_lam);
-  w.grad = ws_alloc(cap * w.ld_in);
+  w.grad = ws_alloc(vcap * w.ld_in);
   w.mid = ws_alloc(layers_[L - 1].act == kSoftmax ? static_cast<size_t>(cap) * m_ * m_ : 1);
   // adjoint partials: [chunks][cap][ldmax]
   int64_t rmax = 1;
   for (auto& d : layers_) rmax = std::max(rmax, d.rows);
   w.adj_chunks_max = ceil_div(rmax, dev::kAdjRows);
   w.ld_part = ldt_ > w.ld_in ? ldt_ : w.ld_in;
-  w.adj_part = ws_alloc(static_cast<size_t>(w.adj_chunks_max) * cap * w.ld_part);
+  w.adj_part = ws_alloc(static_cast<size_t>(w.adj_chunks_max) * vcap * w.ld_part);
   // tangents (only needed with >= 2 layers)
   if (L_ >= 2) {
     w.t[0] = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
@@ -269,7 +270,7 @@ void DeviceNet::ensure_workspace(int batch) {
   w.tm_gz.assign(L, CUtensorMap{});
   for (size_t l = 0; l < L; ++l) {
     w.tm_y[l] = make_tmap(w.y[l], layers_[l].rows, cap, w.ld[l], kBM);
-    w.tm_gz[l] = make_tmap(w.gz[l], layers_[l].rows, cap, w.ld[l], kBM);
+    w.tm_gz[l] = make_tmap(w.gz[l], layers_[l].rows, vcap, w.ld[l], kBM);
   }
   // device-side outputs for the host API
   w.y_out = ws_alloc(static_cast<size_t>(cap) * m_);
@@ -376,7 +377,7 @@ void DeviceNet::after_launch(cudaStream_t st) {
 void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
-  if (nb >= kBatchGemm) ensure_transposed();
+  if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
@@ -497,6 +498,65 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   }
 
   // ---- 2. adjoint chain --------------------------------------------------
+  // Reverse sweep from the seeded gz_{L-1} (nv vectors; vector v belongs to
+  // point v / s_div) down to layer `lstop`, leaving ybar/gz/d per layer and,
+  // for lstop == 0, the input-space result in w.grad (nn.cpp:172-196).
+  auto adjoint_chain = [&](int nv, int s_div, int lstop, bool want_d) {
+    const bool gemm = nv >= kBatchGemm;
+    for (int l = L - 1; l >= lstop; --l) {
+      const DevLayer& d = layers_[static_cast<size_t>(l)];
+      if (gemm) {
+        dev::RowEpi e{};
+        e.mode = dev::kEpiAdj;
+        e.s_div = s_div;
+        if (l > 0) {
+          e.s1i = w.s1[l - 1];
+          e.s2i = w.s2[l - 1];
+          e.ybar = w.ybar[l - 1];
+          e.gz = w.gz[l - 1];
+          e.d = want_d ? w.d[l - 1] : nullptr;
+          e.ld = w.ld[l - 1];
+        } else {
+          e.ybar = w.grad;
+          e.ld = w.ld_in;
+        }
+        batch_gemm(sb, nv, w.tm_gz[static_cast<size_t>(l)], d, true, &e, e.ybar);
+        continue;
+      }
+      const int chunks = ceil_div(d.rows, dev::kAdjRows);
+      dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
+      for (int p0 = 0; p0 < nv;) {
+        const int left = nv - p0;
+        const int pass = left >= 8 ? 8 : (left >= 4 ? 4 : 1);
+        prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * pass, 8.0 * d.rows * d.cols);
+        if (left >= 8) {
+          dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                     nv, p0, w.adj_part, w.ld_part);
+        } else if (left >= 4) {
+          dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                     nv, p0, w.adj_part, w.ld_part);
+        } else {
+          dev::adj_cols_kernel<1><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                     nv, p0, w.adj_part, w.ld_part);
+        }
+        p0 += pass;
+        after_launch(sb);
+      }
+      const int64_t tot = static_cast<int64_t>(nv) * d.cols;
+      prof_begin(sb, kTagAdjReduce, 0, 0);
+      if (l > 0) {
+        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(
+            w.adj_part, chunks, w.ld_part, static_cast<int>(d.cols), nv, w.s1[l - 1], w.s2[l - 1], w.ld[l - 1],
+            w.ybar[l - 1], w.gz[l - 1], want_d ? w.d[l - 1] : nullptr, s_div);
+      } else {
+        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.adj_part, chunks, w.ld_part,
+                                                                   static_cast<int>(d.cols), nv, nullptr, nullptr,
+                                                                   w.ld_in, w.grad, nullptr, nullptr, 1);
+      }
+      after_launch(sb);
+    }
+  };
+
   if (need_adj) {
     link(sa, sb);  // the adjoint needs the forward chain
     prof_begin(sb, kTagAdjSeed, 0, 0);
@@ -504,65 +564,30 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         w.lam, w.ld_lam, w.y[L - 1], w.s1[L - 1], w.s2[L - 1], w.ld[L - 1], static_cast<int>(m_), nb,
         softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
     after_launch(sb);
-    const int lstop = o.g ? 0 : 1;
-    for (int l = L - 1; l >= lstop; --l) {
-      const DevLayer& d = layers_[static_cast<size_t>(l)];
-      if (batched) {
-        dev::RowEpi e{};
-        e.mode = dev::kEpiAdj;
-        if (l > 0) {
-          e.s1i = w.s1[l - 1];
-          e.s2i = w.s2[l - 1];
-          e.ybar = w.ybar[l - 1];
-          e.gz = w.gz[l - 1];
-          e.d = w.d[l - 1];
-          e.ld = w.ld[l - 1];
-        } else {
-          e.ybar = w.grad;
-          e.ld = w.ld_in;
-        }
-        batch_gemm(sb, nb, w.tm_gz[static_cast<size_t>(l)], d, true, &e, e.ybar);
-        continue;
-      }
-      const int chunks = ceil_div(d.rows, dev::kAdjRows);
-      dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
-      for (int p0 = 0; p0 < nb;) {
-        const int left = nb - p0;
-        const int pass = left >= 8 ? 8 : (left >= 4 ? 4 : 1);
-        prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * pass, 8.0 * d.rows * d.cols);
-        if (left >= 8) {
-          dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                     nb, p0, w.adj_part, w.ld_part);
-          p0 += 8;
-        } else if (left >= 4) {
-          dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                     nb, p0, w.adj_part, w.ld_part);
-          p0 += 4;
-        } else {
-          dev::adj_cols_kernel<1><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                     nb, p0, w.adj_part, w.ld_part);
-          p0 += 1;
-        }
-        after_launch(sb);
-      }
-      const int64_t tot = static_cast<int64_t>(nb) * d.cols;
-      prof_begin(sb, kTagAdjReduce, 0, 0);
-      if (l > 0) {
-        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.adj_part, chunks, w.ld_part,
-                                                                   static_cast<int>(d.cols), nb, w.s1[l - 1],
-                                                                   w.s2[l - 1], w.ld[l - 1], w.ybar[l - 1],
-                                                                   w.gz[l - 1], w.d[l - 1]);
-      } else {
-        dev::adj_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.adj_part, chunks, w.ld_part,
-                                                                   static_cast<int>(d.cols), nb, nullptr, nullptr,
-                                                                   w.ld_in, w.grad, nullptr, nullptr);
-      }
-      after_launch(sb);
-    }
+    adjoint_chain(nb, 1, o.g ? 0 : 1, true);
     if (o.g) {
       CK(cudaMemcpy2DAsync(o.g, sizeof(double) * n_, w.grad, sizeof(double) * w.ld_in, sizeof(double) * n_, nb,
                            cudaMemcpyDeviceToDevice, sb));
     }
+  }
+
+  // J without H: reverse mode with m seed vectors per point, like the
+  // reference jacobian (nn.cpp:148-170) -- m weight sweeps instead of the
+  // n-column tangent chain.
+  if (want_j && !want_h) {
+    link(sa, sb);
+    const int nv = nb * static_cast<int>(m_);
+    const int64_t tot = static_cast<int64_t>(nb) * m_ * m_;
+    prof_begin(sb, kTagAdjSeed, 0, 0);
+    dev::jac_seed_kernel<<<ceil_div(tot, 256), 256, 0, sb>>>(w.y[L - 1], w.s1[L - 1], w.ld[L - 1],
+                                                             static_cast<int>(m_), nb, softmax_out ? 1 : 0,
+                                                             w.gz[L - 1]);
+    after_launch(sb);
+    adjoint_chain(nv, static_cast<int>(m_), 0, false);
+    CK(cudaMemcpy2DAsync(o.j, sizeof(double) * n_, w.grad, sizeof(double) * w.ld_in, sizeof(double) * n_, nv,
+                         cudaMemcpyDeviceToDevice, sb));
+    link(sb, sa);
+    return;
   }
 
   if (!need_tan) {
@@ -752,7 +777,7 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
                               double* grad) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
-  if (nb >= kBatchGemm) ensure_transposed();
+  if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
                        cudaMemcpyHostToDevice, stream_));
@@ -777,7 +802,7 @@ void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, do
                                 cudaStream_t user) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
-  if (nb >= kBatchGemm) ensure_transposed();
+  if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
   CK(cudaEventRecord(ev_in_, user));
   CK(cudaStreamWaitEvent(stream_, ev_in_, 0));

@@ -1,0 +1,112 @@
+// C++ drop-in checks: include/gbopt/nn_b200.hpp over libgbopt_b200.so.
+// Mirrors the network cases of proj/tests/test_capi.cpp and the reduced-space
+// cases of proj/tests/test_formulations.cpp:215-274.
+//   ./test_nn_b200        host-side checks (no GPU needed)
+//   ./test_nn_b200 gpu    + device checks (oracle, reduced-space callbacks)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gbopt/nn_b200.hpp"
+
+using namespace gbopt::b200;
+
+static int g_fail = 0;
+#define CHECK(c)                                                     \
+  do {                                                               \
+    if (!(c)) {                                                      \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);       \
+      ++g_fail;                                                      \
+    }                                                                \
+  } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main(int argc, char** argv) {
+  const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
+  // ---- host side ----
+  NeuralNet net = random_net({4, 6, 3}, "tanh", "softmax", 11);
+  CHECK(net.input_dim() == 4 && net.output_dim() == 3);
+  CHECK(net.param_count() == 4 * 6 + 6 + 6 * 3 + 3);
+  const std::string path = "/tmp/gbopt_b200_cpp_test.gbnn";
+  save_weights(net, path);
+  NeuralNet back = load_weights(path);
+  for (int64_t l = 0; l < net.layer_count(); ++l) {
+    Layer a = net.layer(l), b = back.layer(l);
+    CHECK(a.weight.data == b.weight.data && a.bias == b.bias && a.activation == b.activation);
+  }
+  std::remove(path.c_str());
+  CHECK(throws<IoError>([] { load_weights("/nonexistent/net.gbnn"); }));
+  CHECK(throws<StructuralError>([] { random_net({4, 3}, "tanh", "sideways", 1); }));
+  CHECK(throws<StructuralError>([&] { net.forward(RealVec(5, 0.0)); }));
+  {
+    Layer l0;
+    l0.weight = DenseMat(3, 2);
+    l0.bias = RealVec(2, 0.0);  // wrong length
+    CHECK(throws<StructuralError>([&] { NeuralNet bad({l0}); }));
+  }
+  if (!gpu) {
+    if (gbopt_device_count() == 0) CHECK(throws<DeviceError>([&] { net.forward(RealVec(4, 0.1)); }));
+    std::printf("%s host checks\n", g_fail ? "FAILED" : "passed");
+    return g_fail ? 1 : 0;
+  }
+  // ---- device ----
+  const RealVec x = {0.1, 0.7, 0.3, 0.9};
+  RealVec y = net.forward(x);
+  CHECK(std::fabs(y[0] + y[1] + y[2] - 1.0) <= 1e-12);  // softmax simplex (test_capi.cpp:42-43)
+  RealVec y2 = back.forward(x);
+  CHECK(y == y2);
+  // J vs central differences (test_nn.cpp:96-108 style)
+  NeuralNet t = random_net({5, 7, 4}, "tanh", "tanh", 1234);
+  const RealVec xt = {0.3, -0.2, 0.5, 1.1, -0.7};
+  DenseMat j = t.jacobian(xt);
+  for (int c = 0; c < 5; ++c) {
+    RealVec xp = xt, xm = xt;
+    xp[c] += 1e-5;
+    xm[c] -= 1e-5;
+    RealVec fp = t.forward(xp), fm = t.forward(xm);
+    for (int r = 0; r < 4; ++r) CHECK(std::fabs(j(r, c) - (fp[r] - fm[r]) / 2e-5) <= 1e-6);
+  }
+  // reduced-space callbacks: residual 0 at the forward image, -J layout,
+  // Hessian sees -lambda (test_formulations.cpp:215-274)
+  ReducedSpaceOracle rs(t);
+  RealVec xb = xt;
+  RealVec fy = t.forward(xt);
+  xb.insert(xb.end(), fy.begin(), fy.end());
+  RealVec r;
+  rs.residual(xb, r);
+  for (double v : r) CHECK(v == 0.0);
+  RealVec jv;
+  rs.jacobian(xb, jv);
+  CHECK(jv.size() == 4 * 5 + 4);
+  for (int i = 0; i < 4; ++i)
+    for (int c = 0; c < 5; ++c) CHECK(jv[static_cast<size_t>(i * 5 + c)] == -j(i, c));
+  for (int i = 0; i < 4; ++i) CHECK(jv[20 + static_cast<size_t>(i)] == 1.0);
+  const RealVec lam = {0.5, -1.0, 0.25, 2.0};
+  RealVec hv;
+  rs.lag_hessian(xb, lam, hv);
+  RealVec neg = lam;
+  for (double& v : neg) v = -v;
+  DenseMat h = t.lagrangian_hessian(xt, neg);
+  size_t k = 0;
+  for (int a = 0; a < 5; ++a)
+    for (int b = 0; b <= a; ++b) CHECK(std::fabs(hv[k++] - h(a, b)) <= 1e-14);
+  const int64_t evals = rs.evaluations();
+  rs.residual(xb, r);
+  rs.jacobian(xb, jv);
+  rs.lag_hessian(xb, lam, hv);
+  CHECK(rs.evaluations() == evals);  // cached: no new device work at the same iterate
+  std::printf("%s host+device checks\n", g_fail ? "FAILED" : "passed");
+  return g_fail ? 1 : 0;
+}

@@ -223,8 +223,12 @@ def test_c2_full_size_properties():
     assert orc.rel_err(g, j.T @ l1) <= 1e-12
     # Batching may change the SYRK's split-K factor (and so the summation
     # order of H at the rounding level); y and J are batch-invariant bitwise.
+    # (net.jacobian is the reverse-mode sweep; the fused oracle's J comes from
+    # the forward tangents: equal to rounding, compare fused with fused.)
+    _, jf, _ = net.oracle(x, l1)
+    assert orc.rel_err(jf, j) <= 1e-12
     Y, J, H = net.oracle_batched(np.stack([x, x]), np.stack([l1, l1]))
-    assert np.array_equal(J[0], j) and np.array_equal(J[1], j)
+    assert np.array_equal(J[0], jf) and np.array_equal(J[1], jf)
     assert np.array_equal(H[0], H[1]) and orc.rel_err(H[0], h1) <= 1e-13
 
 
