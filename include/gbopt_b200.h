@@ -219,6 +219,15 @@ gbopt_status gbopt_net_profile(const gbopt_net* net, size_t batch,
                                const double* dX, const double* dLambda,
                                int32_t* tags, float* ms, double* flops,
                                double* bytes, size_t cap, size_t* count);
+/* Concurrent-timeline variant of gbopt_net_profile: the launches keep
+ * their two streams (0 = critical path, 1 = side stream) and each reports
+ * start/end in ms from the start of the evaluation.  Synchronous. */
+gbopt_status gbopt_net_profile_timeline(const gbopt_net* net, size_t batch,
+                                        const double* dX,
+                                        const double* dLambda, int32_t* tags,
+                                        int32_t* streams, float* t_start,
+                                        float* t_end, size_t cap,
+                                        size_t* count);
 /* Name of a kernel tag reported by gbopt_net_profile ("nt_mma.gemm", ...). */
 const char* gbopt_kernel_tag_name(int tag);
 

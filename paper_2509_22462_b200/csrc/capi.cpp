@@ -349,6 +349,25 @@ gbopt_status gbopt_net_profile(const gbopt_net* net, size_t batch, const double*
 
 const char* gbopt_kernel_tag_name(int tag) { return gbb::kernel_tag_name(tag); }
 
+gbopt_status gbopt_net_profile_timeline(const gbopt_net* net, size_t batch, const double* dX, const double* dLambda,
+                                        int32_t* tags, int32_t* streams, float* t_start, float* t_end, size_t cap,
+                                        size_t* count) {
+  if (net == nullptr || dX == nullptr || dLambda == nullptr || count == nullptr)
+    return fail_argument("gbopt_net_profile_timeline: null argument");
+  if (batch == 0) return fail_argument("gbopt_net_profile_timeline: batch must be positive");
+  return guarded([&] {
+    std::vector<gbb::ProfResult> res;
+    net->net->device().profile(static_cast<int>(batch), dX, dLambda, &res, true);
+    *count = res.size();
+    for (size_t i = 0; i < res.size() && i < cap; ++i) {
+      if (tags) tags[i] = res[i].tag;
+      if (streams) streams[i] = res[i].stream;
+      if (t_start) t_start[i] = res[i].t0;
+      if (t_end) t_end[i] = res[i].t1;
+    }
+  });
+}
+
 gbopt_status gbopt_net_debug_intermediate(const gbopt_net* net, const char* name, int64_t layer, size_t batch,
                                           double* out, size_t len) {
   if (net == nullptr || name == nullptr || out == nullptr)

@@ -54,8 +54,8 @@ struct Workspace {
   int adj_chunks_max = 0;
   int64_t ld_part = 0;
   double* adj_part = nullptr;
-  double* t[2] = {nullptr, nullptr};
-  std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer l & 1)
+  std::vector<double*> t;                   // ring of tangent buffers
+  std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer (l-1) % ring)
   int64_t ldh = 0;
   double* h = nullptr;
   double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs)
@@ -78,6 +78,8 @@ struct ProfResult {
   float ms;
   double flops;  // algorithmic FP64 flops of this launch
   double bytes;  // algorithmic HBM bytes (weight streams) of this launch
+  float t0, t1;  // start / end relative to the evaluation start (ms)
+  int stream;    // 0 critical-path stream, 1 side stream
 };
 
 struct Outputs {
@@ -104,7 +106,7 @@ class DeviceNet {
   // (nb x rows(l), row-major).  Synchronous; for white-box tests.
   void copy_intermediate(const char* name, int layer, int nb, double* out);
   // Eager run with CUDA events around every launch (on the launching stream).
-  void profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out);
+  void profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out, bool timeline = false);
   // Device buffers, ordered on `user` stream, asynchronous.
   void evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
                        cudaStream_t user);
@@ -132,8 +134,9 @@ class DeviceNet {
     int tag;
     double flops, bytes;
     cudaEvent_t e0, e1;
+    int stream;
   };
-  bool profiling_ = false;
+  bool profiling_ = false, prof_timeline_ = false;
   std::vector<ProfRec> prof_;
   void run(cudaStream_t st, int nb, const Outputs& o);
 

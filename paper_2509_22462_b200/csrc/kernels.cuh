@@ -43,7 +43,7 @@ namespace dev {
 constexpr int kBM = 112;              // tile rows  (7 x 16; 784 = 7 x 112)
 constexpr int kBN = 128;              // tile cols
 constexpr int kBK = 16;               // k per stage = one 128-byte swizzle row
-constexpr int kStages = 6;            // smem ring depth
+constexpr int kStages = 5;            // smem ring depth (leaves room for a GEMV CTA on the SM)
 constexpr int kConsumerWarps = 8;     // 2 (M) x 4 (N)
 constexpr int kWarpM = 56;            // 7 DMMA row blocks
 constexpr int kWarpN = 32;            // 4 DMMA col blocks
@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32)
                     const double* __restrict__ yin, int64_t ld_in, int nb, int act, double* __restrict__ z_out,
                     double* __restrict__ y_out, double* __restrict__ s1_out, double* __restrict__ s2_out,
                     int64_t ld_out) {
-  constexpr int kFwdKChunk = 4096 / NB;  // 32 KB of staged inputs
+  // 16 KB of staged inputs: small enough to co-reside with an nt_mma CTA
+  // (the forward runs beside the tangent GEMMs on the side stream)
+  constexpr int kFwdKChunk = 2048 / NB;
   __shared__ __align__(16) double ys[NB][kFwdKChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * kFwdWarps + warp;

@@ -243,13 +243,20 @@ void DeviceNet::ensure_workspace(int batch) {
   w.ld_part = ldt_ > w.ld_in ? ldt_ : w.ld_in;
   w.adj_part = ws_alloc(static_cast<size_t>(w.adj_chunks_max) * vcap * w.ld_part);
   // tangents (only needed with >= 2 layers)
+  // T_l (l >= 1) lives in ring buffer t_buf(l) = (l - 1) % R.  With R >= the
+  // number of tangent layers the GEMM chain never waits for a SYRK to free
+  // a buffer; R is capped by a memory budget (8 GB) and is at least 2.
   if (L_ >= 2) {
-    w.t[0] = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
-    w.t[1] = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
+    const size_t tbytes = sizeof(double) * static_cast<size_t>(cap) * n_pad_ * ldt_;
+    const int want = std::max(2, static_cast<int>(L_) - 1);
+    const int fit = static_cast<int>(std::max<size_t>(2, (size_t(8) << 30) / std::max<size_t>(tbytes, 1)));
+    const int ring = std::min(want, fit);
+    w.t.assign(static_cast<size_t>(ring), nullptr);
+    for (auto& b : w.t) b = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
     w.tm_t_a.assign(L, CUtensorMap{});
     w.tm_t_b.assign(L, CUtensorMap{});
     for (size_t l = 1; l < L; ++l) {
-      const double* buf = w.t[l & 1];
+      const double* buf = w.t[(l - 1) % w.t.size()];
       w.tm_t_a[l] = make_tmap(buf, layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBM);
       w.tm_t_b[l] = make_tmap(buf, layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBN);
     }
@@ -362,6 +369,7 @@ void DeviceNet::prof_begin(cudaStream_t st, int tag, double flops, double bytes)
   r.tag = tag;
   r.flops = flops;
   r.bytes = bytes;
+  r.stream = st == stream_ ? 0 : 1;
   CK(cudaEventCreate(&r.e0));
   CK(cudaEventCreate(&r.e1));
   CK(cudaEventRecord(r.e0, st));
@@ -374,7 +382,7 @@ void DeviceNet::after_launch(cudaStream_t st) {
   if (profiling_) CK(cudaEventRecord(prof_.back().e1, st));
 }
 
-void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out) {
+void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out, bool timeline) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
   if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
@@ -389,24 +397,31 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
   o.j = w.j_out;
   o.h = w.h_out;
   profiling_ = true;
+  prof_timeline_ = timeline;
   prof_.clear();
   launches_ = 0;
+  cudaEvent_t base;
+  CK(cudaEventCreate(&base));
+  CK(cudaEventRecord(base, stream_));
   try {
     enqueue(stream_, nb, o);
   } catch (...) {
-    profiling_ = false;
+    profiling_ = prof_timeline_ = false;
     throw;
   }
-  profiling_ = false;
+  profiling_ = prof_timeline_ = false;
   CK(cudaStreamSynchronize(stream_));
   out->clear();
   for (auto& r : prof_) {
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f, t1 = 0.f;
     CK(cudaEventElapsedTime(&ms, r.e0, r.e1));
-    out->push_back(ProfResult{r.tag, ms, r.flops, r.bytes});
+    CK(cudaEventElapsedTime(&t0, base, r.e0));
+    CK(cudaEventElapsedTime(&t1, base, r.e1));
+    out->push_back(ProfResult{r.tag, ms, r.flops, r.bytes, t0, t1, r.stream});
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);
   }
+  cudaEventDestroy(base);
   prof_.clear();
 }
 
@@ -421,7 +436,8 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
 // (Profiling runs serialise both onto one stream.)
 void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   Workspace& w = ws_;
-  const bool two = !profiling_ && concurrent_;
+  // profiling serialises onto one stream, except the timeline mode
+  const bool two = concurrent_ && (!profiling_ || prof_timeline_);
   cudaStream_t sa = st;
   cudaStream_t sb = two ? stream2_ : st;
   int ev_next = 0;
@@ -454,8 +470,14 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   const double* yin = w.x;
   int64_t ld_in = w.ld_in;
   const bool batched = nb >= kBatchGemm;
+  // Layer 0 runs on sa (GEMM_1 needs only sigma'_0); layers >= 1 run on sb,
+  // beside the tangent GEMMs, each recording fwd_done[l] for GEMM_{l+1}.
+  std::vector<cudaEvent_t> fwd_done(static_cast<size_t>(L), nullptr);
   for (int l = 0; l < L; ++l) {
     const DevLayer& d = layers_[static_cast<size_t>(l)];
+    if (l == 1) link(sa, sb);
+    // this layer's stream (shadows the outer `sa` inside the loop body)
+    cudaStream_t sa = l == 0 ? st : sb;
     if (batched) {
       dev::RowEpi e{};
       e.mode = dev::kEpiAct;
@@ -467,6 +489,10 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       e.s2o = w.s2[l];
       e.ld = w.ld[l];
       batch_gemm(sa, nb, l == 0 ? w.tm_x : w.tm_y[static_cast<size_t>(l - 1)], d, false, &e, w.z[l]);
+      if (two && l > 0) {
+        fwd_done[static_cast<size_t>(l)] = next_event();
+        CK(cudaEventRecord(fwd_done[static_cast<size_t>(l)], sb));
+      }
       continue;
     }
     const int nbpass = nb >= 8 ? 8 : (nb >= 4 ? 4 : 1);
@@ -483,18 +509,29 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       dev::fwd_rows_kernel<1><<<grid, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
     after_launch(sa);
+    if (two && l > 0) {
+      fwd_done[static_cast<size_t>(l)] = next_event();
+      CK(cudaEventRecord(fwd_done[static_cast<size_t>(l)], sb));
+    }
     yin = w.y[l];
     ld_in = w.ld[l];
   }
+  // the forward's tail (softmax, y copy) follows its last layer's stream
+  cudaStream_t sf = L > 1 ? sb : sa;
   if (softmax_out) {
-    prof_begin(sa, kTagSoftmax, 0, 0);
-    dev::softmax_kernel<<<ceil_div(nb, 4), 128, 0, sa>>>(w.z[L - 1], w.y[L - 1], static_cast<int>(m_), w.ld[L - 1],
+    prof_begin(sf, kTagSoftmax, 0, 0);
+    dev::softmax_kernel<<<ceil_div(nb, 4), 128, 0, sf>>>(w.z[L - 1], w.y[L - 1], static_cast<int>(m_), w.ld[L - 1],
                                                          nb);
-    after_launch(sa);
+    after_launch(sf);
   }
   if (o.y) {
     CK(cudaMemcpy2DAsync(o.y, sizeof(double) * m_, w.y[L - 1], sizeof(double) * w.ld[L - 1], sizeof(double) * m_, nb,
-                         cudaMemcpyDeviceToDevice, sa));
+                         cudaMemcpyDeviceToDevice, sf));
+  }
+  cudaEvent_t fwd_all = nullptr;  // the whole forward chain (sb), for the final layer on sa
+  if (two && L > 1) {
+    fwd_all = next_event();
+    CK(cudaEventRecord(fwd_all, sb));
   }
 
   // ---- 2. adjoint chain --------------------------------------------------
@@ -598,8 +635,11 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   if (want_h) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
   const int kfin_layer = L - 1;
   const bool skinny_final = m_ <= dev::kSkMB;
-  // T_l lives in: l == 0 -> t0_ (broadcast over points), else w.t[l & 1].
-  auto t_ptr = [&](int l) -> const double* { return l == 0 ? t0_ : w.t[l & 1]; };
+  // T_l lives in: l == 0 -> t0_ (broadcast over points), else ring buffer
+  // (l - 1) % R.
+  const int ring = static_cast<int>(w.t.size());
+  auto t_buf = [&](int l) -> double* { return w.t[static_cast<size_t>((l - 1) % ring)]; };
+  auto t_ptr = [&](int l) -> const double* { return l == 0 ? t0_ : t_buf(l); };
   auto t_ld = [&](int l) -> int64_t { return l == 0 ? ldt0_ : ldt_; };
   auto t_point_rows = [&](int l) -> int64_t { return l == 0 ? 0 : n_pad_; };
   auto tmap_a = [&](int l) -> const CUtensorMap& { return l == 0 ? tm_t0_a_ : w.tm_t_a[static_cast<size_t>(l)]; };
@@ -649,9 +689,13 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
     // propagate the tangents to layer l+1 (unless it is a skinny final)
     if (l + 1 == kfin_layer && skinny_final) break;
-    // T_{l+1} overwrites T_{l-1}: wait for SYRK_{l-1}
-    if (l >= 2 && syrk_done[static_cast<size_t>(l - 1)])
-      CK(cudaStreamWaitEvent(sa, syrk_done[static_cast<size_t>(l - 1)], 0));
+    // T_{l+1} overwrites T_{l+1-R} in the ring: wait for that layer's SYRK
+    const int prev = l + 1 - ring;
+    if (prev >= 1 && syrk_done[static_cast<size_t>(prev)])
+      CK(cudaStreamWaitEvent(sa, syrk_done[static_cast<size_t>(prev)], 0));
+    // ... and needs sigma'_l from the forward chain (sb for l >= 1)
+    if (l >= 1 && fwd_done[static_cast<size_t>(l)])
+      CK(cudaStreamWaitEvent(sa, fwd_done[static_cast<size_t>(l)], 0));
     const DevLayer& dn = layers_[static_cast<size_t>(l + 1)];
     dev::NtParams p{};
     p.tiles = nullptr;
@@ -667,7 +711,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.m_rows_valid = static_cast<int>(n_pad_);
     p.scale = w.s1[l];
     p.s_stride = w.ld[l];
-    p.c = w.t[(l + 1) & 1];
+    p.c = t_buf(l + 1);
     p.c_point_stride = n_pad_ * ldt_;
     p.ldc = ldt_;
     p.mode = dev::kStore;
@@ -676,6 +720,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   }
 
   // ---- 4. final layer -------------------------------------------------------
+  if (fwd_all) CK(cudaStreamWaitEvent(sa, fwd_all, 0));  // sigma'/y of the last layers
   const DevLayer& df = layers_[static_cast<size_t>(kfin_layer)];
   const double* u;
   int64_t ldu, u_point_rows;

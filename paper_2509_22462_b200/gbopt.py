@@ -79,6 +79,9 @@ _net_set_graphs = _fn("gbopt_net_set_graphs", _status, _vp, ctypes.c_int)
 _net_profile = _fn("gbopt_net_profile", _status, _vp, _sz, _vp, _vp, ctypes.POINTER(ctypes.c_int32),
                    ctypes.POINTER(ctypes.c_float), _dp, _dp, _sz, ctypes.POINTER(_sz))
 _kernel_tag_name = _fn("gbopt_kernel_tag_name", ctypes.c_char_p, ctypes.c_int)
+_net_profile_timeline = _fn("gbopt_net_profile_timeline", _status, _vp, _sz, _vp, _vp, ctypes.POINTER(ctypes.c_int32),
+                            ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float),
+                            ctypes.POINTER(ctypes.c_float), _sz, ctypes.POINTER(_sz))
 _net_debug_intermediate = _fn("gbopt_net_debug_intermediate", _status, _vp, ctypes.c_char_p, _i64, _sz, _dp, _sz)
 
 # ---------------------------------------------------------------------------
@@ -376,6 +379,20 @@ def profile_launches(net: "NeuralNet", batch: int, dX: int, dLam: int):
     cnt = _sz()
     _check(_net_profile(net._h, batch, dX, dLam, tags, ms, fl, by, cap, ctypes.byref(cnt)))
     return [(_kernel_tag_name(tags[i]).decode(), float(ms[i]), float(fl[i]), float(by[i]))
+            for i in range(min(cnt.value, cap))]
+
+
+def profile_timeline(net: "NeuralNet", batch: int, dX: int, dLam: int):
+    """(kernel, stream, start_ms, end_ms) of every launch of one eager
+    evaluation that keeps the two-stream concurrency."""
+    cap = 4096
+    tags = (ctypes.c_int32 * cap)()
+    st = (ctypes.c_int32 * cap)()
+    t0 = (ctypes.c_float * cap)()
+    t1 = (ctypes.c_float * cap)()
+    cnt = _sz()
+    _check(_net_profile_timeline(net._h, batch, dX, dLam, tags, st, t0, t1, cap, ctypes.byref(cnt)))
+    return [(_kernel_tag_name(tags[i]).decode(), int(st[i]), float(t0[i]), float(t1[i]))
             for i in range(min(cnt.value, cap))]
 
 
