@@ -57,7 +57,11 @@ struct Workspace {
   std::vector<double*> t;                   // ring of tangent buffers
   std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer (l-1) % ring)
   int64_t ldh = 0;
-  double* h = nullptr;
+  double* h = nullptr;             // == hb[0]
+  std::vector<double*> hb;         // H accumulators (one per SYRK job of a stream-K launch)
+  double* sk_slots = nullptr;      // stream-K pieces [2 * #SMs][kBM * kBN]
+  int* sk_counters = nullptr;      // stream-K per-tile arrival counters (self-resetting)
+  int sk_counter_cap = 0;
   double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs)
   CUtensorMap tm_x;                   // x as an A operand [cap][n]
   std::vector<CUtensorMap> tm_y, tm_gz;  // y_l / gz_l as A operands [cap][n_l]
@@ -69,6 +73,7 @@ struct Workspace {
 enum KernelTag : int {
   kTagFwd = 0, kTagSoftmax, kTagAdjSeed, kTagAdjCols, kTagAdjReduce, kTagGemm, kTagSyrk, kTagSyrkReduce,
   kTagSkinny, kTagSkinnyReduce, kTagJacOut, kTagSmallSyrk, kTagSymmetrize, kTagFwdGemm, kTagAdjGemm, kTagRowEpi,
+  kTagStep,
   kTagCount
 };
 const char* kernel_tag_name(int tag);
@@ -127,6 +132,10 @@ class DeviceNet {
   void batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const DevLayer& d, bool transposed,
                   const void* epi, double* store);
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
+  // One job of a persistent stream-K launch (nt_mma_sk_kernel); oracle.cu.
+  struct SkJobDesc;
+  void launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs);
+  bool streamk_ = true;
   void enqueue(cudaStream_t st, int nb, const Outputs& o);
   void prof_begin(cudaStream_t st, int tag, double flops, double bytes);
   void after_launch(cudaStream_t st);
