@@ -129,14 +129,16 @@ def oracle_net_from(net):
     return orc.NeuralNet(layers)
 
 
-def time_cpu_reference(wl, n_points: int, budget_s: float = 25.0, min_evals: int = 1):
+def time_cpu_reference(wl, n_points: int, budget_s: float = 12.0, min_evals: int = 2):
     """Evals/s of the CPU oracle (reference algorithm: forward, reverse-mode
-    Jacobian, forward-over-reverse Hessian) on all host threads."""
+    Jacobian, forward-over-reverse Hessian) on all host threads, over a
+    bounded sample: at least `min_evals` evaluations and about `budget_s`
+    seconds of CPU work, cycling over the first `n_points` points."""
     ref = oracle_net_from(wl.net)
     t_total, evals = 0.0, 0
     t_start = time.perf_counter()
     i = 0
-    while evals < min_evals or (time.perf_counter() - t_start < budget_s and evals < n_points * 4):
+    while evals < min_evals or (time.perf_counter() - t_start < budget_s and evals < 2000):
         x, lam = wl.X[i % wl.X.shape[0]], wl.Lam[i % wl.X.shape[0]]
         t0 = time.perf_counter()
         ref.forward(x)
@@ -373,7 +375,7 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         wls = configs.make(name, batch=min(B, 4))
-        v, ne, tt = time_cpu_reference(wls, n_points=min(B, 4), budget_s=20.0)
+        v, ne, tt = time_cpu_reference(wls, n_points=min(B, 4), budget_s=12.0)
         cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                "sample": f"{ne} single-point evals of {name} in {tt:.1f}s (reference algorithm nn.cpp:113-292, "
                          f"numpy/OpenBLAS, all host threads)"}

@@ -923,21 +923,24 @@ __global__ void jac_seed_kernel(const double* __restrict__ y, const double* __re
 //   partial[c][b][j][i] = sum_{k in chunk c} A[b][j][k] s[b][k] W[i][k]
 // A rows j < n_valid of each point; W is the last layer (m x K, row-major).
 // ---------------------------------------------------------------------------
-constexpr int kSkMB = 16;
+constexpr int kSkMB = 16;      // output slots per row in partial / U
 constexpr int kSkRows = 16;    // rows j per CTA (2 per warp)
-constexpr int kSkKChunk = 256;
+// K chunk per CTA for MB outputs: 32 KB of staged (scaled) weights at most.
+__host__ __device__ constexpr int skinny_kchunk(int mb) { return mb <= 1 ? 1024 : (mb <= 4 ? 512 : 256); }
 
+template <int MB>
 __global__ void __launch_bounds__(256)
     skinny_nt_kernel(const double* __restrict__ a, int64_t lda, int64_t a_point_rows, int n_valid,
                      const double* __restrict__ scale, int64_t s_stride, const double* __restrict__ w, int64_t ldw,
                      int m, int k_dim, double* __restrict__ partial) {
-  __shared__ __align__(16) double ws[kSkMB][kSkKChunk];
+  constexpr int kSkKChunk = skinny_kchunk(MB);
+  __shared__ __align__(16) double ws[MB][kSkKChunk];
   const int point = blockIdx.z;
   const int chunk = blockIdx.y;
   const int k0 = chunk * kSkKChunk;
   const int kc = min(kSkKChunk, k_dim - k0);
   const double* sp = scale ? scale + s_stride * point : nullptr;
-  for (int e = threadIdx.x; e < kSkMB * kSkKChunk; e += blockDim.x) {
+  for (int e = threadIdx.x; e < MB * kSkKChunk; e += blockDim.x) {
     const int i = e / kSkKChunk, k = e % kSkKChunk;
     double v = 0.0;
     if (i < m && k < kc) {
@@ -949,18 +952,18 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j0 = blockIdx.x * kSkRows + warp * 2;
-  double acc[2][kSkMB];
+  double acc[2][MB];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int i = 0; i < kSkMB; ++i) acc[r][i] = 0.0;
+    for (int i = 0; i < MB; ++i) acc[r][i] = 0.0;
   const double* a0 = a + (a_point_rows * point + j0) * lda + k0;
   const bool live0 = j0 < n_valid, live1 = j0 + 1 < n_valid;
   for (int k = 2 * lane; k < kc; k += 64) {
     const double2 x0 = live0 ? *reinterpret_cast<const double2*>(a0 + k) : make_double2(0.0, 0.0);
     const double2 x1 = live1 ? *reinterpret_cast<const double2*>(a0 + lda + k) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int i = 0; i < kSkMB; ++i) {
+    for (int i = 0; i < MB; ++i) {
       const double2 wv = *reinterpret_cast<const double2*>(&ws[i][k]);
       acc[0][i] = fma(x0.x, wv.x, fma(x0.y, wv.y, acc[0][i]));
       acc[1][i] = fma(x1.x, wv.x, fma(x1.y, wv.y, acc[1][i]));
@@ -969,7 +972,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int i = 0; i < kSkMB; ++i) {
+    for (int i = 0; i < MB; ++i) {
       double v = acc[r][i];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -982,9 +985,9 @@ __global__ void __launch_bounds__(256)
   for (int r = 0; r < 2; ++r) {
     double v = 0.0;
 #pragma unroll
-    for (int i = 0; i < kSkMB; ++i)
+    for (int i = 0; i < MB; ++i)
       if (i == lane) v = acc[r][i];
-    if (lane < kSkMB) partial[(base + j0 + r) * kSkMB + lane] = v;
+    if (lane < MB) partial[(base + j0 + r) * kSkMB + lane] = v;
   }
 }
 

@@ -105,18 +105,8 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   sm_count_ = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::nt_mma_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
-  // Full shared-memory carveout for every kernel, so a GEMV CTA (16 KB) fits
-  // on an SM beside an nt_mma CTA (~152 KB) instead of waiting for it.
-  for (const void* f : {reinterpret_cast<const void*>(dev::nt_mma_kernel),
-                        reinterpret_cast<const void*>(dev::nt_mma_sk_kernel),
-                        reinterpret_cast<const void*>(dev::fwd_rows_kernel<1>),
-                        reinterpret_cast<const void*>(dev::fwd_rows_kernel<4>),
-                        reinterpret_cast<const void*>(dev::fwd_rows_kernel<8>),
-                        reinterpret_cast<const void*>(dev::adj_cols_kernel<1>),
-                        reinterpret_cast<const void*>(dev::adj_cols_kernel<4>),
-                        reinterpret_cast<const void*>(dev::adj_cols_kernel<8>),
-                        reinterpret_cast<const void*>(dev::adj_reduce_kernel)})
-    CK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  // (A maximal shared-memory carveout, tried so GEMV CTAs could co-reside with
+  // nt_mma, cost 2% on c2 -- 173.4 vs 177.3 evals/s -- and is not set.)
   // Persistent stream-K layer steps (experimental, GBOPT_STREAMK=1): balanced
   // but it loses the grouped raster's L2 reuse of W and starves the side
   // stream; the default two-stream data-parallel schedule is faster on c2/c5
@@ -298,7 +288,7 @@ void DeviceNet::ensure_workspace(int batch) {
   w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, n_syrk_tiles_)) * kBM * kBN);
   // final-layer skinny product: U [cap][n_pad][16], partials [chunks][cap][n_pad][16]
   const int64_t kfin = layers_[L - 1].cols;
-  w.sk_chunks = ceil_div(kfin, dev::kSkKChunk);
+  w.sk_chunks = ceil_div(kfin, dev::skinny_kchunk(m_ <= 1 ? 1 : (m_ <= 4 ? 4 : 16)));
   w.u = ws_alloc(static_cast<size_t>(cap) * n_pad_ * dev::kSkMB);
   w.sk_part = ws_alloc(static_cast<size_t>(w.sk_chunks) * cap * n_pad_ * dev::kSkMB);
   // vectors as TMA A operands (batched forward / adjoint GEMMs)
@@ -914,9 +904,19 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     const int l = kfin_layer - 1;
     dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
     prof_begin(sa, kTagSkinny, 2.0 * n_ * m_ * df.cols * nb, 0);
-    dev::skinny_nt_kernel<<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_), w.s1[l],
-                                                w.ld[l], df.w, df.ldw, static_cast<int>(m_),
-                                                static_cast<int>(df.cols), w.sk_part);
+    // template on the output count: no work on empty output slots
+    if (m_ <= 1)
+      dev::skinny_nt_kernel<1><<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_),
+                                                     w.s1[l], w.ld[l], df.w, df.ldw, static_cast<int>(m_),
+                                                     static_cast<int>(df.cols), w.sk_part);
+    else if (m_ <= 4)
+      dev::skinny_nt_kernel<4><<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_),
+                                                     w.s1[l], w.ld[l], df.w, df.ldw, static_cast<int>(m_),
+                                                     static_cast<int>(df.cols), w.sk_part);
+    else
+      dev::skinny_nt_kernel<16><<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_),
+                                                      w.s1[l], w.ld[l], df.w, df.ldw, static_cast<int>(m_),
+                                                      static_cast<int>(df.cols), w.sk_part);
     after_launch(sa);
     const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
     prof_begin(sa, kTagSkinnyReduce, 0, 0);
