@@ -59,8 +59,8 @@ struct Workspace {
   int64_t ldh = 0;
   double* h = nullptr;             // == hb[0]
   std::vector<double*> hb;         // H accumulators (one per SYRK job of a stream-K launch)
-  double* sk_slots = nullptr;      // stream-K pieces [2 * #SMs][kBM * kBN]
-  int* sk_counters = nullptr;      // stream-K per-tile arrival counters (self-resetting)
+  double* sk_slots[2] = {nullptr, nullptr};  // stream-K pieces [2 * #SMs][kBM * kBN], per stream
+  int* sk_counters[2] = {nullptr, nullptr};  // per-tile arrival counters (self-resetting), per stream
   int sk_counter_cap = 0;
   double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs)
   CUtensorMap tm_x;                   // x as an A operand [cap][n]
@@ -134,8 +134,9 @@ class DeviceNet {
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
   // One job of a persistent stream-K launch (nt_mma_sk_kernel); oracle.cu.
   struct SkJobDesc;
-  void launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs);
-  bool streamk_ = true;
+  void launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs, bool hybrid = true);
+  bool streamk_ = true;   // layer steps: GEMM_{l+1} + SYRKs in one launch
+  bool hybrid_ = false;   // two-stream schedule with hybrid DP/stream-K launches
   void enqueue(cudaStream_t st, int nb, const Outputs& o);
   void prof_begin(cudaStream_t st, int tag, double flops, double bytes);
   void after_launch(cudaStream_t st);

@@ -374,18 +374,26 @@ struct SkParams {
   SkJob job[kSkJobs];
   int n_jobs;
   int64_t iters;   // total iterations (sum of tiles * k_blocks)
+  // Hybrid schedule: the first dp_waves * gridDim.x tiles of job 0 run
+  // data-parallel (CTA c takes tiles c, c + grid, ...: whole tiles, the
+  // grouped raster's L2 reuse intact); the iterations from sk0 on are cut
+  // stream-K.  The host keeps (iters - sk0) == 0 or >= gridDim.x so every
+  // CTA's stream-K range is non-empty.
+  int dp_waves;
+  int64_t sk0;
   double* slots;   // [2 * gridDim.x][kBM * kBN] pieces of split tiles
   int* counters;   // [total tiles]; zero on entry, reset to zero on exit
 };
 
-__device__ __forceinline__ int64_t sk_begin(int64_t iters, int cta, int grid) {
-  return (iters * cta) / grid;
+// First stream-K iteration of CTA `cta`.
+__device__ __forceinline__ int64_t sk_begin(const SkParams& P, int cta, int grid) {
+  return P.sk0 + ((P.iters - P.sk0) * cta) / grid;
 }
-// CTA whose range contains global iteration `it`.
-__device__ __forceinline__ int sk_cta_of(int64_t iters, int grid, int64_t it) {
-  int c = static_cast<int>((it * grid) / iters);
-  while (c + 1 < grid && sk_begin(iters, c + 1, grid) <= it) ++c;
-  while (c > 0 && sk_begin(iters, c, grid) > it) --c;
+// CTA whose stream-K range contains global iteration `it` (>= sk0).
+__device__ __forceinline__ int sk_cta_of(const SkParams& P, int grid, int64_t it) {
+  int c = static_cast<int>(((it - P.sk0) * grid) / (P.iters - P.sk0));
+  while (c + 1 < grid && sk_begin(P, c + 1, grid) <= it) ++c;
+  while (c > 0 && sk_begin(P, c, grid) > it) --c;
   return c;
 }
 
@@ -458,8 +466,20 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int cta = blockIdx.x, grid = gridDim.x;
-  const int64_t begin = sk_begin(P.iters, cta, grid);
-  const int64_t end = sk_begin(P.iters, cta + 1, grid);
+  const int64_t skb = sk_begin(P, cta, grid);
+  const int64_t ske = sk_begin(P, cta + 1, grid);
+  const int64_t kb_dp = P.job[0].p.k_blocks;
+  // work range w: the w-th data-parallel tile of this CTA, then (w ==
+  // dp_waves) its stream-K slice
+  auto range_of = [&](int w, int64_t& r_beg, int64_t& r_end) {
+    if (w < P.dp_waves) {
+      r_beg = (static_cast<int64_t>(w) * grid + cta) * kb_dp;
+      r_end = r_beg + kb_dp;
+    } else {
+      r_beg = skb;
+      r_end = ske;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -478,8 +498,11 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
         tma_prefetch_desc(&P.job[j].tmB);
       }
       int64_t gk = 0;  // k-blocks issued by this CTA (ring position)
-      for (int64_t it = begin; it < end;) {
-        const SkSeg sg = sk_segment(P, it, end);
+      for (int w = 0; w <= P.dp_waves; ++w) {
+      int64_t r_beg, r_end;
+      range_of(w, r_beg, r_end);
+      for (int64_t it = r_beg; it < r_end;) {
+        const SkSeg sg = sk_segment(P, it, r_end);
         const SkJob& J = P.job[sg.job];
         int point, tm, tn;
         sk_tile_coords(J.p, sg.tile, point, tm, tn);
@@ -496,6 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
         }
         it += sg.nkb;
       }
+      }
     }
     return;
   }
@@ -507,8 +531,11 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
   const int rb = wn * kWarpN + row_perm(g);
   const int pg = row_perm(g), pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
   int64_t gk = 0;
-  for (int64_t it = begin; it < end;) {
-    const SkSeg sg = sk_segment(P, it, end);
+  for (int w = 0; w <= P.dp_waves; ++w) {
+  int64_t r_beg, r_end;  // (not rb: that is the B-fragment row base)
+  range_of(w, r_beg, r_end);
+  for (int64_t it = r_beg; it < r_end;) {
+    const SkSeg sg = sk_segment(P, it, r_end);
     const NtParams& p = P.job[sg.job].p;
     int point, tm, tn;
     sk_tile_coords(p, sg.tile, point, tm, tn);
@@ -558,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
     } else {
       // piece of a split tile: slot 2*cta (first segment of this CTA's range)
       // or 2*cta+1 (last segment)
-      const int my_slot = 2 * cta + (it == begin ? 0 : 1);
+      const int my_slot = 2 * cta + (it == skb ? 0 : 1);
       double* out = P.slots + static_cast<int64_t>(my_slot) * kBM * kBN;
 #pragma unroll
       for (int mi = 0; mi < kMI; ++mi)
@@ -571,8 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
         }
       __threadfence();
       consumer_bar();
-      const int c0 = sk_cta_of(P.iters, grid, sg.tile_it0);
-      const int c1 = sk_cta_of(P.iters, grid, sg.tile_it1 - 1);
+      const int c0 = sk_cta_of(P, grid, sg.tile_it0);
+      const int c1 = sk_cta_of(P, grid, sg.tile_it1 - 1);
       int* cnt = P.counters + P.job[sg.job].tile0 + sg.tile;
       if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1) == c1 - c0);
       consumer_bar();
@@ -586,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
         for (int c = c0; c <= c1; ++c) {
           // the piece of CTA c: its first segment (slot 2c) unless its range
           // began before this tile (then the tile is its last segment)
-          const int slot = 2 * c + (sk_begin(P.iters, c, grid) < sg.tile_it0 ? 1 : 0);
+          const int slot = 2 * c + (sk_begin(P, c, grid) < sg.tile_it0 ? 1 : 0);
           const double* in = P.slots + static_cast<int64_t>(slot) * kBM * kBN;
 #pragma unroll
           for (int mi = 0; mi < kMI; ++mi)
@@ -604,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_con
       consumer_bar();  // slots of this CTA may be rewritten only after this
     }
     it += sg.nkb;
+  }
   }
 }
 

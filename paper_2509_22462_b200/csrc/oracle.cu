@@ -112,6 +112,7 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   // stream; the default two-stream data-parallel schedule is faster on c2/c5
   // (profiles/r01_notes.md).
   streamk_ = std::getenv("GBOPT_STREAMK") != nullptr;
+  hybrid_ = std::getenv("GBOPT_HYBRID") != nullptr;
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
@@ -276,13 +277,14 @@ void DeviceNet::ensure_workspace(int batch) {
   w.h = w.hb[0];
   // stream-K: two piece slots per CTA; one counter per tile of a launch
   // (GEMM tiles of the widest layer + kSkJobs SYRK jobs)
-  w.sk_slots = ws_alloc(static_cast<size_t>(2) * sm_count_ * kBM * kBN);
+  for (int s = 0; s < 2; ++s) w.sk_slots[s] = ws_alloc(static_cast<size_t>(2) * sm_count_ * kBM * kBN);
   {
     int64_t wn = 1;
     for (auto& d : layers_) wn = std::max(wn, d.rows);
     const int64_t gemm_tiles = static_cast<int64_t>(cap) * (n_pad_ / kBM) * ceil_div(wn, kBN);
     w.sk_counter_cap = static_cast<int>(gemm_tiles + static_cast<int64_t>(dev::kSkJobs) * cap * n_syrk_tiles_);
-    w.sk_counters = reinterpret_cast<int*>(ws_alloc((static_cast<size_t>(w.sk_counter_cap) + 1) / 2));
+    for (int s = 0; s < 2; ++s)
+      w.sk_counters[s] = reinterpret_cast<int*>(ws_alloc((static_cast<size_t>(w.sk_counter_cap) + 1) / 2));
   }
   // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
   w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, n_syrk_tiles_)) * kBM * kBN);
@@ -388,7 +390,7 @@ struct DeviceNet::SkJobDesc {
 // One persistent stream-K launch over up to kSkJobs jobs: grid = #SMs (or
 // the iteration count if smaller), each CTA one contiguous slice of the
 // jobs' (tile, k-block) iterations.
-void DeviceNet::launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs) {
+void DeviceNet::launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs, bool hybrid) {
   if (jobs.empty()) return;
   if (static_cast<int>(jobs.size()) > dev::kSkJobs) throw StructuralError("launch_sk: too many jobs");
   dev::SkParams P;
@@ -411,9 +413,22 @@ void DeviceNet::launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs) {
   if (tiles > ws_.sk_counter_cap) throw StructuralError("launch_sk: tile counter capacity exceeded");
   P.n_jobs = static_cast<int>(jobs.size());
   P.iters = iters;
-  P.slots = ws_.sk_slots;
-  P.counters = ws_.sk_counters;
+  // each stream has its own slots / counters: launches on sa and sb may overlap
+  const int set = st == stream2_ ? 1 : 0;
+  P.slots = ws_.sk_slots[set];
+  P.counters = ws_.sk_counters[set];
   const int grid = static_cast<int>(std::min<int64_t>(sm_count_, iters));
+  // hybrid: whole waves of job 0 data-parallel, the rest stream-K; keep the
+  // stream-K part either empty or at least one iteration per CTA
+  int waves = hybrid ? jobs[0].tiles / grid : 0;
+  const int64_t kb0 = jobs[0].p.k_blocks;
+  while (waves > 0) {
+    const int64_t rest = iters - static_cast<int64_t>(waves) * grid * kb0;
+    if (rest == 0 || rest >= grid) break;
+    --waves;
+  }
+  P.dp_waves = waves;
+  P.sk0 = static_cast<int64_t>(waves) * grid * kb0;
   prof_begin(st, kTagStep, flops, 0);
   dev::nt_mma_sk_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(P);
   after_launch(st);
@@ -725,6 +740,18 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.ldc = n_pad_;
     p.mode = p.split > 1 ? dev::kPartial : dev::kAccum;
     p.partial = w.syrk_part;
+    if (hybrid_) {  // whole waves data-parallel, the remainder stream-K: no split-K pass
+      p.split = 1;
+      p.mode = dev::kAccum;
+      std::vector<SkJobDesc> jobs(1);
+      jobs[0].ta = &tmap_a(l);
+      jobs[0].tb = &tmap_b(l);
+      jobs[0].p = p;
+      jobs[0].tiles = nb * n_syrk_tiles_;
+      jobs[0].flops = static_cast<double>(d.rows) * n_ * (n_ + 1) * nb;
+      launch_sk(sb, jobs, true);
+      return;
+    }
     prof_begin(sb, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
     launch_nt(sb, tmap_a(l), tmap_b(l), p, nb * n_syrk_tiles_ * p.split);
     if (p.split > 1) {
@@ -887,6 +914,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.c_point_stride = n_pad_ * ldt_;
     p.ldc = ldt_;
     p.mode = dev::kStore;
+    if (hybrid_) {
+      std::vector<SkJobDesc> jobs(1);
+      jobs[0].ta = &tmap_a(l);
+      jobs[0].tb = &dn.tm_w;
+      jobs[0].p = p;
+      jobs[0].tiles = nb * p.n_tiles;
+      jobs[0].flops = 2.0 * n_ * dn.rows * dn.cols * nb;
+      launch_sk(sa, jobs, true);
+      continue;
+    }
     prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
     launch_nt(sa, tmap_a(l), dn.tm_w, p, nb * p.n_tiles);
   }
