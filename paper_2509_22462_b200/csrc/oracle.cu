@@ -115,8 +115,22 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   hybrid_ = std::getenv("GBOPT_HYBRID") != nullptr;
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  CK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
-  CK(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, prio_lo));
+  // Which stream gets the SMs first.  A layer's SYRK costs (n+1)/(2 n_{l-1})
+  // of its tangent GEMM: when that is small (c2: 0.08) the GEMM chain is the
+  // critical path and keeps priority (the SYRKs fill its last waves); when it
+  // is large (c5: 0.38) the side stream goes first so the adjoint and SYRKs
+  // are not starved into a tail (measured: c2 177 vs 172 evals/s, c5 579 vs
+  // 624).  GBOPT_SIDE_HIGH=0/1 overrides.
+  double ratio = 0.0;
+  {
+    const int64_t n = net.input_dim();
+    for (int64_t l = 1; l + 1 < net.layer_count(); ++l)
+      ratio = std::max(ratio, static_cast<double>(n + 1) / (2.0 * static_cast<double>(net.layer(l).cols)));
+  }
+  bool side_high = ratio > 0.2;
+  if (const char* e = std::getenv("GBOPT_SIDE_HIGH")) side_high = e[0] == '1';
+  CK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, side_high ? prio_lo : prio_hi));
+  CK(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, side_high ? prio_hi : prio_lo));
   concurrent_ = std::getenv("GBOPT_SERIAL") == nullptr;  // debugging / A-B switch
   CK(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
