@@ -62,7 +62,8 @@ struct Workspace {
   double* sk_slots[2] = {nullptr, nullptr};  // stream-K pieces [2 * #SMs][kBM * kBN], per stream
   int* sk_counters[2] = {nullptr, nullptr};  // per-tile arrival counters (self-resetting), per stream
   int sk_counter_cap = 0;
-  double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs)
+  double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs; side stream)
+  double* gemm_part = nullptr;  // split-K partials of single-point tangent GEMMs (main stream)
   CUtensorMap tm_x;                   // x as an A operand [cap][n]
   std::vector<CUtensorMap> tm_y, tm_gz;  // y_l / gz_l as A operands [cap][n_l]
   int sk_chunks = 0;

@@ -662,7 +662,7 @@ __global__ void syrk_partial_reduce_kernel(const double* __restrict__ partial, c
 // The epilogue runs either inside the split-K reduction or as a separate
 // elementwise pass over the stored GEMM result.
 // ---------------------------------------------------------------------------
-enum EpiMode : int { kEpiAct = 0, kEpiAdj = 1 };
+enum EpiMode : int { kEpiAct = 0, kEpiAdj = 1, kEpiStore = 2 };
 
 struct RowEpi {
   int mode;
@@ -677,6 +677,10 @@ struct RowEpi {
 
 __device__ __forceinline__ void apply_row_epi(const RowEpi& e, int r, int c, double v) {
   const int64_t o = static_cast<int64_t>(r) * e.ld + c;
+  if (e.mode == kEpiStore) {  // plain store into e.z (pitch e.ld)
+    e.z[o] = v;
+    return;
+  }
   if (e.mode == kEpiAct) {
     const double zz = v + e.bias[c];
     double yy, d1, d2;

@@ -302,6 +302,7 @@ void DeviceNet::ensure_workspace(int batch) {
   }
   // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
   w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, n_syrk_tiles_)) * kBM * kBN);
+  w.gemm_part = ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN);
   // final-layer skinny product: U [cap][n_pad][16], partials [chunks][cap][n_pad][16]
   const int64_t kfin = layers_[L - 1].cols;
   w.sk_chunks = ceil_div(kfin, dev::skinny_kchunk(m_ <= 1 ? 1 : (m_ <= 4 ? 4 : 16)));
@@ -928,6 +929,26 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.c_point_stride = n_pad_ * ldt_;
     p.ldc = ldt_;
     p.mode = dev::kStore;
+    // a single point with fewer tiles than half the SMs (c1: 28 tiles):
+    // split K, then a fixed-order reduction stores T_{l+1}
+    if (nb == 1 && !hybrid_ && p.n_tiles * 2 <= sm_count_) {
+      p.split = std::max(1, std::min(sm_count_ / p.n_tiles, p.k_blocks / 8));
+      if (p.split > 1) {
+        p.mode = dev::kPartial;
+        p.partial = w.gemm_part;  // not syrk_part: SYRKs on sb may run concurrently
+        prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
+        launch_nt(sa, tmap_a(l), dn.tm_w, p, p.n_tiles * p.split);
+        dev::RowEpi e{};
+        e.mode = dev::kEpiStore;
+        e.z = p.c;
+        e.ld = ldt_;
+        prof_begin(sa, kTagRowEpi, 0, 0);
+        dev::gemm_partial_reduce_kernel<<<dim3(4, p.n_tiles), 256, 0, sa>>>(
+            w.gemm_part, p.split, p.tiles_m, p.tiles_n, static_cast<int>(n_pad_), static_cast<int>(dn.rows), e);
+        after_launch(sa);
+        continue;
+      }
+    }
     if (hybrid_) {
       std::vector<SkJobDesc> jobs(1);
       jobs[0].ta = &tmap_a(l);
