@@ -244,6 +244,23 @@ gbopt_status gbopt_net_debug_intermediate(const gbopt_net* net,
 /* Enables/disables CUDA-graph capture of the oracle sequence (default on). */
 gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled);
 
+/* ---- KKT factorisation --------------------------------
+ * Dense symmetric-indefinite LDL^T with the contract of the reference
+ * ldlt_factor / LdltFactorization (proj/include/gbopt/linalg.hpp:24-78):
+ * finite (NUMERIC) and symmetric to 1e-12*max(1,max|A|) (STRUCTURAL)
+ * input, symmetric Ruiz equilibration, Bunch-Kaufman factorisation on the
+ * GPU, inertia with zero threshold 1e-11*max|SAS|, solve with iterative
+ * refinement when keep_input != 0; solve on a factorisation with zero
+ * pivots is GBOPT_ERR_SINGULAR.  A is n x n row-major. */
+typedef struct gbopt_ldlt gbopt_ldlt;
+gbopt_status gbopt_ldlt_factor(const double* A, size_t n, int keep_input,
+                               gbopt_ldlt** out);
+gbopt_status gbopt_ldlt_inertia(const gbopt_ldlt* f, int64_t* n_pos,
+                                int64_t* n_neg, int64_t* n_zero);
+gbopt_status gbopt_ldlt_solve(const gbopt_ldlt* f, const double* b, size_t n,
+                              double* x);
+void gbopt_ldlt_free(gbopt_ldlt* f);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -9,6 +9,6 @@ from .gbopt import (  # noqa: F401
     INIT_UNIFORM_FANIN, INIT_XAVIER_UNIFORM, INIT_XAVIER_NORMAL, INIT_NORMAL_FANIN,
     GboptError, StructuralError, NumericError, SingularError, IoError, FormatError, DimensionError,
     TruncatedError, RangeError, ArgumentError, DeviceError,
-    NeuralNet, Prng, load_weights, save_weights, random_net, random_net_ex,
+    NeuralNet, Prng, load_weights, save_weights, random_net, random_net_ex, LdltFactorization, ldlt_factor,
     device_count, last_error, version, LIB_PATH,
 )

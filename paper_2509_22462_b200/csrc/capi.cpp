@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -15,6 +16,7 @@
 #include <vector>
 
 #include "device_net.hpp"
+#include "ldlt.hpp"
 #include "net.hpp"
 
 struct gbopt_net {
@@ -23,6 +25,10 @@ struct gbopt_net {
 
 struct gbopt_prng {
   gbb::Prng rng;
+};
+
+struct gbopt_ldlt {
+  std::unique_ptr<gbb::Ldlt> f;
 };
 
 namespace {
@@ -44,6 +50,8 @@ gbopt_status to_status(const std::exception_ptr& ep) noexcept {
     return GBOPT_ERR_RANGE;
   } catch (const gbb::NumericError&) {
     return GBOPT_ERR_NUMERIC;
+  } catch (const gbb::SingularError&) {
+    return GBOPT_ERR_SINGULAR;
   } catch (const gbb::StructuralError&) {
     return GBOPT_ERR_STRUCTURAL;
   } catch (const gbb::DeviceError&) {
@@ -382,5 +390,35 @@ gbopt_status gbopt_net_debug_intermediate(const gbopt_net* net, const char* name
     d->copy_intermediate(name, static_cast<int>(layer), static_cast<int>(batch), out);
   });
 }
+
+/* ---- KKT factorisation ---------------------------------------------------- */
+
+gbopt_status gbopt_ldlt_factor(const double* A, size_t n, int keep_input, gbopt_ldlt** out) {
+  if (out == nullptr || (A == nullptr && n > 0)) return fail_argument("gbopt_ldlt_factor: null argument");
+  return guarded([&] {
+    auto h = std::make_unique<gbopt_ldlt>();
+    h->f = gbb::Ldlt::factor(A, static_cast<int64_t>(n), keep_input != 0);
+    *out = h.release();
+  });
+}
+
+gbopt_status gbopt_ldlt_inertia(const gbopt_ldlt* f, int64_t* n_pos, int64_t* n_neg, int64_t* n_zero) {
+  if (f == nullptr) return fail_argument("gbopt_ldlt_inertia: null factorization");
+  return guarded([&] {
+    if (n_pos) *n_pos = f->f->n_pos();
+    if (n_neg) *n_neg = f->f->n_neg();
+    if (n_zero) *n_zero = f->f->n_zero();
+  });
+}
+
+gbopt_status gbopt_ldlt_solve(const gbopt_ldlt* f, const double* b, size_t n, double* x) {
+  if (f == nullptr || ((b == nullptr || x == nullptr) && n > 0)) return fail_argument("gbopt_ldlt_solve: null argument");
+  return guarded([&] {
+    const std::vector<double> r = f->f->solve(b, static_cast<int64_t>(n));
+    std::copy(r.begin(), r.end(), x);
+  });
+}
+
+void gbopt_ldlt_free(gbopt_ldlt* f) { delete f; }
 
 }  // extern "C"

@@ -37,6 +37,10 @@ class TruncatedError : public IoError {
  public:
   using IoError::IoError;
 };
+class SingularError : public Error {
+ public:
+  using Error::Error;
+};
 class RangeError : public Error {
  public:
   using Error::Error;

@@ -82,6 +82,10 @@ _kernel_tag_name = _fn("gbopt_kernel_tag_name", ctypes.c_char_p, ctypes.c_int)
 _net_profile_timeline = _fn("gbopt_net_profile_timeline", _status, _vp, _sz, _vp, _vp, ctypes.POINTER(ctypes.c_int32),
                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_float),
                             ctypes.POINTER(ctypes.c_float), _sz, ctypes.POINTER(_sz))
+_ldlt_factor = _fn("gbopt_ldlt_factor", _status, _dp, _sz, ctypes.c_int, ctypes.POINTER(_vp))
+_ldlt_inertia = _fn("gbopt_ldlt_inertia", _status, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64))
+_ldlt_solve = _fn("gbopt_ldlt_solve", _status, _vp, _dp, _sz, _dp)
+_ldlt_free = _fn("gbopt_ldlt_free", None, _vp)
 _net_debug_intermediate = _fn("gbopt_net_debug_intermediate", _status, _vp, ctypes.c_char_p, _i64, _sz, _dp, _sz)
 
 # ---------------------------------------------------------------------------
@@ -394,6 +398,42 @@ def profile_timeline(net: "NeuralNet", batch: int, dX: int, dLam: int):
     _check(_net_profile_timeline(net._h, batch, dX, dLam, tags, st, t0, t1, cap, ctypes.byref(cnt)))
     return [(_kernel_tag_name(tags[i]).decode(), int(st[i]), float(t0[i]), float(t1[i]))
             for i in range(min(cnt.value, cap))]
+
+
+class LdltFactorization:
+    """GPU LDL^T of a symmetric (KKT) matrix: reference ldlt_factor /
+    LdltFactorization (proj/include/gbopt/linalg.hpp:24-78)."""
+
+    def __init__(self, A, keep_input: bool = True):
+        A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+        if A.ndim != 2 or A.shape[0] != A.shape[1]:
+            raise StructuralError(f"ldlt_factor: matrix is not square {A.shape}")
+        h = _vp()
+        _check(_ldlt_factor(_dptr(A), A.shape[0], 1 if keep_input else 0, ctypes.byref(h)))
+        self._h = h
+        self.dim = A.shape[0]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _ldlt_free(h)
+            self._h = None
+
+    @property
+    def inertia(self):
+        p, n, z = _i64(), _i64(), _i64()
+        _check(_ldlt_inertia(self._h, ctypes.byref(p), ctypes.byref(n), ctypes.byref(z)))
+        return p.value, n.value, z.value
+
+    def solve(self, b):
+        b = _vec(b)
+        x = np.empty_like(b)
+        _check(_ldlt_solve(self._h, _dptr(b), b.size, _dptr(x)))
+        return x
+
+
+def ldlt_factor(A, keep_input: bool = True) -> LdltFactorization:
+    return LdltFactorization(A, keep_input)
 
 
 def load_weights(path: str) -> NeuralNet:

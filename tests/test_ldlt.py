@@ -1,0 +1,107 @@
+"""KKT factorisation row (f3): GPU LDL^T vs the reference contract
+(proj/tests/test_linalg.cpp cases restated) and the CPU oracle."""
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from oracle import ldlt_oracle as lo
+
+
+def test_oracle_inertia_known_spectra():
+    rng = np.random.default_rng(3)
+    assert lo.inertia(np.eye(5)) == (5, 0, 0)
+    assert lo.inertia(np.diag([2.0, -5.0])) == (1, 1, 0)
+    A = lo.matrix_with_spectrum(rng, [4, 3, 2, 1, -1, -2, -3, 0])
+    assert lo.inertia(A) == (4, 3, 1)
+    assert lo.inertia(np.zeros((4, 4))) == (0, 0, 4)
+    for n in (5, 17, 40):
+        A = lo.matrix_with_spectrum(rng, rng.uniform(-3, 3, n))
+        ev = np.linalg.eigvalsh(A)
+        assert lo.inertia(A) == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
+
+
+def test_cpu_argument_checks():
+    import paper_2509_22462_b200 as gb
+    with pytest.raises(gb.StructuralError):
+        gb.LdltFactorization(np.ones((2, 3)))
+    with pytest.raises(gb.NumericError):
+        gb.LdltFactorization(np.array([[1.0, np.nan], [np.nan, 1.0]]))
+    with pytest.raises(gb.StructuralError):
+        gb.LdltFactorization(np.array([[1.0, 2.0], [0.0, 1.0]]))  # not symmetric
+    if gb.device_count() == 0:
+        with pytest.raises(gb.DeviceError):
+            gb.LdltFactorization(np.eye(3))
+
+
+@pytest.mark.gpu
+class TestGpuLdlt:
+    @pytest.fixture(autouse=True)
+    def _gpu(self):
+        if not has_gpu():
+            pytest.skip("no GPU")
+
+    def test_known_inertias(self):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(3)
+        assert gb.ldlt_factor(np.eye(6)).inertia == (6, 0, 0)                    # test_linalg.cpp:42
+        assert gb.ldlt_factor(np.diag([2.0, -5.0])).inertia == (1, 1, 0)         # :47
+        assert gb.ldlt_factor(np.array([[3.0]])).inertia == (1, 0, 0)            # :55
+        assert gb.ldlt_factor(np.array([[-0.5]])).inertia == (0, 1, 0)
+        z = np.array([[0.0, 1.0], [1.0, 0.0]])                                   # :63 zero diagonal
+        assert gb.ldlt_factor(z).inertia == (1, 1, 0)
+        A = lo.matrix_with_spectrum(rng, [4, 3, 2, 1, -1, -2, -3, 0])           # :76
+        assert gb.ldlt_factor(A).inertia == (4, 3, 1)
+        assert gb.ldlt_factor(np.zeros((4, 4))).inertia == (0, 0, 4)             # :211
+
+    @pytest.mark.parametrize("n", [3, 10, 64, 200, 513])
+    def test_inertia_matches_oracle_and_eigenvalues(self, n):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(n)
+        eigs = rng.uniform(1, 5, n) * rng.choice([-1.0, 1.0], n)
+        A = lo.matrix_with_spectrum(rng, eigs)
+        got = gb.ldlt_factor(A).inertia
+        assert got == lo.inertia(A) == (int((eigs > 0).sum()), int((eigs < 0).sum()), 0)
+
+    def test_rank_deficiency_counts_zeros(self):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(11)
+        eigs = np.array([3.0, -2.0, 1.5, 0.0, 0.0, -1.0])
+        A = lo.matrix_with_spectrum(rng, eigs)
+        f = gb.ldlt_factor(A)
+        assert f.inertia == (2, 2, 2)
+        with pytest.raises(gb.SingularError):
+            f.solve(np.ones(6))
+
+    @pytest.mark.parametrize("keep", [True, False])
+    def test_solve_round_trip(self, keep):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(5)
+        A = lo.matrix_with_spectrum(rng, rng.uniform(0.5, 4, 40) * rng.choice([-1.0, 1.0], 40))
+        f = gb.ldlt_factor(A, keep_input=keep)
+        for _ in range(10):
+            v = rng.uniform(-1, 1, 40)
+            x = f.solve(A @ v)
+            assert np.abs(x - v).max() <= 1e-10
+
+    def test_ipm_like_badly_scaled_kkt(self):
+        """Barrier diagonals of 1e8 beside O(1) constraint rows (the reason
+        for the Ruiz equilibration, linalg.cpp:72-84): inertia (n, m, 0) and
+        a small residual."""
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(8)
+        n, m = 60, 20
+        Hm = lo.matrix_with_spectrum(rng, rng.uniform(1, 3, n)) + np.diag(10.0 ** rng.uniform(-2, 8, n))
+        Jm = rng.uniform(-1, 1, (m, n))
+        K = np.block([[Hm, Jm.T], [Jm, -1e-8 * np.eye(m)]])
+        f = gb.ldlt_factor(K)
+        assert f.inertia == (n, m, 0) == lo.inertia(K)
+        b = rng.uniform(-1, 1, n + m)
+        x = f.solve(b)
+        assert np.abs(K @ x - b).max() <= 1e-8 * (np.abs(K).max() * np.abs(x).max() + np.abs(b).max())
+
+    def test_permutation_invariance(self):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(2)
+        A = lo.matrix_with_spectrum(rng, [5, -4, 3, -2, 1, 0.5, -0.25])
+        p = rng.permutation(7)
+        assert gb.ldlt_factor(A).inertia == gb.ldlt_factor(A[np.ix_(p, p)]).inertia == (4, 3, 0)
