@@ -7,13 +7,16 @@
 //     1e-12 * max(1, max|A|) (StructuralError)            linalg.cpp:45-71
 //   * symmetric Ruiz equilibration, <= 20 rounds, tol 0.01  linalg.cpp:72-99
 //   * Bunch-Kaufman factorisation P S A S P^T = L D L^T of the equilibrated
-//     matrix -- here cuSOLVER's dsytrf on the device (a plain library
-//     factorisation: this row is outside the oracle's hot path)
+//     matrix -- cuSOLVER's dsytrf (a plain library factorisation: this row
+//     is outside the oracle's hot path)
 //   * inertia from the 1x1 / 2x2 pivot blocks with zero threshold
 //     1e-11 * max|S A S|                                     linalg.cpp:101-120
 //   * solve: refuses singular factorizations (SingularError); x = S y with
 //     S A S y = S b, iterative refinement while the residual shrinks, at
 //     most 10 rounds, returning the best iterate              linalg.cpp:393-438
+// Everything O(n^2) per pass (checks, equilibration, residuals) runs on the
+// device too; only the 2n pivot-block entries and vectors cross PCIe after
+// the matrix upload.
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -37,16 +40,85 @@ void cs_check(cusolverStatus_t s, const char* what) {
 #define CK(x) cuda_check((x), #x)
 #define CS(x) cs_check((x), #x)
 
+__device__ inline void atomic_max_pos(double* addr, double v) {
+  // v >= 0: ordering of non-negative doubles matches their bit patterns
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), __double_as_longlong(v));
+}
+
+// out[0] = max|A|, out[1] = max|A - A^T| (lower vs upper), out[2] = #non-finite
+__global__ void ldlt_check_kernel(const double* __restrict__ a, int64_t n, double* out) {
+  double amax = 0.0, asym = 0.0, bad = 0.0;
+  const int64_t nn = n * n;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nn;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    const double v = a[e];
+    if (!isfinite(v)) {
+      bad += 1.0;
+      continue;
+    }
+    amax = fmax(amax, fabs(v));
+    if (j < i) asym = fmax(asym, fabs(v - a[j * n + i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(out + 0, amax);
+    if (asym == asym) atomic_max_pos(out + 1, asym);
+    if (bad > 0) atomicAdd(out + 2, bad);
+  }
+}
+
+// cmax[j] = max_i |A[i][j]|  (one warp per column, symmetric: rows = cols)
+__global__ void ldlt_colmax_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ cmax) {
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (col >= n) return;
+  const int lane = threadIdx.x & 31;
+  // row `col` of the symmetric matrix == column `col`: read it contiguously
+  double m = 0.0;
+  for (int64_t k = lane; k < n; k += 32) m = fmax(m, fabs(a[col * n + k]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) cmax[col] = m;
+}
+
+__global__ void ldlt_scale_kernel(double* __restrict__ a, int64_t n, const double* __restrict__ rs) {
+  const int64_t nn = n * n;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nn;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    a[e] *= rs[e / n] * rs[e % n];
+}
+
+// r = b - A x (one warp per row), also |r|_inf and |x|_inf into out[0..1]
+__global__ void ldlt_residual_kernel(const double* __restrict__ a, int64_t n, const double* __restrict__ x,
+                                     const double* __restrict__ b, double* __restrict__ r, double* out) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int64_t k = lane; k < n; k += 32) s = fma(a[row * n + k], x[k], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    const double v = b[row] - s;
+    r[row] = v;
+    atomic_max_pos(out + 0, fabs(v));
+    atomic_max_pos(out + 1, fabs(x[row]));
+  }
+}
+
+int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t>((work + per - 1) / per, 4096)); }
+
 }  // namespace
 
 Ldlt::~Ldlt() {
   if (dev_ >= 0) {
     DeviceGuard g(dev_);
-    if (d_fact_) cudaFree(d_fact_);
-    if (d_ipiv_) cudaFree(d_ipiv_);
-    if (d_work_) cudaFree(d_work_);
-    if (d_info_) cudaFree(d_info_);
-    if (d_rhs_) cudaFree(d_rhs_);
+    for (void* p : {static_cast<void*>(d_fact_), static_cast<void*>(d_ipiv_), static_cast<void*>(d_work_),
+                    static_cast<void*>(d_info_), static_cast<void*>(d_rhs_), static_cast<void*>(d_input_),
+                    static_cast<void*>(d_vec_), static_cast<void*>(d_ipiv64_), d_sbuf_})
+      if (p) cudaFree(p);
     if (handle_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(handle_));
     if (stream_) cudaStreamDestroy(stream_);
   }
@@ -54,49 +126,9 @@ Ldlt::~Ldlt() {
 
 std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, int device) {
   if (n < 0) throw StructuralError("ldlt_factor: negative dimension");
-  for (int64_t i = 0; i < n * n; ++i)
-    if (!std::isfinite(a[i])) throw NumericError("ldlt_factor: matrix contains NaN or Inf");
-  double amax = 0.0;
-  for (int64_t i = 0; i < n * n; ++i) amax = std::max(amax, std::fabs(a[i]));
-  const double sym_tol = 1e-12 * std::max(1.0, amax);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t j = 0; j < i; ++j) {
-      const double dev = std::fabs(a[i * n + j] - a[j * n + i]);
-      if (dev > sym_tol)
-        throw StructuralError("ldlt_factor: matrix is not symmetric (max deviation " + std::to_string(dev) + ")");
-    }
-
   auto f = std::unique_ptr<Ldlt>(new Ldlt());
   f->n_ = n;
-  // Symmetric Ruiz equilibration (linalg.cpp:72-99).
-  std::vector<double> bal(a, a + n * n);
-  f->scale_.assign(static_cast<size_t>(n), 1.0);
-  {
-    constexpr int kRuizMaxRounds = 20;
-    constexpr double kRuizTol = 0.01;
-    std::vector<double> rs(static_cast<size_t>(n));
-    for (int round = 0; round < kRuizMaxRounds; ++round) {
-      double dev = 0.0;
-      for (int64_t i = 0; i < n; ++i) {
-        double cmax = 0.0;
-        for (int64_t k = 0; k < n; ++k) cmax = std::max(cmax, std::fabs(bal[k * n + i]));
-        rs[i] = cmax > 0.0 ? 1.0 / std::sqrt(cmax) : 1.0;
-        if (cmax > 0.0) dev = std::max(dev, std::fabs(cmax - 1.0));
-      }
-      if (dev <= kRuizTol) break;
-      for (int64_t i = 0; i < n; ++i)
-        for (int64_t j = 0; j < n; ++j) bal[i * n + j] *= rs[i] * rs[j];
-      for (int64_t i = 0; i < n; ++i) f->scale_[i] *= rs[i];
-    }
-  }
-  double bmax = 0.0;
-  for (double v : bal) bmax = std::max(bmax, std::fabs(v));
-  f->zero_thresh_ = 1e-11 * (n > 0 ? bmax : 0.0);
-  if (keep_input) f->input_ = bal;
   if (n == 0) return f;
-
-  // Device factorisation (lower triangle; row-major == column-major for a
-  // symmetric matrix).
   if (device < 0) {
     if (cudaGetDevice(&device) != cudaSuccess) {
       cudaGetLastError();
@@ -110,33 +142,87 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   }
   f->dev_ = device;
   DeviceGuard g(device);
-  CK(cudaStreamCreateWithFlags(&f->stream_, cudaStreamNonBlocking));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  f->stream_ = st;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n) * n;
+  CK(cudaMalloc(&f->d_fact_, bytes));
+  CK(cudaMalloc(&f->d_vec_, sizeof(double) * (4 * n + 8)));  // rs | scale | cmax | x ... | scalars
+  CK(cudaMalloc(&f->d_rhs_, sizeof(double) * n));
+  CK(cudaMemcpyAsync(f->d_fact_, a, bytes, cudaMemcpyHostToDevice, st));
+  double* rs = f->d_vec_;
+  double* scale = rs + n;
+  double* cmax = scale + n;
+  double* scal = f->d_vec_ + 4 * n;  // 8 scalars
+
+  // checks (linalg.cpp:45-71)
+  CK(cudaMemsetAsync(scal, 0, sizeof(double) * 3, st));
+  ldlt_check_kernel<<<blocks_for(n * n, 256), 256, 0, st>>>(f->d_fact_, n, scal);
+  CK(cudaGetLastError());
+  double chk[3];
+  CK(cudaMemcpyAsync(chk, scal, sizeof(chk), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (chk[2] > 0) throw NumericError("ldlt_factor: matrix contains NaN or Inf");
+  if (chk[1] > 1e-12 * std::max(1.0, chk[0]))
+    throw StructuralError("ldlt_factor: matrix is not symmetric (max deviation " + std::to_string(chk[1]) + ")");
+
+  // Ruiz equilibration (linalg.cpp:72-99) on the device; the round control
+  // (max |cmax - 1|) is a host reduction of n values per round.
+  std::vector<double> h_cmax(static_cast<size_t>(n)), h_rs(static_cast<size_t>(n));
+  f->scale_.assign(static_cast<size_t>(n), 1.0);
+  for (int round = 0; round < 20; ++round) {
+    ldlt_colmax_kernel<<<blocks_for(n, 8), 256, 0, st>>>(f->d_fact_, n, cmax);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h_cmax.data(), cmax, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double dev = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      h_rs[i] = h_cmax[i] > 0.0 ? 1.0 / std::sqrt(h_cmax[i]) : 1.0;
+      if (h_cmax[i] > 0.0) dev = std::max(dev, std::fabs(h_cmax[i] - 1.0));
+    }
+    if (dev <= 0.01) break;
+    CK(cudaMemcpyAsync(rs, h_rs.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    ldlt_scale_kernel<<<blocks_for(n * n, 256), 256, 0, st>>>(f->d_fact_, n, rs);
+    CK(cudaGetLastError());
+    for (int64_t i = 0; i < n; ++i) f->scale_[i] *= h_rs[i];
+  }
+  double bmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) bmax = std::max(bmax, h_cmax[i]);  // cmax of the final matrix
+  f->zero_thresh_ = 1e-11 * bmax;
+  CK(cudaMemcpyAsync(scale, f->scale_.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  if (keep_input) {
+    CK(cudaMalloc(&f->d_input_, bytes));
+    CK(cudaMemcpyAsync(f->d_input_, f->d_fact_, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+
+  // Bunch-Kaufman on the device (lower; row-major == column-major here)
   cusolverDnHandle_t h = nullptr;
   CS(cusolverDnCreate(&h));
   f->handle_ = h;
-  CS(cusolverDnSetStream(h, f->stream_));
-  const size_t bytes = sizeof(double) * static_cast<size_t>(n) * n;
-  CK(cudaMalloc(&f->d_fact_, bytes));
+  CS(cusolverDnSetStream(h, st));
   CK(cudaMalloc(&f->d_ipiv_, sizeof(int) * n));
+  CK(cudaMalloc(&f->d_ipiv64_, sizeof(int64_t) * n));
   CK(cudaMalloc(&f->d_info_, sizeof(int)));
-  CK(cudaMalloc(&f->d_rhs_, sizeof(double) * n));
-  CK(cudaMemcpyAsync(f->d_fact_, bal.data(), bytes, cudaMemcpyHostToDevice, f->stream_));
   int lwork = 0;
   CS(cusolverDnDsytrf_bufferSize(h, static_cast<int>(n), f->d_fact_, static_cast<int>(n), &lwork));
   CK(cudaMalloc(&f->d_work_, sizeof(double) * std::max(lwork, 1)));
   CS(cusolverDnDsytrf(h, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), f->d_fact_, static_cast<int>(n), f->d_ipiv_,
                       f->d_work_, lwork, f->d_info_));
-  // D blocks and pivots back to the host for the inertia.
-  std::vector<double> fact(static_cast<size_t>(n) * n);
+  // only the pivot blocks come back: diagonal and first subdiagonal
+  std::vector<double> diag(static_cast<size_t>(n)), sub(static_cast<size_t>(n), 0.0);
   f->ipiv_.assign(static_cast<size_t>(n), 0);
   int info = 0;
-  CK(cudaMemcpyAsync(fact.data(), f->d_fact_, bytes, cudaMemcpyDeviceToHost, f->stream_));
-  CK(cudaMemcpyAsync(f->ipiv_.data(), f->d_ipiv_, sizeof(int) * n, cudaMemcpyDeviceToHost, f->stream_));
-  CK(cudaMemcpyAsync(&info, f->d_info_, sizeof(int), cudaMemcpyDeviceToHost, f->stream_));
-  CK(cudaStreamSynchronize(f->stream_));
+  CK(cudaMemcpy2DAsync(diag.data(), sizeof(double), f->d_fact_, sizeof(double) * (n + 1), sizeof(double), n,
+                       cudaMemcpyDeviceToHost, st));
+  if (n > 1)
+    CK(cudaMemcpy2DAsync(sub.data(), sizeof(double), f->d_fact_ + 1, sizeof(double) * (n + 1), sizeof(double), n - 1,
+                         cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(f->ipiv_.data(), f->d_ipiv_, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&info, f->d_info_, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   if (info < 0) throw DeviceError("ldlt_factor: dsytrf rejected argument " + std::to_string(-info));
-  // column-major element (i, j) of the factor: fact[j * n + i]
-  auto D = [&](int64_t i, int64_t j) { return fact[static_cast<size_t>(j * n + i)]; };
+  std::vector<int64_t> ipiv64(f->ipiv_.begin(), f->ipiv_.end());
+  CK(cudaMemcpyAsync(f->d_ipiv64_, ipiv64.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
   auto classify = [&](double eig) {
     if (std::fabs(eig) <= f->zero_thresh_) ++f->n_zero_;
     else if (eig > 0.0) ++f->n_pos_;
@@ -144,43 +230,32 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   };
   for (int64_t k = 0; k < n;) {
     if (f->ipiv_[static_cast<size_t>(k)] > 0) {  // 1x1 block (LAPACK lower convention)
-      classify(D(k, k));
+      classify(diag[k]);
       k += 1;
-    } else {  // 2x2 block in rows/cols k, k+1
-      const double p = D(k, k), q = D(k + 1, k), r = D(k + 1, k + 1);
+    } else {  // 2x2 block D(k:k+1, k:k+1), D(k+1,k) in the subdiagonal
+      const double p = diag[k], q = sub[k], r = diag[k + 1];
       const double mid = 0.5 * (p + r), rad = std::hypot(0.5 * (p - r), q);
       classify(mid + rad);
       classify(mid - rad);
       k += 2;
     }
   }
+  size_t dws = 0, hws = 0;
+  CS(cusolverDnXsytrs_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, f->d_fact_, n, f->d_ipiv64_, CUDA_R_64F,
+                                 f->d_rhs_, n, &dws, &hws));
+  f->sws_dev_ = std::max<size_t>(dws, 8);
+  f->sws_host_ = std::max<size_t>(hws, 8);
+  CK(cudaMalloc(&f->d_sbuf_, f->sws_dev_));
+  CK(cudaStreamSynchronize(st));
   return f;
 }
 
-void Ldlt::solve_factored(std::vector<double>& x) const {
-  DeviceGuard g(dev_);
+// in place on the device vector v: v <- (S A S)^{-1} v
+void Ldlt::solve_factored(double* d_v) const {
   auto h = static_cast<cusolverDnHandle_t>(handle_);
-  const int64_t n = n_;
-  std::vector<int64_t> ipiv64(ipiv_.begin(), ipiv_.end());
-  int64_t* d_ipiv64 = nullptr;
-  CK(cudaMalloc(&d_ipiv64, sizeof(int64_t) * n));
-  CK(cudaMemcpyAsync(d_ipiv64, ipiv64.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, stream_));
-  CK(cudaMemcpyAsync(d_rhs_, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice, stream_));
-  size_t dws = 0, hws = 0;
-  CS(cusolverDnXsytrs_bufferSize(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, d_fact_, n, d_ipiv64, CUDA_R_64F, d_rhs_,
-                                 n, &dws, &hws));
-  void* dbuf = nullptr;
-  CK(cudaMalloc(&dbuf, std::max<size_t>(dws, 8)));
-  std::vector<char> hbuf(std::max<size_t>(hws, 8));
-  int* d_info = nullptr;
-  CK(cudaMalloc(&d_info, sizeof(int)));
-  CS(cusolverDnXsytrs(h, CUBLAS_FILL_MODE_LOWER, n, 1, CUDA_R_64F, d_fact_, n, d_ipiv64, CUDA_R_64F, d_rhs_, n, dbuf,
-                      dws, hbuf.data(), hws, d_info));
-  CK(cudaMemcpyAsync(x.data(), d_rhs_, sizeof(double) * n, cudaMemcpyDeviceToHost, stream_));
-  CK(cudaStreamSynchronize(stream_));
-  cudaFree(dbuf);
-  cudaFree(d_info);
-  cudaFree(d_ipiv64);
+  std::vector<char> hbuf(sws_host_);
+  CS(cusolverDnXsytrs(h, CUBLAS_FILL_MODE_LOWER, n_, 1, CUDA_R_64F, d_fact_, n_, d_ipiv64_, CUDA_R_64F, d_v, n_,
+                      d_sbuf_, sws_dev_, hbuf.data(), sws_host_, d_info_));
 }
 
 std::vector<double> Ldlt::solve(const double* b, int64_t len) const {
@@ -190,39 +265,62 @@ std::vector<double> Ldlt::solve(const double* b, int64_t len) const {
   if (n_zero_ > 0)
     throw SingularError("ldlt_solve: matrix is singular (" + std::to_string(n_zero_) + " zero pivots)");
   const int64_t n = n_;
+  std::vector<double> x(static_cast<size_t>(n));
+  if (n == 0) return x;
+  DeviceGuard g(dev_);
+  cudaStream_t st = stream_;
   std::vector<double> bs(static_cast<size_t>(n));
   for (int64_t i = 0; i < n; ++i) bs[i] = scale_[i] * b[i];
-  std::vector<double> x = bs;
-  if (n > 0) solve_factored(x);
-  if (!input_.empty() && n > 0) {
-    double a_max = 0.0, b_norm = 0.0;
-    for (double v : input_) a_max = std::max(a_max, std::fabs(v));
-    for (double v : bs) b_norm = std::max(b_norm, std::fabs(v));
-    constexpr int kMaxRounds = 10;
+  double b_norm = 0.0;
+  for (double v : bs) b_norm = std::max(b_norm, std::fabs(v));
+  double* d_bs = d_vec_;            // reuse: rs slot
+  double* d_x = d_vec_ + 2 * n;     // cmax slot
+  double* d_r = d_vec_ + 3 * n;
+  double* scal = d_vec_ + 4 * n;
+  CK(cudaMemcpyAsync(d_bs, bs.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_x, d_bs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  solve_factored(d_x);
+  if (d_input_) {
+    // refinement (linalg.cpp:403-435): residuals on the device, round
+    // control on the host from two scalars per round
+    const double a_max = zero_thresh_ / 1e-11;
     const double eps = std::numeric_limits<double>::epsilon();
-    std::vector<double> best_x = x, r(static_cast<size_t>(n));
+    double* d_best = d_rhs_;
     double best_res = std::numeric_limits<double>::infinity();
-    for (int round = 0; round < kMaxRounds; ++round) {
-      double res = 0.0, xn = 0.0;
-      for (int64_t i = 0; i < n; ++i) {
-        double s = bs[i];
-        const double* row = input_.data() + i * n;
-        for (int64_t k = 0; k < n; ++k) s -= row[k] * x[k];
-        r[i] = s;
-        res = std::max(res, std::fabs(s));
-        xn = std::max(xn, std::fabs(x[i]));
-      }
-      if (!(res < best_res)) break;  // stalled at this factorization's accuracy
-      best_res = res;
-      best_x = x;
-      if (res <= eps * (b_norm + a_max * xn)) break;
-      solve_factored(r);
-      for (int64_t i = 0; i < n; ++i) x[i] += r[i];
+    CK(cudaMemcpyAsync(d_best, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    for (int round = 0; round < 10; ++round) {
+      CK(cudaMemsetAsync(scal, 0, sizeof(double) * 2, st));
+      ldlt_residual_kernel<<<blocks_for(n, 8), 256, 0, st>>>(d_input_, n, d_x, d_bs, d_r, scal);
+      CK(cudaGetLastError());
+      double rr[2];
+      CK(cudaMemcpyAsync(rr, scal, sizeof(rr), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!(rr[0] < best_res)) break;
+      best_res = rr[0];
+      CK(cudaMemcpyAsync(d_best, d_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      if (rr[0] <= eps * (b_norm + a_max * rr[1])) break;
+      solve_factored(d_r);
+      refine_add_kernel_launch(d_x, d_r, n, st);
     }
-    x = best_x;
+    CK(cudaMemcpyAsync(x.data(), d_best, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(x.data(), d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   }
+  CK(cudaStreamSynchronize(st));
   for (int64_t i = 0; i < n; ++i) x[i] *= scale_[i];
   return x;
+}
+
+namespace {
+__global__ void ldlt_axpy_kernel(double* __restrict__ x, const double* __restrict__ r, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] += r[i];
+}
+}  // namespace
+
+void Ldlt::refine_add_kernel_launch(double* d_x, const double* d_r, int64_t n, cudaStream_t st) const {
+  ldlt_axpy_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(d_x, d_r, n);
+  CK(cudaGetLastError());
 }
 
 }  // namespace gbb

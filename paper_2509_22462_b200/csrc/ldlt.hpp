@@ -14,9 +14,9 @@ namespace gbb {
 
 class Ldlt {
  public:
-  // Factors the symmetric n x n matrix `a` (row-major) on CUDA device
-  // `device` (-1: current).  keep_input retains the equilibrated matrix for
-  // iterative refinement in solve().
+  // Factors the symmetric n x n matrix `a` (row-major, host) on CUDA device
+  // `device` (-1: current).  keep_input retains the equilibrated matrix on
+  // the device for iterative refinement in solve().
   static std::unique_ptr<Ldlt> factor(const double* a, int64_t n, bool keep_input, int device = -1);
   ~Ldlt();
   Ldlt(const Ldlt&) = delete;
@@ -30,20 +30,26 @@ class Ldlt {
 
  private:
   Ldlt() = default;
-  void solve_factored(std::vector<double>& x) const;
+  void solve_factored(double* d_v) const;
+  void refine_add_kernel_launch(double* d_x, const double* d_r, int64_t n, cudaStream_t st) const;
 
   int64_t n_ = 0, n_pos_ = 0, n_neg_ = 0, n_zero_ = 0;
   double zero_thresh_ = 0.0;
-  std::vector<double> scale_, input_;
+  std::vector<double> scale_;
   std::vector<int> ipiv_;
   int dev_ = -1;
   cudaStream_t stream_ = nullptr;
   void* handle_ = nullptr;  // cusolverDnHandle_t
   double* d_fact_ = nullptr;
+  double* d_input_ = nullptr;  // equilibrated copy (keep_input)
   int* d_ipiv_ = nullptr;
+  int64_t* d_ipiv64_ = nullptr;
   double* d_work_ = nullptr;
   int* d_info_ = nullptr;
   double* d_rhs_ = nullptr;
+  double* d_vec_ = nullptr;
+  void* d_sbuf_ = nullptr;
+  size_t sws_dev_ = 0, sws_host_ = 0;
 };
 
 }  // namespace gbb
