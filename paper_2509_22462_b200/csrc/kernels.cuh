@@ -746,6 +746,75 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int
 // ---------------------------------------------------------------------------
 constexpr int kFwdWarps = 8;
 
+// Single point (the c2 hot case): HBM-streaming GEMV, no shared-memory
+// staging and no block barriers in the k loop (y is re-read through L1).
+// WPR warps share a row (split K, fixed-order reduction through shared
+// memory: deterministic) so layers with few rows still fill the GPU; each
+// lane keeps 8 independent 16-byte weight loads in flight.
+template <int WPR>
+__global__ void __launch_bounds__(kFwdWarps * 32)
+    fwd_row1_kernel(const double* __restrict__ w, int64_t ldw, const double* __restrict__ bias, int rows, int k_dim,
+                    const double* __restrict__ yin, int act, double* __restrict__ z_out, double* __restrict__ y_out,
+                    double* __restrict__ s1_out, double* __restrict__ s2_out) {
+  constexpr int kRowsPerCta = kFwdWarps / WPR;
+  __shared__ double part[kFwdWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kRowsPerCta + warp / WPR;
+  const int part_idx = warp % WPR;
+  // this warp's k range: whole 64-double chunks, split WPR ways
+  const int chunks = (k_dim + 63) / 64;
+  const int c0 = (chunks * part_idx) / WPR, c1 = (chunks * (part_idx + 1)) / WPR;
+  double acc0 = 0.0, acc1 = 0.0;
+  if (row < rows) {
+    const double* wr = w + static_cast<int64_t>(row) * ldw;
+    int c = c0;
+    // kU chunks (kU x 16 B per lane) per step: loads first, then the FMAs
+    constexpr int kU = 8;  // 16 measured slower (3.9 vs 4.6 TB/s)
+    for (; c + kU <= c1; c += kU) {
+      double2 wv[kU], yv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = (c + u) * 64 + 2 * lane;
+        wv[u] = k < k_dim ? __ldcs(reinterpret_cast<const double2*>(wr + k)) : make_double2(0.0, 0.0);
+        yv[u] = k < k_dim ? __ldg(reinterpret_cast<const double2*>(yin + k)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        acc0 = fma(wv[u].x, yv[u].x, acc0);
+        acc1 = fma(wv[u].y, yv[u].y, acc1);
+      }
+    }
+    for (; c < c1; ++c) {
+      const int k = c * 64 + 2 * lane;
+      if (k < k_dim) {
+        const double2 wv = __ldcs(reinterpret_cast<const double2*>(wr + k));
+        const double2 yv = __ldg(reinterpret_cast<const double2*>(yin + k));
+        acc0 = fma(wv.x, yv.x, acc0);
+        acc1 = fma(wv.y, yv.y, acc1);
+      }
+    }
+  }
+  double v = acc0 + acc1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (WPR > 1) {
+    if (lane == 0) part[warp] = v;
+    __syncthreads();
+    if (part_idx != 0) return;
+    v = 0.0;
+    for (int i = 0; i < WPR; ++i) v += part[warp + i];  // fixed order
+  }
+  if (lane == 0 && row < rows) {
+    const double zz = v + bias[row];
+    double yy, d1, d2;
+    act_eval(act, zz, yy, d1, d2);
+    z_out[row] = zz;
+    y_out[row] = yy;
+    s1_out[row] = d1;
+    s2_out[row] = d2;
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kFwdWarps * 32)
     fwd_rows_kernel(const double* __restrict__ w, int64_t ldw, const double* __restrict__ bias, int rows, int k_dim,
@@ -890,7 +959,7 @@ __global__ void __launch_bounds__(kAdjThreads)
 #pragma unroll
   for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0;
   const double* wp = w + static_cast<int64_t>(r0) * ldw + k;
-#pragma unroll 8
+#pragma unroll 16
   for (int i = 0; i < nr; ++i) {
     const double2 wv = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw));
 #pragma unroll

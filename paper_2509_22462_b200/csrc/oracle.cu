@@ -590,7 +590,25 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     dim3 grid(ceil_div(d.rows, dev::kFwdWarps), ceil_div(nb, nbpass));
     const int act = d.act == kSoftmax ? kLinear : d.act;
     prof_begin(sa, kTagFwd, 2.0 * d.rows * d.cols * nb, 8.0 * d.rows * d.cols * ceil_div(nb, nbpass));
-    if (nbpass == 8)
+    if (nb == 1) {
+      // warps per row so that short layers (the 10-row output) still spread
+      // over the GPU: aim at >= 16 warps per SM
+      const int64_t target = static_cast<int64_t>(sm_count_) * 16;
+      const int wpr = d.rows >= target ? 1 : d.rows * 2 >= target ? 2 : d.rows * 4 >= target ? 4 : 8;
+      const dim3 g1(ceil_div(d.rows * wpr, dev::kFwdWarps));
+      if (wpr == 1)
+        dev::fwd_row1_kernel<1><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+      else if (wpr == 2)
+        dev::fwd_row1_kernel<2><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+      else if (wpr == 4)
+        dev::fwd_row1_kernel<4><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+      else
+        dev::fwd_row1_kernel<8><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+    } else if (nbpass == 8)
       dev::fwd_rows_kernel<8><<<grid, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
     else if (nbpass == 4)
