@@ -133,9 +133,14 @@ def test_batched_equals_single():
     X = rng.uniform(-1, 1, (9, 20))
     L = rng.uniform(-1, 1, (9, 5))
     Y, J, H = net.oracle_batched(X, L)
+    # batched and single-point calls use different GEMV reductions (the
+    # single-point forward splits k across warps), so they agree to rounding;
+    # points within one batched call are evaluated identically.
     for b in range(9):
         y, j, h = net.oracle(X[b], L[b])
-        assert np.array_equal(Y[b], y) and np.array_equal(J[b], j) and np.array_equal(H[b], h)
+        assert orc.rel_err(Y[b], y) <= 1e-14 and orc.rel_err(J[b], j) <= 1e-13 and orc.rel_err(H[b], h) <= 1e-13
+    Y2, J2, H2 = net.oracle_batched(np.repeat(X[:1], 9, 0), np.repeat(L[:1], 9, 0))
+    assert all(np.array_equal(Y2[0], Y2[b]) and np.array_equal(H2[0], H2[b]) for b in range(9))
 
 
 def test_graphs_off_matches_graphs_on():
@@ -228,7 +233,7 @@ def test_c2_full_size_properties():
     _, jf, _ = net.oracle(x, l1)
     assert orc.rel_err(jf, j) <= 1e-12
     Y, J, H = net.oracle_batched(np.stack([x, x]), np.stack([l1, l1]))
-    assert np.array_equal(J[0], jf) and np.array_equal(J[1], jf)
+    assert np.array_equal(J[0], J[1]) and orc.rel_err(J[0], jf) <= 1e-13
     assert np.array_equal(H[0], H[1]) and orc.rel_err(H[0], h1) <= 1e-13
 
 
