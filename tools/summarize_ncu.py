@@ -12,7 +12,7 @@ from collections import OrderedDict
 
 MINE = ("nt_mma", "fwd_rows", "adj_", "skinny", "syrk", "softmax", "jacobian_out", "symmetrize", "copy_rows",
         "small_k", "act_", "ew_")
-TAGS = [("nt_mma", "nt_mma_kernel"), ("fwd_rows", "fwd_rows_kernel"), ("adj_cols", "adj_cols_kernel"),
+TAGS = [("nt_mma", "nt_mma_kernel"), ("fwd_row1", "fwd_row1_kernel"), ("fwd_rows", "fwd_rows_kernel"), ("adj_cols", "adj_cols_kernel"),
         ("adj_reduce", "adj_reduce_kernel"), ("adj_seed", "adj_seed_kernel"), ("skinny_nt", "skinny_nt_kernel"),
         ("skinny_reduce", "skinny_reduce_kernel"), ("syrk_partial_reduce", "syrk_partial_reduce_kernel"),
         ("jacobian_out", "jacobian_out_kernel"), ("symmetrize", "symmetrize_out_kernel"),
@@ -35,7 +35,8 @@ def launches(path, out):
     mine = [(short(n), t, g) for n, t, g in recs if short(n)]
     # one oracle evaluation = the launches between consecutive fwd_rows runs of
     # length L; take the LAST complete evaluation (graph replay, warm).
-    starts = [i for i in range(len(mine)) if mine[i][0] == "fwd_rows" and (i == 0 or mine[i - 1][0] != "fwd_rows")]
+    fwd = ("fwd_rows", "fwd_row1")
+    starts = [i for i in range(len(mine)) if mine[i][0] in fwd and (i == 0 or mine[i - 1][0] not in fwd)]
     seg = mine[starts[-2]:starts[-1]] if len(starts) >= 2 else mine
     unit = "ns" if rows and rows[0]["Metric Unit"] == "ns" else rows[0]["Metric Unit"]
     scale = 1e-3 if unit == "ns" else (1.0 if unit == "us" else 1e3)
