@@ -205,6 +205,31 @@ gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net,
                                              size_t m, double* dY, double* dJ,
                                              double* dH, void* stream);
 
+/* Oracle schedule of this handle's fused (y, J, H) evaluations:
+ *   -1  automatic (default; GBOPT_DATAFLOW=0/1 in the environment at bind
+ *       time forces 0/1): the persistent dataflow launch when every tangent
+ *       GEMM layer has at least one tile per SM, else layer by layer;
+ *    0  layer-by-layer launches (two streams, CUDA graph);
+ *    1  the persistent dataflow launch whenever the shape allows it
+ *       (batch <= 112, output width <= 16, no softmax output).
+ * Both schedules compute the same quantities (equal to rounding). */
+gbopt_status gbopt_net_set_schedule(gbopt_net* net, int schedule);
+
+/* Diagnostics: one eager dataflow evaluation of `batch` points (device
+ * pointers) with a per-item trace.  Writes up to `cap` doubles to `out`,
+ * 12 per item in claim order: {kind (0 fwd, 1 adj, 2 tangent GEMM, 3 SYRK),
+ * job, point, tm, tn, kb0, kb1, SM id, t_claimed, t_ready, t_begin, t_end}
+ * (microseconds from the first claim); *n_items = number of items.  `out`
+ * may be NULL to query the count.  GBOPT_ERR_STRUCTURE if the dataflow
+ * schedule does not apply to this handle and batch. */
+gbopt_status gbopt_net_dataflow_trace(const gbopt_net* net, size_t batch,
+                                      const double* dX, const double* dLambda,
+                                      double* out, size_t cap, size_t* n_items);
+
+/* 1 if the most recent oracle call used the dataflow launch, 0 if it ran
+ * layer by layer, -1 if the handle is not bound to a device. */
+int gbopt_net_last_schedule(const gbopt_net* net);
+
 /* Number of kernels the most recent oracle call on this handle launched
  * (graph replays count their kernel nodes). */
 int64_t gbopt_net_last_launch_count(const gbopt_net* net);

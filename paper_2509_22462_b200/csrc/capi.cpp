@@ -247,6 +247,29 @@ gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled) {
   return guarded([&] { net->net->use_graphs = enabled != 0; });
 }
 
+gbopt_status gbopt_net_set_schedule(gbopt_net* net, int schedule) {
+  if (net == nullptr) return fail_argument("gbopt_net_set_schedule: net must be non-null");
+  if (schedule < -1 || schedule > 1) return fail_argument("gbopt_net_set_schedule: schedule must be -1, 0 or 1");
+  return guarded([&] { net->net->schedule = schedule; });
+}
+
+gbopt_status gbopt_net_dataflow_trace(const gbopt_net* net, size_t batch, const double* dX, const double* dLambda,
+                                      double* out, size_t cap, size_t* n_items) {
+  if (net == nullptr || dX == nullptr || dLambda == nullptr || n_items == nullptr)
+    return fail_argument("gbopt_net_dataflow_trace: null argument");
+  if (batch == 0) return fail_argument("gbopt_net_dataflow_trace: batch must be positive");
+  return guarded([&] {
+    const std::vector<double> t = net->net->device().dataflow_trace(static_cast<int>(batch), dX, dLambda);
+    *n_items = t.size() / 12;
+    if (out != nullptr) std::copy(t.begin(), t.begin() + static_cast<std::ptrdiff_t>(std::min(t.size(), cap)), out);
+  });
+}
+
+int gbopt_net_last_schedule(const gbopt_net* net) {
+  if (net == nullptr || net->net->device_if_bound() == nullptr) return -1;
+  return net->net->device_if_bound()->last_dataflow() ? 1 : 0;
+}
+
 int64_t gbopt_net_last_launch_count(const gbopt_net* net) {
   if (net == nullptr || net->net->device_if_bound() == nullptr) return 0;
   return net->net->device_if_bound()->last_launches();

@@ -1,0 +1,383 @@
+// Persistent dataflow kernel: one launch evaluates the forward chain, the
+// adjoint chain, the tangent GEMM chain and the Hessian SYRKs of a small
+// batch (reference src/nn.cpp:113-292: forward, lagrangian_gradient's
+// adjoint, and lagrangian_hessian's tangents + curvature).
+//
+// Why: launched layer by layer, every tangent GEMM ends in a partial wave
+// (c2: 280 tiles on 148 SMs; c5: 896 tiles = 6.05 waves) and every layer
+// boundary is a grid-wide barrier.  But the rows of T_l are independent
+// tangent directions: row block tm of T_{l+1} needs only row block tm of
+// T_l (and sigma'_l), so the layer barrier is artificial.  Here every unit
+// of work is an "item" -- one 112 x 128 NT tile over a k-range -- and items
+// wait only on the counters of the items they really depend on:
+//
+//   FWD  z_l = W_l y_{l-1} + b_l (+ sigma, sigma', sigma''; the top layer also
+//        seeds gz = lambda .* sigma', d = lambda .* sigma'')   A = Y_{l-1}, B = W_l
+//   ADJ  ybar_{l-1} = W_l^T gz_l, gz_{l-1}, d_{l-1}              A = GZ_l,   B = W_l^T
+//   GEMM T_{l+1}[tm] = T_l[tm] diag(sigma'_l) W_{l+1}^T          A = T_l,    B = W_{l+1}
+//   SYRK H_q += T_l[tm] diag(d_l) T_l[tn]^T over k-piece q       A = B = T_l
+//
+// The host orders the item list by a list-scheduling simulation (priority =
+// longest path to the end), so the list is topological; CTAs claim items in
+// list order with one atomicAdd.  A CTA only waits on items claimed before
+// its own, by CTAs that are already running, so the kernel cannot deadlock
+// whatever the residency.  The producer warp claims the next item when it
+// has issued the last TMA load of the current one, waits for that item's
+// counters (ld.acquire.gpu), and streams its k-blocks while the consumers
+// are still finishing the current tile: tile prologue / epilogue overlap.
+//
+// Determinism: every item has a fixed k-range and a fixed output; SYRK
+// pieces q accumulate into H slot q in layer order (the slot counter orders
+// them), and the slots are summed in a fixed order by the symmetrise pass.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace gbb {
+namespace dev {
+
+enum DfKind : int { kDfFwd = 0, kDfAdj = 1, kDfGemm = 2, kDfSyrk = 3 };
+constexpr int kDfMaxWait = 5;
+
+struct alignas(16) DfJob {
+  int ta, tb;             // A / B operand: indices into DfParams::maps
+                          // (A rows: points for FWD/ADJ, tangent rows else)
+  const double* scale;    // per-k scale on B (GEMM: sigma'_l, SYRK: d_l), nullable
+  int64_t s_stride;
+  int64_t a_point_rows, b_point_rows;
+  int kind, act;
+  int a_bytes;  // bytes of one A box (FWD / ADJ: a box of round_up(points, 8) rows)
+  int m_valid;  // FWD/ADJ: points; GEMM: n_pad; SYRK: n
+  int n_valid;  // valid output columns
+  // GEMM: T_{l+1}; SYRK: H slot 0 (slots slot_stride apart)
+  double* c;
+  int64_t c_point_stride, ldc, slot_stride;
+  // FWD: bias, z, y, s1, s2 (pitch ld); top layer: gz/d seeds from lambda
+  const double* bias;
+  double *z, *y, *s1, *s2;
+  int64_t ld;
+  const double* lam;
+  int64_t ld_lam;
+  double *gz_seed, *d_seed;
+  // ADJ: ybar, gz, d of layer l-1 and its sigma', sigma'' (pitch ld)
+  double *ybar, *gz, *d;
+  const double *s1i, *s2i;
+};
+
+struct DfItem {
+  int job, point, tm, tn, kb0, kb1, slot, sig, nwait, pad;
+  int widx[kDfMaxWait], wtgt[kDfMaxWait];
+};
+
+// TMA descriptors travel in the kernel parameters (param space, like the
+// __grid_constant__ maps of nt_mma_kernel): 192 x 128 B = 24 KB of the 32 KB
+// parameter limit.
+constexpr int kDfMaxMaps = 192;
+
+struct DfParams {
+  CUtensorMap maps[kDfMaxMaps];
+  const DfItem* items;
+  int n_items;
+  const DfJob* jobs;
+  int* counters;  // zeroed before the launch; counters[0] is the claim counter
+  // optional per-item trace [n_items][4] (globaltimer ns): claimed, dependencies
+  // met, consumers start, epilogue done; and trace_sm[n_items] = SM id
+  unsigned long long* trace;
+  int* trace_sm;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int sm_id() {
+  int r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// The consumer k-loop over [kb0, kb1).  Full tiles (tangent GEMM, SYRK): the
+// 2 x 4 warp grid of nt_mma_kernel, 7 x 4 DMMA blocks per warp.  Point-row
+// tiles (FWD / ADJ, M = points <= 56): every warp takes 16 of the 128
+// columns and the MI live 8-row blocks, so no DMMA is issued for empty rows
+// (a predicated-off DMMA still occupies the tensor pipe).  The per-k scale
+// is produced inside the launch: L2 loads (ld.cg), one k-block ahead.
+// Scale vectors are single-assignment within a launch and only read after
+// their producer's counter: the non-coherent path cannot hold a stale copy.
+__device__ __forceinline__ double ld_scale(const double* p) {
+  return __ldg(p);
+}
+
+template <int MI, int NJ>
+__device__ __forceinline__ void df_mainloop(double (&acc)[kMI][kNJ][2], const char* smem, uint64_t* full,
+                                            uint64_t* empty, uint32_t& gk, int kb0, int kb1, const double* sp,
+                                            int ra, int rb, int t, int lane) {
+  double sc_next[4] = {1.0, 1.0, 1.0, 1.0};
+  if (sp && kb0 < kb1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sc_next[q] = ld_scale(sp + kb0 * kBK + 4 * q + t);
+  }
+  for (int kb = kb0; kb < kb1; ++kb, ++gk) {
+    const int s = static_cast<int>(gk % kStages);
+    double sc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sc[q] = sc_next[q];
+    if (sp && kb + 1 < kb1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sc_next[q] = ld_scale(sp + (kb + 1) * kBK + 4 * q + t);
+    }
+    mbar_wait(&full[s], (gk / kStages) & 1);
+    const char* sa = smem + s * kStageBytes;
+    const char* sb = sa + kABytes;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * q + t;
+      double a[MI], b[NJ];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc[q];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj) dmma884(acc[mi][nj], a[mi], b[nj]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__ DfParams P) {
+  extern __shared__ unsigned char smem_raw[];
+  char* smem = reinterpret_cast<char*>(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* qfull = empty + kStages;  // item hand-off, 2 slots
+  uint64_t* qempty = qfull + 2;
+  int* qitem = reinterpret_cast<int*>(qempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ===== producer: claim, wait for dependencies, stream k-blocks =====
+    // (the next item is claimed right after the current one's last load:
+    // claiming earlier measured slower -- c3 358 vs 353 ms)
+    if (lane == 0) {
+      uint32_t gk = 0;
+      for (int i = 0;; ++i) {
+        const int slot = i & 1;
+        if (i >= 2) mbar_wait(&qempty[slot], ((i >> 1) - 1) & 1);
+        const int idx = atomicAdd(P.counters, 1);
+        if (idx >= P.n_items) {
+          qitem[slot] = -1;
+          mbar_arrive(&qfull[slot]);
+          break;
+        }
+        const DfItem& it = P.items[idx];
+        if (P.trace) {
+          P.trace[4 * idx] = global_ns();
+          P.trace_sm[idx] = sm_id();
+        }
+        for (int w = 0; w < it.nwait; ++w) {
+          const int* cnt = P.counters + it.widx[w];
+          const int tgt = it.wtgt[w];
+          if (ld_acquire(cnt) < tgt) {
+            int ns = 32;
+            while (ld_acquire(cnt) < tgt) {
+              __nanosleep(ns);
+              ns = ns < 256 ? ns * 2 : 256;
+            }
+          }
+        }
+        fence_proxy_async_global();  // generic-proxy results -> TMA reads below
+        if (P.trace) P.trace[4 * idx + 1] = global_ns();
+        qitem[slot] = idx;
+        mbar_arrive(&qfull[slot]);
+        const DfJob& J = P.jobs[it.job];
+        const int a_row0 = static_cast<int>(J.a_point_rows * it.point) + it.tm * kBM;
+        const int b_row0 = static_cast<int>(J.b_point_rows * it.point) + it.tn * kBN;
+        for (int kb = it.kb0; kb < it.kb1; ++kb, ++gk) {
+          const int s = static_cast<int>(gk % kStages);
+          if (gk >= kStages) mbar_wait(&empty[s], ((gk / kStages) - 1) & 1);
+          char* sa = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], J.a_bytes + kBBytes);
+          tma_load_2d(sa, &P.maps[J.ta], &full[s], kb * kBK, a_row0);
+          tma_load_2d(sa + kABytes, &P.maps[J.tb], &full[s], kb * kBK, b_row0);
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  const int ra = wm * kWarpM + row_perm(g);
+  const int rb = wn * kWarpN + row_perm(g);
+  const int pg = row_perm(g), pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
+  uint32_t gk = 0;
+  for (int i = 0;; ++i) {
+    const int slot = i & 1;
+    mbar_wait(&qfull[slot], (i >> 1) & 1);
+    const int idx = qitem[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qempty[slot]);
+    if (idx < 0) break;
+    if (P.trace && threadIdx.x == 0) P.trace[4 * idx + 2] = global_ns();
+    const DfItem& it = P.items[idx];
+    const DfJob& J = P.jobs[it.job];
+    const int kind = J.kind;
+    // FWD / ADJ tiles hold only m_valid (= points) live rows: skip the
+    // DMMA blocks past them (uniform per warp)
+    const int m_live = kind <= kDfAdj ? J.m_valid : kBM;
+    const double* sp = J.scale ? J.scale + J.s_stride * it.point : nullptr;
+
+    double acc[kMI][kNJ][2];
+#pragma unroll
+    for (int a = 0; a < kMI; ++a)
+#pragma unroll
+      for (int b = 0; b < kNJ; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    // point-row tiles (FWD / ADJ) with few points use the column-split warp layout
+    const int small = (kind <= kDfAdj && m_live <= 56) ? (m_live <= 8 ? 1 : m_live <= 16 ? 2 : m_live <= 32 ? 4 : 7) : 0;
+    const int row0 = small ? 0 : wm * kWarpM;
+    const int col0 = small ? warp * 16 : wn * kWarpN;
+    const int mi_n = small ? small : kMI;
+    const int nj_n = small ? 2 : kNJ;
+    const int ra_s = row_perm(g), rb_s = warp * 16 + row_perm(g);
+    if (small == 0)
+      df_mainloop<kMI, kNJ>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra, rb, t, lane);
+    else if (small == 1)
+      df_mainloop<1, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
+    else if (small == 2)
+      df_mainloop<2, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
+    else if (small == 4)
+      df_mainloop<4, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
+    else
+      df_mainloop<7, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
+
+    // ---- epilogue: thread holds C[row0+8mi+pg][col0+8nj+pc0 / pc1] ----
+    // GEMM: store T; SYRK: accumulate into H slot; FWD / ADJ: raw tile into
+    // z / ybar, then one elementwise pass (activation or gz / d) over it.
+    double* raw = kind == kDfGemm ? J.c + J.c_point_stride * it.point
+                : kind == kDfSyrk ? J.c + J.slot_stride * it.slot + J.c_point_stride * it.point
+                : kind == kDfFwd  ? J.z : J.ybar;
+    const int64_t ldr = kind >= kDfGemm ? J.ldc : J.ld;
+    if (kind == kDfSyrk) {
+      // all loads of the H slot first (the stores below could alias them, so
+      // the compiler would otherwise serialise load -> store per element)
+#pragma unroll
+      for (int mi = 0; mi < kMI; ++mi) {
+        const int r = it.tm * kBM + row0 + 8 * mi + pg;
+        if (r >= J.m_valid) continue;
+#pragma unroll
+        for (int nj = 0; nj < kNJ; ++nj) {
+          const int cb = it.tn * kBN + col0 + 8 * nj;
+          const double* src = raw + static_cast<int64_t>(r) * ldr + cb;
+          if (cb + pc0 < J.n_valid) acc[mi][nj][0] += __ldcg(src + pc0);
+          if (cb + pc1 < J.n_valid) acc[mi][nj][1] += __ldcg(src + pc1);
+        }
+      }
+    }
+#pragma unroll
+    for (int mi = 0; mi < kMI; ++mi) {
+      const int r = it.tm * kBM + row0 + 8 * mi + pg;
+      if (mi >= mi_n || r >= J.m_valid) continue;
+#pragma unroll
+      for (int nj = 0; nj < kNJ; ++nj) {
+        if (nj >= nj_n) continue;
+        const int cb = it.tn * kBN + col0 + 8 * nj;
+        double* dst = raw + static_cast<int64_t>(r) * ldr + cb;
+        if (cb + pc0 < J.n_valid) dst[pc0] = acc[mi][nj][0];
+        if (cb + pc1 < J.n_valid) dst[pc1] = acc[mi][nj][1];
+      }
+    }
+    if (kind <= kDfAdj) {
+      consumer_bar();  // the raw tile is complete (CTA-scope ordering of the stores)
+      const int cols = min(kBN, J.n_valid - it.tn * kBN);
+      for (int e = threadIdx.x; e < J.m_valid * cols; e += kConsumerWarps * 32) {
+        const int r = e / cols, c = it.tn * kBN + e % cols;
+        const int64_t o = static_cast<int64_t>(r) * J.ld + c;
+        const double v = J.kind == kDfFwd ? J.z[o] : J.ybar[o];
+        if (kind == kDfFwd) {  // r = point, c = unit of layer l
+          const double zz = v + __ldg(J.bias + c);
+          double yy, d1, d2;
+          act_eval(J.act, zz, yy, d1, d2);
+          J.z[o] = zz;
+          J.y[o] = yy;
+          J.s1[o] = d1;
+          J.s2[o] = d2;
+          if (J.lam) {
+            const double lv = __ldg(J.lam + static_cast<int64_t>(r) * J.ld_lam + c);
+            J.gz_seed[o] = lv * d1;
+            J.d_seed[o] = lv * d2;
+          }
+        } else {  // ADJ: r = point, c = unit of layer l-1
+          J.gz[o] = v * __ldcg(J.s1i + o);
+          J.d[o] = v * __ldcg(J.s2i + o);
+        }
+      }
+    }
+    // ---- publish: stores visible (generic + async proxy) before the count ----
+    if (it.sig > 0) {
+#ifdef DF_PROXY_FENCE_ALL
+      fence_proxy_async_global();
+#endif
+      consumer_bar();  // CTA-scope: every consumer's stores precede thread 0's release
+      if (threadIdx.x == 0) {
+        // cumulative gpu-scope fence + generic -> async proxy fence: the
+        // tile is visible to later TMA reads of the items that wait on it
+        __threadfence();
+        fence_proxy_async_global();
+        red_release_add(P.counters + it.sig, 1);
+      }
+    }
+    if (P.trace && threadIdx.x == 0) P.trace[4 * idx + 3] = global_ns();
+  }
+}
+
+// Sum of the SYRK slots' lower triangles, mirrored: H_out[b][r][c] =
+// sum_q H_q[b][max(r,c)][min(r,c)] in slot order (exactly symmetric).
+__global__ void symmetrize_slots_kernel(const double* __restrict__ hws, int slots, int64_t slot_stride,
+                                        int64_t h_point_stride, int64_t ldh, int n, int nb,
+                                        double* __restrict__ out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  if (e >= nn * nb) return;
+  const int b = static_cast<int>(e / nn);
+  const int r = static_cast<int>((e % nn) / n), c = static_cast<int>(e % n);
+  const int hi = r > c ? r : c, lo = r > c ? c : r;
+  const int64_t o = h_point_stride * b + static_cast<int64_t>(hi) * ldh + lo;
+  double v = 0.0;
+  for (int q = 0; q < slots; ++q) v += hws[slot_stride * q + o];
+  out[e] = v;
+}
+
+}  // namespace dev
+}  // namespace gbb

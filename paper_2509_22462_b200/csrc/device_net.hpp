@@ -15,6 +15,8 @@
 namespace gbb {
 namespace dev {
 struct NtParams;
+struct DfItem;
+struct DfJob;
 }
 
 void cuda_check(cudaError_t e, const char* what);
@@ -74,7 +76,7 @@ struct Workspace {
 enum KernelTag : int {
   kTagFwd = 0, kTagSoftmax, kTagAdjSeed, kTagAdjCols, kTagAdjReduce, kTagGemm, kTagSyrk, kTagSyrkReduce,
   kTagSkinny, kTagSkinnyReduce, kTagJacOut, kTagSmallSyrk, kTagSymmetrize, kTagFwdGemm, kTagAdjGemm, kTagRowEpi,
-  kTagStep,
+  kTagStep, kTagDataflow,
   kTagCount
 };
 const char* kernel_tag_name(int tag);
@@ -95,6 +97,22 @@ struct Outputs {
   double* g = nullptr;  // [nb][n]
 };
 
+// One persistent dataflow launch (dataflow.cuh) for a batch size: the
+// ordered item list, the jobs, their TMA descriptors and the counters, all
+// in device memory.  Built on first use, dropped with the workspace.
+struct DfPlan {
+  int nb = 0;
+  int n_items = 0, n_counters = 0, slots = 0;
+  int64_t slot_stride = 0;  // doubles between H slots
+  dev::DfItem* items = nullptr;
+  dev::DfJob* jobs = nullptr;
+  std::vector<CUtensorMap> maps;  // TMA descriptors (kernel parameters)
+  int* counters = nullptr;
+  double* hslots = nullptr;  // [slots][nb][n_pad][n_pad]
+  double flops = 0, bytes = 0;  // algorithmic work of the launch
+  double sim_ms = 0;            // list-scheduling estimate of the launch
+};
+
 class DeviceNet {
  public:
   DeviceNet(const Net& net, int ordinal);
@@ -104,6 +122,7 @@ class DeviceNet {
 
   int ordinal() const { return ordinal_; }
   int64_t last_launches() const { return last_launches_; }
+  bool last_dataflow() const { return last_dataflow_; }
 
   // Host buffers in/out (synchronous).  Any output may be null.
   void evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess, double* grad);
@@ -118,7 +137,7 @@ class DeviceNet {
                        cudaStream_t user);
 
  private:
-  using GraphKey = std::tuple<int, double*, double*, double*, double*>;
+  using GraphKey = std::tuple<int, double*, double*, double*, double*, bool>;
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;
@@ -130,6 +149,8 @@ class DeviceNet {
   double* ws_alloc(size_t n_doubles);
   int syrk_split(int points, int k_blocks) const;
   void ensure_transposed();
+  void prepare(int nb, const Outputs& o);
+  void launch_skinny(cudaStream_t st, int nb, const double* t, int64_t ldt, int64_t t_point_rows, int l);
   void batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const DevLayer& d, bool transposed,
                   const void* epi, double* store);
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
@@ -139,6 +160,29 @@ class DeviceNet {
   bool streamk_ = true;   // layer steps: GEMM_{l+1} + SYRKs in one launch
   bool hybrid_ = false;   // two-stream schedule with hybrid DP/stream-K launches
   void enqueue(cudaStream_t st, int nb, const Outputs& o);
+  // Persistent dataflow path (y, J, H at small batch): oracle.cu.
+  bool dataflow_ok(int nb, const Outputs& o) const;
+  bool dataflow_possible(int nb, const Outputs& o) const;
+  using ChoiceKey = std::tuple<int, bool, bool, bool>;
+  static ChoiceKey choice_key(int nb, const Outputs& o) { return ChoiceKey{nb, o.y != nullptr, o.j != nullptr, o.h != nullptr}; }
+  std::map<ChoiceKey, bool> df_choice_;                     // auto schedule: dataflow measured faster
+  std::map<ChoiceKey, std::pair<float, float>> df_tuned_ms_;  // (layered, dataflow) ms of the autotune
+  int df_force_ = -1;  // autotune override of the schedule mode
+  void autotune(cudaStream_t st, int nb, const Outputs& o);
+  void dispatch(cudaStream_t st, int nb, const Outputs& o);
+  DfPlan& dataflow_plan(int nb);
+  void enqueue_dataflow(cudaStream_t st, int nb, const Outputs& o);
+  void free_plans();
+  unsigned long long* df_trace_ = nullptr;
+  int* df_trace_sm_ = nullptr;
+
+ public:
+  std::vector<double> dataflow_trace(int nb, const double* dx, const double* dlam);
+
+ private:
+  int dataflow_mode_ = -1;  // GBOPT_DATAFLOW: -1 auto, 0 off, 1 whenever the shape allows
+  std::map<int, DfPlan> df_plans_;
+  int df_group_ = 4;  // row blocks per raster group of the tangent GEMM items (GBOPT_DF_GROUP)
   void prof_begin(cudaStream_t st, int tag, double flops, double bytes);
   void after_launch(cudaStream_t st);
   struct ProfRec {
@@ -172,6 +216,7 @@ class DeviceNet {
   std::vector<void*> ws_allocs_;
   std::map<GraphKey, GraphEntry> graphs_;
   int64_t launches_ = 0, last_launches_ = 0;
+  bool last_dataflow_ = false;
 };
 
 }  // namespace gbb

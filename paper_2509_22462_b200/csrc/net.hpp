@@ -48,6 +48,7 @@ class Net {
   DeviceNet* device_if_bound() const { return dev_.get(); }
   int bound_ordinal() const;
   bool use_graphs = true;
+  int schedule = -1;  // oracle schedule: -1 auto, 0 layer-by-layer launches, 1 dataflow where the shape allows
 
  private:
   std::vector<HostLayer> layers_;

@@ -25,10 +25,12 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <queue>
 #include <string>
 #include <tuple>
 #include <vector>
 
+#include "dataflow.cuh"
 #include "device_net.hpp"
 #include "kernels.cuh"
 #include "net.hpp"
@@ -105,6 +107,9 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   sm_count_ = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::nt_mma_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
+  CK(cudaFuncSetAttribute(dev::df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
+  if (const char* e = std::getenv("GBOPT_DATAFLOW")) dataflow_mode_ = e[0] == '0' ? 0 : 1;
+  if (const char* e = std::getenv("GBOPT_DF_GROUP")) df_group_ = std::max(1, std::atoi(e));
   // (A maximal shared-memory carveout, tried so GEMV CTAs could co-reside with
   // nt_mma, cost 2% on c2 -- 173.4 vs 177.3 evals/s -- and is not set.)
   // Persistent stream-K layer steps (experimental, GBOPT_STREAMK=1): balanced
@@ -198,6 +203,7 @@ DeviceNet::~DeviceNet() {
 }
 
 void DeviceNet::free_workspace() {
+  free_plans();
   for (void* p : ws_allocs_) cudaFree(p);
   ws_allocs_.clear();
   ws_cap_ = 0;
@@ -268,11 +274,12 @@ void DeviceNet::ensure_workspace(int batch) {
   // tangents (only needed with >= 2 layers)
   // T_l (l >= 1) lives in ring buffer t_buf(l) = (l - 1) % R.  With R >= the
   // number of tangent layers the GEMM chain never waits for a SYRK to free
-  // a buffer; R is capped by a memory budget (8 GB) and is at least 2.
+  // a buffer (and the dataflow path applies); R is capped by a memory
+  // budget (32 GB of the 180 GB) and is at least 2.
   if (L_ >= 2) {
     const size_t tbytes = sizeof(double) * static_cast<size_t>(cap) * n_pad_ * ldt_;
     const int want = std::max(2, static_cast<int>(L_) - 1);
-    const int fit = static_cast<int>(std::max<size_t>(2, (size_t(8) << 30) / std::max<size_t>(tbytes, 1)));
+    const int fit = static_cast<int>(std::max<size_t>(2, (size_t(32) << 30) / std::max<size_t>(tbytes, 1)));
     const int ring = std::min(want, fit);
     w.t.assign(static_cast<size_t>(ring), nullptr);
     for (auto& b : w.t) b = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
@@ -476,17 +483,17 @@ void DeviceNet::after_launch(cudaStream_t st) {
 void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out, bool timeline) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
-  if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
+  Outputs o;
+  o.y = w.y_out;
+  o.j = w.j_out;
+  o.h = w.h_out;
+  prepare(nb, o);
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
                        cudaMemcpyDeviceToDevice, stream_));
   CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, dlam, sizeof(double) * m_, sizeof(double) * m_, nb,
                        cudaMemcpyDeviceToDevice, stream_));
-  Outputs o;
-  o.y = w.y_out;
-  o.j = w.j_out;
-  o.h = w.h_out;
   profiling_ = true;
   prof_timeline_ = timeline;
   prof_.clear();
@@ -516,6 +523,40 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
   prof_.clear();
 }
 
+// Final layer with m <= 16 outputs: U = T_l diag(sigma'_l) W_{l+1}^T into
+// w.u ([nb][n_pad][16]) by the skinny split-K kernel + fixed-order reduce.
+void DeviceNet::launch_skinny(cudaStream_t st, int nb, const double* t, int64_t ldt, int64_t t_point_rows, int l) {
+  Workspace& w = ws_;
+  const DevLayer& df = layers_[static_cast<size_t>(l + 1)];
+  dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
+  prof_begin(st, kTagSkinny, 2.0 * n_ * m_ * df.cols * nb, 0);
+  // template on the output count: no work on empty output slots
+  if (m_ <= 1)
+    dev::skinny_nt_kernel<1><<<grid, 256, 0, st>>>(t, ldt, t_point_rows, static_cast<int>(n_), w.s1[l], w.ld[l], df.w,
+                                                   df.ldw, static_cast<int>(m_), static_cast<int>(df.cols), w.sk_part);
+  else if (m_ <= 4)
+    dev::skinny_nt_kernel<4><<<grid, 256, 0, st>>>(t, ldt, t_point_rows, static_cast<int>(n_), w.s1[l], w.ld[l], df.w,
+                                                   df.ldw, static_cast<int>(m_), static_cast<int>(df.cols), w.sk_part);
+  else
+    dev::skinny_nt_kernel<16><<<grid, 256, 0, st>>>(t, ldt, t_point_rows, static_cast<int>(n_), w.s1[l], w.ld[l],
+                                                    df.w, df.ldw, static_cast<int>(m_), static_cast<int>(df.cols),
+                                                    w.sk_part);
+  after_launch(st);
+  const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
+  prof_begin(st, kTagSkinnyReduce, 0, 0);
+  dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.sk_part, w.sk_chunks, nb, static_cast<int>(n_pad_),
+                                                                static_cast<int>(m_), w.u);
+  after_launch(st);
+}
+
+// Everything an evaluation needs that cannot be done inside a stream
+// capture (allocations, synchronous uploads): W^T copies, dataflow plans.
+void DeviceNet::prepare(int nb, const Outputs& o) {
+  const bool df = dataflow_ok(nb, o);
+  if (df || static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
+  if (df) dataflow_plan(nb);
+}
+
 // The whole evaluation for `nb` points whose x / lambda already sit in the
 // workspace.  Outputs go to the given device pointers (nullable).
 //
@@ -526,6 +567,10 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
 // GEMM_{l+1} overwrites T_{l-1}'s buffer, so it waits for SYRK_{l-1}.
 // (Profiling runs serialise both onto one stream.)
 void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
+  if (dataflow_ok(nb, o)) {
+    enqueue_dataflow(st, nb, o);
+    return;
+  }
   Workspace& w = ws_;
   // profiling serialises onto one stream, except the timeline mode
   const bool two = concurrent_ && (!profiling_ || prof_timeline_);
@@ -992,27 +1037,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     u_point_rows = 0;
   } else if (skinny_final) {
     const int l = kfin_layer - 1;
-    dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
-    prof_begin(sa, kTagSkinny, 2.0 * n_ * m_ * df.cols * nb, 0);
-    // template on the output count: no work on empty output slots
-    if (m_ <= 1)
-      dev::skinny_nt_kernel<1><<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_),
-                                                     w.s1[l], w.ld[l], df.w, df.ldw, static_cast<int>(m_),
-                                                     static_cast<int>(df.cols), w.sk_part);
-    else if (m_ <= 4)
-      dev::skinny_nt_kernel<4><<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_),
-                                                     w.s1[l], w.ld[l], df.w, df.ldw, static_cast<int>(m_),
-                                                     static_cast<int>(df.cols), w.sk_part);
-    else
-      dev::skinny_nt_kernel<16><<<grid, 256, 0, sa>>>(t_ptr(l), t_ld(l), t_point_rows(l), static_cast<int>(n_),
-                                                      w.s1[l], w.ld[l], df.w, df.ldw, static_cast<int>(m_),
-                                                      static_cast<int>(df.cols), w.sk_part);
-    after_launch(sa);
-    const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
-    prof_begin(sa, kTagSkinnyReduce, 0, 0);
-    dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, sa>>>(w.sk_part, w.sk_chunks, nb,
-                                                                  static_cast<int>(n_pad_), static_cast<int>(m_), w.u);
-    after_launch(sa);
+    launch_skinny(sa, nb, t_ptr(l), t_ld(l), t_point_rows(l), l);
     u = w.u;
     ldu = dev::kSkMB;
     u_point_rows = n_pad_;
@@ -1062,7 +1087,48 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
 }
 
 void DeviceNet::run(cudaStream_t st, int nb, const Outputs& o) {
-  const GraphKey key{nb, o.y, o.j, o.h, o.g};
+  const int mode = net_.schedule >= 0 ? net_.schedule : dataflow_mode_;
+  if (mode < 0 && dataflow_possible(nb, o) && df_choice_.count(choice_key(nb, o)) == 0) autotune(st, nb, o);
+  dispatch(st, nb, o);
+}
+
+// Auto schedule: the first evaluation of a shape runs both schedules twice
+// (warm, then timed with events on `st`) and keeps the faster.  Both compute
+// the same quantities; the measured winner depends on how the tangent GEMM
+// tiles quantise onto the SMs.
+void DeviceNet::autotune(cudaStream_t st, int nb, const Outputs& o) {
+  ensure_transposed();
+  dataflow_plan(nb);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float ms[2] = {0.f, 0.f};
+  try {
+    for (int f = 0; f < 2; ++f) {
+      df_force_ = f;
+      dispatch(st, nb, o);
+      CK(cudaEventRecord(e0, st));
+      dispatch(st, nb, o);
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms[f], e0, e1));
+    }
+  } catch (...) {
+    df_force_ = -1;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  df_force_ = -1;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  df_choice_[choice_key(nb, o)] = ms[1] < ms[0];
+  df_tuned_ms_[choice_key(nb, o)] = {ms[0], ms[1]};
+}
+
+void DeviceNet::dispatch(cudaStream_t st, int nb, const Outputs& o) {
+  last_dataflow_ = dataflow_ok(nb, o);
+  const GraphKey key{nb, o.y, o.j, o.h, o.g, last_dataflow_};
   if (!net_.use_graphs) {
     launches_ = 0;
     enqueue(st, nb, o);
@@ -1100,18 +1166,18 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
                               double* grad) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
-  if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
-  CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
-                       cudaMemcpyHostToDevice, stream_));
-  if (lam)
-    CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam, sizeof(double) * m_, sizeof(double) * m_, nb,
-                         cudaMemcpyHostToDevice, stream_));
   Outputs o;
   o.y = y ? w.y_out : nullptr;
   o.j = jac ? w.j_out : nullptr;
   o.h = hess ? w.h_out : nullptr;
   o.g = grad ? w.g_out : nullptr;
+  prepare(nb, o);
+  CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
+                       cudaMemcpyHostToDevice, stream_));
+  if (lam)
+    CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam, sizeof(double) * m_, sizeof(double) * m_, nb,
+                         cudaMemcpyHostToDevice, stream_));
   run(stream_, nb, o);
   if (y) CK(cudaMemcpyAsync(y, w.y_out, sizeof(double) * nb * m_, cudaMemcpyDeviceToHost, stream_));
   if (jac) CK(cudaMemcpyAsync(jac, w.j_out, sizeof(double) * nb * m_ * n_, cudaMemcpyDeviceToHost, stream_));
@@ -1125,8 +1191,14 @@ void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, do
                                 cudaStream_t user) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
-  if (static_cast<int64_t>(nb) * std::max<int64_t>(m_, 1) >= kBatchGemm) ensure_transposed();
   Workspace& w = ws_;
+  {
+    Outputs po;
+    po.y = dy;
+    po.j = dj;
+    po.h = dh;
+    prepare(nb, po);
+  }
   CK(cudaEventRecord(ev_in_, user));
   CK(cudaStreamWaitEvent(stream_, ev_in_, 0));
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
@@ -1159,6 +1231,488 @@ void DeviceNet::copy_intermediate(const char* name, int layer, int nb, double* o
 }
 
 // ---------------------------------------------------------------------------
+// Persistent dataflow path (dataflow.cuh): plan construction and launch.
+// ---------------------------------------------------------------------------
+// Shapes the dataflow launch can run (independent of the schedule mode).
+bool DeviceNet::dataflow_possible(int nb, const Outputs& o) const {
+  if (streamk_ || hybrid_ || !concurrent_) return false;
+  if (o.h == nullptr || o.g != nullptr) return false;  // the full (y, J, H) oracle only
+  if (L_ < 2 || m_ > dev::kSkMB || layers_[static_cast<size_t>(L_ - 1)].act == kSoftmax) return false;
+  if (6 * L_ + 1 > dev::kDfMaxMaps) return false;  // TMA descriptors in the kernel parameters
+  if (nb < 1 || nb > kBM) return false;  // FWD / ADJ items hold all points in one M tile
+  if (L_ >= 3 && static_cast<int64_t>(ws_.t.size()) < L_ - 2) return false;  // one T buffer per tangent layer
+  return true;
+}
+
+bool DeviceNet::dataflow_ok(int nb, const Outputs& o) const {
+  int mode = net_.schedule >= 0 ? net_.schedule : dataflow_mode_;
+  if (df_force_ >= 0) mode = df_force_;
+  if (mode == 0 || !dataflow_possible(nb, o)) return false;
+  if (mode == 1) return true;
+  // auto: what the first evaluation of this shape measured (autotune in run())
+  const auto c = df_choice_.find(choice_key(nb, o));
+  return c != df_choice_.end() && c->second;
+}
+
+// One eager dataflow evaluation with the per-item trace on: rows of
+// {kind, job, point, tm, tn, kb0, kb1, sm, t_claim, t_ready, t_begin, t_end}
+// (times in us from the earliest claim), in claim order.
+std::vector<double> DeviceNet::dataflow_trace(int nb, const double* dx, const double* dlam) {
+  DeviceGuard g(ordinal_);
+  ensure_workspace(nb);
+  Workspace& w = ws_;
+  Outputs o;
+  o.y = w.y_out;
+  o.j = w.j_out;
+  o.h = w.h_out;
+  if (!dataflow_ok(nb, o)) throw StructuralError("dataflow_trace: the dataflow schedule does not apply");
+  prepare(nb, o);
+  DfPlan& P = df_plans_.at(nb);
+  CK(cudaDeviceSynchronize());
+  CK(cudaMalloc(&df_trace_, sizeof(unsigned long long) * 4 * P.n_items));
+  CK(cudaMalloc(&df_trace_sm_, sizeof(int) * P.n_items));
+  CK(cudaMemcpy2D(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
+                  cudaMemcpyDeviceToDevice));
+  CK(cudaMemcpy2D(w.lam, sizeof(double) * w.ld_lam, dlam, sizeof(double) * m_, sizeof(double) * m_, nb,
+                  cudaMemcpyDeviceToDevice));
+  std::vector<unsigned long long> tr(static_cast<size_t>(4) * P.n_items);
+  std::vector<int> sm(static_cast<size_t>(P.n_items));
+  std::vector<dev::DfItem> items(static_cast<size_t>(P.n_items));
+  std::vector<dev::DfJob> jobs;
+  try {
+    enqueue_dataflow(stream_, nb, o);
+    CK(cudaStreamSynchronize(stream_));
+    CK(cudaMemcpy(tr.data(), df_trace_, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sm.data(), df_trace_sm_, sizeof(int) * sm.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(items.data(), P.items, sizeof(dev::DfItem) * items.size(), cudaMemcpyDeviceToHost));
+    int nj = 0;
+    for (const auto& it : items) nj = std::max(nj, it.job + 1);
+    jobs.resize(static_cast<size_t>(nj));
+    CK(cudaMemcpy(jobs.data(), P.jobs, sizeof(dev::DfJob) * jobs.size(), cudaMemcpyDeviceToHost));
+  } catch (...) {
+    cudaFree(df_trace_);
+    cudaFree(df_trace_sm_);
+    df_trace_ = nullptr;
+    df_trace_sm_ = nullptr;
+    throw;
+  }
+  cudaFree(df_trace_);
+  cudaFree(df_trace_sm_);
+  df_trace_ = nullptr;
+  df_trace_sm_ = nullptr;
+  unsigned long long t0 = ~0ull;
+  for (int i = 0; i < P.n_items; ++i) t0 = std::min(t0, tr[static_cast<size_t>(4 * i)]);
+  std::vector<double> out;
+  out.reserve(static_cast<size_t>(12) * P.n_items);
+  for (int i = 0; i < P.n_items; ++i) {
+    const dev::DfItem& it = items[static_cast<size_t>(i)];
+    out.push_back(jobs[static_cast<size_t>(it.job)].kind);
+    out.push_back(it.job);
+    out.push_back(it.point);
+    out.push_back(it.tm);
+    out.push_back(it.tn);
+    out.push_back(it.kb0);
+    out.push_back(it.kb1);
+    out.push_back(sm[static_cast<size_t>(i)]);
+    for (int k = 0; k < 4; ++k) out.push_back(1e-3 * static_cast<double>(tr[static_cast<size_t>(4 * i + k)] - t0));
+  }
+  return out;
+}
+
+void DeviceNet::free_plans() {
+  for (auto& kv : df_plans_) {
+    DfPlan& p = kv.second;
+    cudaFree(p.items);
+    cudaFree(p.jobs);
+    cudaFree(p.counters);
+    cudaFree(p.hslots);
+  }
+  df_plans_.clear();
+}
+
+// The item list of one dataflow launch, ordered by a list-scheduling
+// simulation of the GPU (sm_count workers, priority = longest remaining
+// path), so the order is topological and claims the critical path first.
+DfPlan& DeviceNet::dataflow_plan(int nb) {
+  auto found = df_plans_.find(nb);
+  if (found != df_plans_.end()) return found->second;
+  Workspace& w = ws_;
+  const int L = static_cast<int>(L_);
+  const int tiles_m = static_cast<int>(n_pad_ / kBM);
+  auto rows = [&](int l) { return layers_[static_cast<size_t>(l)].rows; };
+  auto cols = [&](int l) { return layers_[static_cast<size_t>(l)].cols; };
+  auto kbs = [&](int64_t k) { return ceil_div(k, kBK); };
+  const int ring = static_cast<int>(w.t.size());
+  auto t_buf = [&](int l) -> double* { return w.t[static_cast<size_t>((l - 1) % ring)]; };
+  auto t_point_rows = [&](int l) -> int64_t { return l == 0 ? 0 : n_pad_; };
+
+  // ---- TMA descriptors (copied to device memory; jobs point at them) ----
+  std::vector<CUtensorMap> maps;
+  auto map_id = [&](const CUtensorMap& m) {
+    for (size_t i = 0; i < maps.size(); ++i)
+      if (std::memcmp(&maps[i], &m, sizeof(CUtensorMap)) == 0) return static_cast<int>(i);
+    if (maps.size() >= static_cast<size_t>(dev::kDfMaxMaps)) throw StructuralError("dataflow: too many TMA descriptors");
+    maps.push_back(m);
+    return static_cast<int>(maps.size()) - 1;
+  };
+  std::vector<dev::DfJob> jobs;
+  std::vector<std::pair<int, int>> job_maps;
+  auto add_job = [&](const dev::DfJob& j, int ma, int mb) {
+    jobs.push_back(j);
+    job_maps.emplace_back(ma, mb);
+    return static_cast<int>(jobs.size()) - 1;
+  };
+
+  // ---- counters ----
+  int nc = 1;  // [0] = claim counter
+  std::vector<int> fwd_cnt(static_cast<size_t>(L)), adj_cnt(static_cast<size_t>(L), 0), row_base(static_cast<size_t>(L), 0);
+  for (int l = 0; l < L; ++l) fwd_cnt[static_cast<size_t>(l)] = nc++;
+  for (int l = 1; l < L; ++l) adj_cnt[static_cast<size_t>(l)] = nc++;
+  for (int l = 1; l + 1 < L; ++l) {
+    row_base[static_cast<size_t>(l)] = nc;
+    nc += nb * tiles_m;
+  }
+  std::vector<int2> stiles;
+  for (int tm = 0; tm * kBM < n_; ++tm)
+    for (int tn = 0; tn * kBN < n_; ++tn)
+      if (static_cast<int64_t>(tn) * kBN <= static_cast<int64_t>(tm) * kBM + kBM - 1) stiles.push_back(make_int2(tm, tn));
+  const int n_st = static_cast<int>(stiles.size());
+  std::vector<int> syrk_layers, pieces;
+  int slots = 1;
+  for (int l = 0; l + 1 < L; ++l) {
+    if (layers_[static_cast<size_t>(l)].act == kLinear) continue;
+    syrk_layers.push_back(l);
+    const int p = std::max(1, std::min(8, static_cast<int>(std::lround(kbs(rows(l)) / 64.0))));
+    pieces.push_back(p);
+    slots = std::max(slots, p);
+  }
+  const int hcnt_base = nc;
+  nc += slots * nb * n_st;
+  auto hcnt = [&](int q, int p, int t) { return hcnt_base + (q * nb + p) * n_st + t; };
+
+  // ---- items (created in a topological order) ----
+  const double sm_rate = 35.0e12 / 148.0;                     // FP64 flop/s per SM (DMMA)
+  const double t_kb = 2.0 * kBM * kBN * kBK / sm_rate * 1e3;   // ms per full k-block
+  const double t_kb_mem = 16384.0 / 60.0e9 * 1e3;             // ms per streamed 16 KB B box
+  const double t_item = 2.0e-3;                                // ms per item (epilogue, hand-off)
+  struct Node {
+    dev::DfItem it;
+    double cost;
+  };
+  std::vector<Node> nodes;
+  auto add_item = [&](int job, int point, int tm, int tn, int kb0, int kb1, int slot, int sig,
+                      std::initializer_list<std::pair<int, int>> waits, double cost) {
+    Node nd{};
+    nd.it.job = job;
+    nd.it.point = point;
+    nd.it.tm = tm;
+    nd.it.tn = tn;
+    nd.it.kb0 = kb0;
+    nd.it.kb1 = kb1;
+    nd.it.slot = slot;
+    nd.it.sig = sig;
+    for (const auto& wt : waits) {
+      if (wt.second <= 0) continue;
+      bool dup = false;
+      for (int i = 0; i < nd.it.nwait; ++i) dup = dup || (nd.it.widx[i] == wt.first && nd.it.wtgt[i] >= wt.second);
+      if (dup) continue;
+      if (nd.it.nwait >= dev::kDfMaxWait) throw StructuralError("dataflow: too many dependencies");
+      nd.it.widx[nd.it.nwait] = wt.first;
+      nd.it.wtgt[nd.it.nwait] = wt.second;
+      ++nd.it.nwait;
+    }
+    nd.cost = cost;
+    nodes.push_back(nd);
+  };
+  // FWD / ADJ A operands (points x K): a box of round_up(nb, 8) rows, not 112
+  const int a_rows = static_cast<int>(std::min<int64_t>(kBM, round_up(nb, 8)));
+  const int a_bytes_small = a_rows * kBK * 8;
+  const int tm_x = map_id(make_tmap(w.x, n_, ws_cap_, w.ld_in, a_rows));
+  std::vector<int> nfwd(static_cast<size_t>(L)), nadj(static_cast<size_t>(L), 0);
+  const double gemv_mma = std::min(1.0, ceil_div(nb, 8) / 14.0) * t_kb;
+  double flops = 0, bytes = 0;
+  // forward chain (+ the adjoint seed in the top layer's epilogue)
+  for (int l = 0; l < L; ++l) {
+    const DevLayer& d = layers_[static_cast<size_t>(l)];
+    dev::DfJob j{};
+    j.kind = dev::kDfFwd;
+    j.act = d.act;
+    j.m_valid = nb;
+    j.n_valid = static_cast<int>(d.rows);
+    j.bias = d.b;
+    j.z = w.z[static_cast<size_t>(l)];
+    j.y = w.y[static_cast<size_t>(l)];
+    j.s1 = w.s1[static_cast<size_t>(l)];
+    j.s2 = w.s2[static_cast<size_t>(l)];
+    j.ld = w.ld[static_cast<size_t>(l)];
+    if (l == L - 1) {
+      j.lam = w.lam;
+      j.ld_lam = w.ld_lam;
+      j.gz_seed = w.gz[static_cast<size_t>(l)];
+      j.d_seed = w.d[static_cast<size_t>(l)];
+    }
+    j.a_bytes = a_bytes_small;
+    const int job = add_job(j, l == 0 ? tm_x : map_id(make_tmap(w.y[static_cast<size_t>(l - 1)], rows(l - 1), ws_cap_,
+                                                                  w.ld[static_cast<size_t>(l - 1)], a_rows)),
+                            map_id(d.tm_w));
+    nfwd[static_cast<size_t>(l)] = ceil_div(d.rows, kBN);
+    const int kb = kbs(d.cols);
+    for (int tn = 0; tn < nfwd[static_cast<size_t>(l)]; ++tn)
+      add_item(job, 0, 0, tn, 0, kb, 0, fwd_cnt[static_cast<size_t>(l)],
+               {{l > 0 ? fwd_cnt[static_cast<size_t>(l - 1)] : 0, l > 0 ? nfwd[static_cast<size_t>(l - 1)] : 0}},
+               kb * std::max(t_kb_mem, gemv_mma) + t_item);
+    flops += 2.0 * d.rows * d.cols * nb;
+    bytes += 8.0 * d.rows * d.cols;
+  }
+  // adjoint chain down to ybar_0 / d_0 (layer 0's input gradient is not needed)
+  for (int l = L - 1; l >= 1; --l) {
+    const DevLayer& d = layers_[static_cast<size_t>(l)];
+    dev::DfJob j{};
+    j.kind = dev::kDfAdj;
+    j.m_valid = nb;
+    j.n_valid = static_cast<int>(d.cols);
+    j.ybar = w.ybar[static_cast<size_t>(l - 1)];
+    j.gz = w.gz[static_cast<size_t>(l - 1)];
+    j.d = w.d[static_cast<size_t>(l - 1)];
+    j.s1i = w.s1[static_cast<size_t>(l - 1)];
+    j.s2i = w.s2[static_cast<size_t>(l - 1)];
+    j.ld = w.ld[static_cast<size_t>(l - 1)];
+    j.a_bytes = a_bytes_small;
+    const int job = add_job(j, map_id(make_tmap(w.gz[static_cast<size_t>(l)], rows(l), ws_cap_ * std::max<int64_t>(m_, 1),
+                                                w.ld[static_cast<size_t>(l)], a_rows)),
+                            map_id(d.tm_wt));
+    nadj[static_cast<size_t>(l)] = ceil_div(d.cols, kBN);
+    const int kb = kbs(d.rows);
+    const std::pair<int, int> dep = l == L - 1 ? std::make_pair(fwd_cnt[static_cast<size_t>(L - 1)], nfwd[static_cast<size_t>(L - 1)])
+                                               : std::make_pair(adj_cnt[static_cast<size_t>(l + 1)], nadj[static_cast<size_t>(l + 1)]);
+    for (int tn = 0; tn < nadj[static_cast<size_t>(l)]; ++tn)
+      add_item(job, 0, 0, tn, 0, kb, 0, adj_cnt[static_cast<size_t>(l)], {dep},
+               kb * std::max(t_kb_mem, gemv_mma) + t_item);
+    flops += 2.0 * d.rows * d.cols * nb;
+    bytes += 8.0 * d.rows * d.cols;
+  }
+  // tangent GEMMs T_{l+1} = T_l diag(sigma'_l) W_{l+1}^T, l + 1 <= L - 2, and
+  // the SYRK pieces of layer l once T_l exists
+  std::vector<int> ntiles_n(static_cast<size_t>(L), 0);
+  size_t si = 0;
+  for (int l = 0; l + 1 < L; ++l) {
+    if (l + 2 < L) {
+      const DevLayer& dn = layers_[static_cast<size_t>(l + 1)];
+      dev::DfJob j{};
+      j.kind = dev::kDfGemm;
+      j.a_bytes = dev::kABytes;
+      j.scale = w.s1[static_cast<size_t>(l)];
+      j.s_stride = w.ld[static_cast<size_t>(l)];
+      j.a_point_rows = t_point_rows(l);
+      j.m_valid = static_cast<int>(n_pad_);
+      j.n_valid = static_cast<int>(dn.rows);
+      j.c = t_buf(l + 1);
+      j.c_point_stride = n_pad_ * ldt_;
+      j.ldc = ldt_;
+      const int ma = l == 0 ? map_id(tm_t0_a_) : map_id(w.tm_t_a[static_cast<size_t>(l)]);
+      const int job = add_job(j, ma, map_id(dn.tm_w));
+      const int tn_n = ceil_div(dn.rows, kBN);
+      ntiles_n[static_cast<size_t>(l + 1)] = tn_n;
+      const int kb = kbs(dn.cols);
+      // groups of df_group_ row blocks sweep the N tiles together: the
+      // W_{l+1} tile of one tn is read by the group's CTAs at about the same
+      // time (L2 reuse), and a group's rows complete after group * tn_n
+      // tiles, so the next layer can start on them early
+      for (int p = 0; p < nb; ++p)
+        for (int g0 = 0; g0 < tiles_m; g0 += df_group_)
+          for (int tn = 0; tn < tn_n; ++tn)
+            for (int tm = g0; tm < std::min(tiles_m, g0 + df_group_); ++tm)
+            add_item(job, p, tm, tn, 0, kb, 0, row_base[static_cast<size_t>(l + 1)] + p * tiles_m + tm,
+                     {{fwd_cnt[static_cast<size_t>(l)], nfwd[static_cast<size_t>(l)]},
+                      {l >= 1 ? row_base[static_cast<size_t>(l)] + p * tiles_m + tm : 0,
+                       l >= 1 ? ntiles_n[static_cast<size_t>(l)] : 0}},
+                     kb * t_kb + t_item);
+      flops += 2.0 * n_ * dn.rows * dn.cols * nb;
+    }
+    if (si < syrk_layers.size() && syrk_layers[si] == l) {
+      const DevLayer& d = layers_[static_cast<size_t>(l)];
+      dev::DfJob j{};
+      j.kind = dev::kDfSyrk;
+      j.a_bytes = dev::kABytes;
+      j.scale = w.d[static_cast<size_t>(l)];
+      j.s_stride = w.ld[static_cast<size_t>(l)];
+      j.a_point_rows = t_point_rows(l);
+      j.b_point_rows = t_point_rows(l);
+      j.m_valid = static_cast<int>(n_);
+      j.n_valid = static_cast<int>(n_);
+      j.c = nullptr;  // patched: the plan's H slots
+      j.c_point_stride = n_pad_ * n_pad_;
+      j.ldc = n_pad_;
+      const int ma = l == 0 ? map_id(tm_t0_a_) : map_id(w.tm_t_a[static_cast<size_t>(l)]);
+      const int mb = l == 0 ? map_id(tm_t0_b_) : map_id(w.tm_t_b[static_cast<size_t>(l)]);
+      const int job = add_job(j, ma, mb);
+      const int kb = kbs(d.rows);
+      const int np = pieces[si];
+      // d_l comes from ADJ(l+1) (its epilogue), T_l rows from GEMM(l-1)
+      const std::pair<int, int> ddep{adj_cnt[static_cast<size_t>(l + 1)], nadj[static_cast<size_t>(l + 1)]};
+      for (int p = 0; p < nb; ++p)
+        for (int t = 0; t < n_st; ++t) {
+          const int ti = stiles[static_cast<size_t>(t)].x, tj = stiles[static_cast<size_t>(t)].y;
+          const int b0 = std::min(tiles_m - 1, tj * kBN / kBM), b1 = std::min(tiles_m - 1, (tj * kBN + kBN - 1) / kBM);
+          auto rdep = [&](int blk) -> std::pair<int, int> {
+            if (l == 0) return {0, 0};
+            return {row_base[static_cast<size_t>(l)] + p * tiles_m + blk, ntiles_n[static_cast<size_t>(l)]};
+          };
+          for (int q = 0; q < np; ++q) {
+            // ordinal of layer l among the SYRK layers that use slot q
+            int ord = 0;
+            for (size_t u = 0; u < si; ++u) ord += pieces[u] > q ? 1 : 0;
+            const int k0 = static_cast<int>(static_cast<int64_t>(kb) * q / np);
+            const int k1 = static_cast<int>(static_cast<int64_t>(kb) * (q + 1) / np);
+            add_item(job, p, ti, tj, k0, k1, q, hcnt(q, p, t),
+                     {ddep, rdep(ti), rdep(b0), rdep(b1), {hcnt(q, p, t), ord}}, (k1 - k0) * t_kb + t_item);
+          }
+        }
+      flops += static_cast<double>(d.rows) * n_ * (n_ + 1) * nb;
+      ++si;
+    }
+  }
+
+  // ---- list-scheduling simulation -> claim order ----
+  const size_t N = nodes.size();
+  std::vector<double> rank(N, 0.0), cmax(static_cast<size_t>(nc), 0.0);
+  for (size_t i = N; i-- > 0;) {
+    rank[i] = nodes[i].cost + cmax[static_cast<size_t>(nodes[i].it.sig)];
+    for (int k = 0; k < nodes[i].it.nwait; ++k) {
+      double& c = cmax[static_cast<size_t>(nodes[i].it.widx[k])];
+      c = std::max(c, rank[i]);
+    }
+  }
+  std::vector<std::vector<std::pair<int, int>>> waiters(static_cast<size_t>(nc));
+  std::vector<int> pending(N, 0), count(static_cast<size_t>(nc), 0);
+  for (size_t i = 0; i < N; ++i) {
+    pending[i] = nodes[i].it.nwait;
+    for (int k = 0; k < nodes[i].it.nwait; ++k)
+      waiters[static_cast<size_t>(nodes[i].it.widx[k])].emplace_back(static_cast<int>(i), nodes[i].it.wtgt[k]);
+  }
+  auto by_rank = [&](int a, int b) { return rank[static_cast<size_t>(a)] < rank[static_cast<size_t>(b)] ||
+                                            (rank[static_cast<size_t>(a)] == rank[static_cast<size_t>(b)] && a > b); };
+  std::priority_queue<int, std::vector<int>, decltype(by_rank)> ready(by_rank);
+  using Ev = std::pair<double, int>;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> events;
+  for (size_t i = 0; i < N; ++i)
+    if (pending[i] == 0) ready.push(static_cast<int>(i));
+  std::vector<int> order;
+  order.reserve(N);
+  int free_w = sm_count_;
+  double now = 0.0;
+  while (order.size() < N) {
+    while (free_w > 0 && !ready.empty()) {
+      const int i = ready.top();
+      ready.pop();
+      order.push_back(i);
+      events.emplace(now + nodes[static_cast<size_t>(i)].cost, i);
+      --free_w;
+    }
+    if (events.empty()) throw StructuralError("dataflow: dependency cycle in the item list");
+    const Ev e = events.top();
+    events.pop();
+    now = e.first;
+    ++free_w;
+    const int sig = nodes[static_cast<size_t>(e.second)].it.sig;
+    const int c = ++count[static_cast<size_t>(sig)];
+    for (const auto& wt : waiters[static_cast<size_t>(sig)])
+      if (wt.second == c && --pending[static_cast<size_t>(wt.first)] == 0) ready.push(wt.first);
+  }
+  while (!events.empty()) {
+    now = events.top().first;
+    events.pop();
+  }
+
+  // ---- upload ----
+  DfPlan plan;
+  plan.nb = nb;
+  plan.n_items = static_cast<int>(N);
+  plan.n_counters = nc;
+  plan.slots = slots;
+  plan.slot_stride = static_cast<int64_t>(nb) * n_pad_ * n_pad_;
+  plan.flops = flops;
+  plan.bytes = bytes;
+  plan.sim_ms = now;
+  plan.maps = maps;
+  CK(cudaMalloc(&plan.hslots, sizeof(double) * static_cast<size_t>(plan.slot_stride) * slots));
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    jobs[i].ta = job_maps[i].first;
+    jobs[i].tb = job_maps[i].second;
+    if (jobs[i].kind == dev::kDfSyrk) {
+      jobs[i].c = plan.hslots;
+      jobs[i].slot_stride = plan.slot_stride;
+    }
+  }
+  CK(cudaMalloc(&plan.jobs, sizeof(dev::DfJob) * jobs.size()));
+  CK(cudaMemcpy(plan.jobs, jobs.data(), sizeof(dev::DfJob) * jobs.size(), cudaMemcpyHostToDevice));
+  std::vector<dev::DfItem> items(N);
+  for (size_t i = 0; i < N; ++i) items[i] = nodes[static_cast<size_t>(order[i])].it;
+  CK(cudaMalloc(&plan.items, sizeof(dev::DfItem) * N));
+  CK(cudaMemcpy(plan.items, items.data(), sizeof(dev::DfItem) * N, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&plan.counters, sizeof(int) * static_cast<size_t>(nc)));
+  return df_plans_.emplace(nb, plan).first->second;
+}
+
+// One evaluation on the dataflow path: counters/H slots reset, the
+// persistent launch, then the final layer (U, J, output curvature) and the
+// symmetrise pass.
+void DeviceNet::enqueue_dataflow(cudaStream_t st, int nb, const Outputs& o) {
+  auto found = df_plans_.find(nb);
+  if (found == df_plans_.end()) throw StructuralError("dataflow plan missing (prepare() not called)");
+  DfPlan& P = found->second;
+  Workspace& w = ws_;
+  const int L = static_cast<int>(L_);
+  CK(cudaMemsetAsync(P.counters, 0, sizeof(int) * static_cast<size_t>(P.n_counters), st));
+  CK(cudaMemsetAsync(P.hslots, 0, sizeof(double) * static_cast<size_t>(P.slot_stride) * P.slots, st));
+  thread_local dev::DfParams prm;  // 24 KB: not on the stack (copied at launch)
+  std::memset(&prm, 0, sizeof(prm));
+  std::copy(P.maps.begin(), P.maps.end(), prm.maps);
+  prm.items = P.items;
+  prm.n_items = P.n_items;
+  prm.jobs = P.jobs;
+  prm.counters = P.counters;
+  prm.trace = df_trace_;
+  prm.trace_sm = df_trace_sm_;
+  prof_begin(st, kTagDataflow, P.flops, P.bytes);
+  const int grid = std::min(sm_count_, P.n_items);
+  dev::df_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(prm);
+  after_launch(st);
+  if (o.y)
+    CK(cudaMemcpy2DAsync(o.y, sizeof(double) * m_, w.y[static_cast<size_t>(L - 1)],
+                         sizeof(double) * w.ld[static_cast<size_t>(L - 1)], sizeof(double) * m_, nb,
+                         cudaMemcpyDeviceToDevice, st));
+  // final layer: U = T_{L-2} diag(sigma'_{L-2}) W_{L-1}^T (m <= 16 outputs)
+  const int l = L - 2;
+  const double* tl = l == 0 ? t0_ : w.t[static_cast<size_t>((l - 1) % static_cast<int>(w.t.size()))];
+  launch_skinny(st, nb, tl, l == 0 ? ldt0_ : ldt_, l == 0 ? 0 : n_pad_, l);
+  const DevLayer& df = layers_[static_cast<size_t>(L - 1)];
+  if (o.j) {
+    const int64_t tot = static_cast<int64_t>(nb) * n_;
+    prof_begin(st, kTagJacOut, 0, 0);
+    dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, st>>>(w.u, dev::kSkMB, n_pad_, w.s1[static_cast<size_t>(L - 1)],
+                                                                 w.y[static_cast<size_t>(L - 1)],
+                                                                 w.ld[static_cast<size_t>(L - 1)], static_cast<int>(n_),
+                                                                 static_cast<int>(m_), nb, 0, o.j);
+    after_launch(st);
+  }
+  if (df.act != kLinear) {  // output-layer curvature, K = m: into slot 0
+    dim3 blk(16, 16);
+    dim3 grid2(ceil_div(n_, 16), ceil_div(n_, 16), nb);
+    prof_begin(st, kTagSmallSyrk, 0, 0);
+    dev::small_k_syrk_kernel<<<grid2, blk, 0, st>>>(w.u, dev::kSkMB, n_pad_, w.d[static_cast<size_t>(L - 1)],
+                                                    w.ld[static_cast<size_t>(L - 1)], nullptr, 0, static_cast<int>(n_),
+                                                    static_cast<int>(m_), nb, P.hslots, n_pad_ * n_pad_, n_pad_);
+    after_launch(st);
+  }
+  const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
+  prof_begin(st, kTagSymmetrize, 0, 0);
+  dev::symmetrize_slots_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(P.hslots, P.slots, P.slot_stride, n_pad_ * n_pad_,
+                                                                   n_pad_, static_cast<int>(n_), nb, o.h);
+  after_launch(st);
+}
+
+// ---------------------------------------------------------------------------
 // Net <-> DeviceNet glue.
 // ---------------------------------------------------------------------------
 Net::~Net() = default;
@@ -1188,7 +1742,7 @@ const char* kernel_tag_name(int tag) {
                                          "adj_reduce",   "nt_mma.gemm",   "nt_mma.syrk",  "syrk_reduce",
                                          "skinny_nt",    "skinny_reduce", "jacobian_out", "small_k_syrk",
                                          "symmetrize",   "nt_mma.fwd",    "nt_mma.adj",   "row_epilogue",
-                                         "nt_mma.step"};
+                                         "nt_mma.step",  "dataflow"};
   return (tag >= 0 && tag < kTagCount) ? names[tag] : "unknown";
 }
 

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgbopt_b200.so")
+LIB_PATH = os.environ.get("GBOPT_LIB") or os.path.join(_HERE, "libgbopt_b200.so")  # GBOPT_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -75,6 +75,9 @@ _net_oracle_batched = _fn("gbopt_net_oracle_batched", _status, _vp, _sz, _dp, _s
 _net_oracle_batched_device = _fn("gbopt_net_oracle_batched_device", _status, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp,
                                  _vp, _vp)
 _net_last_launch_count = _fn("gbopt_net_last_launch_count", _i64, _vp)
+_net_set_schedule = _fn("gbopt_net_set_schedule", _status, _vp, ctypes.c_int)
+_net_last_schedule = _fn("gbopt_net_last_schedule", ctypes.c_int, _vp)
+_net_dataflow_trace = _fn("gbopt_net_dataflow_trace", _status, _vp, _sz, _vp, _vp, _dp, _sz, ctypes.POINTER(_sz))
 _net_set_graphs = _fn("gbopt_net_set_graphs", _status, _vp, ctypes.c_int)
 _net_profile = _fn("gbopt_net_profile", _status, _vp, _sz, _vp, _vp, ctypes.POINTER(ctypes.c_int32),
                    ctypes.POINTER(ctypes.c_float), _dp, _dp, _sz, ctypes.POINTER(_sz))
@@ -297,6 +300,16 @@ class NeuralNet:
     def last_launch_count(self) -> int:
         return int(_net_last_launch_count(self._h))
 
+    def set_schedule(self, schedule: str) -> "NeuralNet":
+        """'auto', 'layered' or 'dataflow' (gbopt_net_set_schedule)."""
+        code = {"auto": -1, "layered": 0, "dataflow": 1}[schedule]
+        _check(_net_set_schedule(self._h, code))
+        return self
+
+    @property
+    def last_schedule(self) -> str:
+        return {-1: "unbound", 0: "layered", 1: "dataflow"}[int(_net_last_schedule(self._h))]
+
     # ---- oracle ----------------------------------------------------------
     def forward(self, x) -> np.ndarray:
         x = _vec(x)
@@ -398,6 +411,17 @@ def profile_timeline(net: "NeuralNet", batch: int, dX: int, dLam: int):
     _check(_net_profile_timeline(net._h, batch, dX, dLam, tags, st, t0, t1, cap, ctypes.byref(cnt)))
     return [(_kernel_tag_name(tags[i]).decode(), int(st[i]), float(t0[i]), float(t1[i]))
             for i in range(min(cnt.value, cap))]
+
+
+def dataflow_trace(net: "NeuralNet", batch: int, dX: int, dLam: int) -> np.ndarray:
+    """Per-item trace of one eager dataflow evaluation (gbopt_net_dataflow_trace):
+    rows {kind, job, point, tm, tn, kb0, kb1, sm, t_claimed, t_ready, t_begin,
+    t_end} in claim order, times in microseconds."""
+    cnt = _sz()
+    _check(_net_dataflow_trace(net._h, batch, dX, dLam, None, 0, ctypes.byref(cnt)))
+    out = np.empty(12 * cnt.value, dtype=np.float64)
+    _check(_net_dataflow_trace(net._h, batch, dX, dLam, out.ctypes.data_as(_dp), out.size, ctypes.byref(cnt)))
+    return out.reshape(-1, 12)
 
 
 class LdltFactorization:
