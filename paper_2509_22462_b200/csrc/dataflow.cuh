@@ -37,6 +37,22 @@ namespace gbb {
 namespace dev {
 
 enum DfKind : int { kDfFwd = 0, kDfAdj = 1, kDfGemm = 2, kDfSyrk = 3 };
+
+// Stage of the dataflow ring: A box (14 KB) | B box (16 KB) | the item's
+// per-k scale for the stage's 16 k (128 B, bulk-copied with the boxes, so the
+// consumers hold no scale registers and issue no global loads), padded so
+// every stage starts 1024-byte aligned (128B swizzle).
+constexpr int kDfScaleOff = kABytes + kBBytes;
+constexpr int kDfStageBytes = (kDfScaleOff + kBK * 8 + 1023) / 1024 * 1024;  // 31744
+constexpr int kDfSmemBytes = kStages * kDfStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+
+// 1-D bulk copy global -> shared, completion counted in bytes on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 constexpr int kDfMaxWait = 5;
 
 struct alignas(16) DfJob {
@@ -47,6 +63,8 @@ struct alignas(16) DfJob {
   int64_t a_point_rows, b_point_rows;
   int kind, act;
   int a_bytes;  // bytes of one A box (FWD / ADJ: a box of round_up(points, 8) rows)
+  int b_bytes;  // bytes of one B box (kBN rows; square SYRK tiles: kBM rows)
+  int b_tile;   // C columns per tile = B row offset per tn (kBN, or kBM for square SYRK tiles)
   int m_valid;  // FWD/ADJ: points; GEMM: n_pad; SYRK: n
   int n_valid;  // valid output columns
   // GEMM: T_{l+1}; SYRK: H slot 0 (slots slot_stride apart)
@@ -109,61 +127,87 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// The consumer k-loop over [kb0, kb1).  Full tiles (tangent GEMM, SYRK): the
-// 2 x 4 warp grid of nt_mma_kernel, 7 x 4 DMMA blocks per warp.  Point-row
+// The consumer k-loop over [kb0, kb1).  Full tiles (tangent GEMM): the
+// 2 x 4 warp grid of nt_mma_kernel, 7 x 4 DMMA blocks per warp.  Square
+// SYRK tiles (112 x 112): SM sub-partition q = warp & 3 owns the 56 x 56
+// quadrant q, split between its two warps as 4 + 3 block rows x 7 block
+// columns (49 blocks per sub-partition: the DMMA pipes stay balanced, and
+// no warp holds more than 28 accumulator blocks).  Point-row
 // tiles (FWD / ADJ, M = points <= 56): every warp takes 16 of the 128
 // columns and the MI live 8-row blocks, so no DMMA is issued for empty rows
 // (a predicated-off DMMA still occupies the tensor pipe).  The per-k scale
-// is produced inside the launch: L2 loads (ld.cg), one k-block ahead.
-// Scale vectors are single-assignment within a launch and only read after
-// their producer's counter: the non-coherent path cannot hold a stale copy.
-__device__ __forceinline__ double ld_scale(const double* p) {
-  return __ldg(p);
-}
+// arrives in the stage (bulk copy by the producer).
+constexpr int kAcc = kMI * kNJ;  // 28 DMMA accumulator blocks per warp, in every layout
 
 template <int MI, int NJ>
-__device__ __forceinline__ void df_mainloop(double (&acc)[kMI][kNJ][2], const char* smem, uint64_t* full,
-                                            uint64_t* empty, uint32_t& gk, int kb0, int kb1, const double* sp,
+__device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* smem, uint64_t* full,
+                                            uint64_t* empty, uint32_t& gk, int kb0, int kb1, bool scaled,
                                             int ra, int rb, int t, int lane) {
-  double sc_next[4] = {1.0, 1.0, 1.0, 1.0};
-  if (sp && kb0 < kb1) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sc_next[q] = ld_scale(sp + kb0 * kBK + 4 * q + t);
-  }
   for (int kb = kb0; kb < kb1; ++kb, ++gk) {
     const int s = static_cast<int>(gk % kStages);
-    double sc[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sc[q] = sc_next[q];
-    if (sp && kb + 1 < kb1) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sc_next[q] = ld_scale(sp + (kb + 1) * kBK + 4 * q + t);
-    }
     mbar_wait(&full[s], (gk / kStages) & 1);
-    const char* sa = smem + s * kStageBytes;
+    const char* sa = smem + s * kDfStageBytes;
     const char* sb = sa + kABytes;
+    const double* ss = reinterpret_cast<const double*>(sa + kDfScaleOff);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int k = 4 * q + t;
+      const double sc = scaled ? ss[k] : 1.0;
       double a[MI], b[NJ];
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc[q];
+      for (int nj = 0; nj < NJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc;
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < NJ; ++nj) dmma884(acc[mi][nj], a[mi], b[nj]);
+        for (int nj = 0; nj < NJ; ++nj) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
+// Epilogue of one warp's accumulator blocks (layout MI x NJ, the first mi_n
+// block rows live): block mi * NJ + nj holds C[rbase + 8 mi][cbase + 8 nj +
+// pc0 / pc1].  rmw: accumulate into C (SYRK H slots), with every load
+// issued before the first store (they could alias, so the compiler would
+// otherwise serialise load -> store per element).
+template <int MI, int NJ>
+__device__ __forceinline__ void df_store(double (&acc)[kAcc][2], double* raw, int64_t ldr, int rbase, int cbase,
+                                         int mi_n, int m_valid, int n_valid, int pc0, int pc1, bool rmw) {
+  if (rmw) {
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int r = rbase + 8 * mi;
+      if (mi >= mi_n || r >= m_valid) continue;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj) {
+        const int cb = cbase + 8 * nj;
+        const double* src = raw + static_cast<int64_t>(r) * ldr + cb;
+        if (cb + pc0 < n_valid) acc[mi * NJ + nj][0] += __ldcg(src + pc0);
+        if (cb + pc1 < n_valid) acc[mi * NJ + nj][1] += __ldcg(src + pc1);
+      }
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int r = rbase + 8 * mi;
+    if (mi >= mi_n || r >= m_valid) continue;
+#pragma unroll
+    for (int nj = 0; nj < NJ; ++nj) {
+      const int cb = cbase + 8 * nj;
+      double* dst = raw + static_cast<int64_t>(r) * ldr + cb;
+      if (cb + pc0 < n_valid) dst[pc0] = acc[mi * NJ + nj][0];
+      if (cb + pc1 < n_valid) dst[pc1] = acc[mi * NJ + nj][1];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__ DfParams P) {
   extern __shared__ unsigned char smem_raw[];
   char* smem = reinterpret_cast<char*>(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kDfStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* qfull = empty + kStages;  // item hand-off, 2 slots
   uint64_t* qempty = qfull + 2;
@@ -221,14 +265,17 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
         mbar_arrive(&qfull[slot]);
         const DfJob& J = P.jobs[it.job];
         const int a_row0 = static_cast<int>(J.a_point_rows * it.point) + it.tm * kBM;
-        const int b_row0 = static_cast<int>(J.b_point_rows * it.point) + it.tn * kBN;
+        const int b_row0 = static_cast<int>(J.b_point_rows * it.point) + it.tn * J.b_tile;
+        // the scale vector has >= 16 * k_blocks entries (zero padded)
+        const double* sp = J.scale ? J.scale + J.s_stride * it.point : nullptr;
         for (int kb = it.kb0; kb < it.kb1; ++kb, ++gk) {
           const int s = static_cast<int>(gk % kStages);
           if (gk >= kStages) mbar_wait(&empty[s], ((gk / kStages) - 1) & 1);
-          char* sa = smem + s * kStageBytes;
-          mbar_arrive_expect_tx(&full[s], J.a_bytes + kBBytes);
+          char* sa = smem + s * kDfStageBytes;
+          mbar_arrive_expect_tx(&full[s], J.a_bytes + J.b_bytes + (sp ? kBK * 8 : 0));
           tma_load_2d(sa, &P.maps[J.ta], &full[s], kb * kBK, a_row0);
           tma_load_2d(sa + kABytes, &P.maps[J.tb], &full[s], kb * kBK, b_row0);
+          if (sp) bulk_load(sa + kDfScaleOff, sp + kb * kBK, kBK * 8, &full[s]);
         }
       }
     }
@@ -256,68 +303,67 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
     // FWD / ADJ tiles hold only m_valid (= points) live rows: skip the
     // DMMA blocks past them (uniform per warp)
     const int m_live = kind <= kDfAdj ? J.m_valid : kBM;
-    const double* sp = J.scale ? J.scale + J.s_stride * it.point : nullptr;
+    const bool scaled = J.scale != nullptr;
 
-    double acc[kMI][kNJ][2];
+    double acc[kAcc][2];
 #pragma unroll
-    for (int a = 0; a < kMI; ++a)
-#pragma unroll
-      for (int b = 0; b < kNJ; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int a = 0; a < kAcc; ++a) acc[a][0] = acc[a][1] = 0.0;
 
+    // warp layout of this item: rows row0 + 8 mi (+ pg), mi < mi_n; columns
+    // col0 + 8 nj (+ pc), nj < nj_n; accumulator block mi * nj_n + nj
+    int row0, col0, mi_n, nj_n;
+    const int sq = kind == kDfSyrk && J.b_tile == kBM;
     // point-row tiles (FWD / ADJ) with few points use the column-split warp layout
     const int small = (kind <= kDfAdj && m_live <= 56) ? (m_live <= 8 ? 1 : m_live <= 16 ? 2 : m_live <= 32 ? 4 : 7) : 0;
-    const int row0 = small ? 0 : wm * kWarpM;
-    const int col0 = small ? warp * 16 : wn * kWarpN;
-    const int mi_n = small ? small : kMI;
-    const int nj_n = small ? 2 : kNJ;
-    const int ra_s = row_perm(g), rb_s = warp * 16 + row_perm(g);
-    if (small == 0)
-      df_mainloop<kMI, kNJ>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra, rb, t, lane);
-    else if (small == 1)
-      df_mainloop<1, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
-    else if (small == 2)
-      df_mainloop<2, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
-    else if (small == 4)
-      df_mainloop<4, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
-    else
-      df_mainloop<7, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, sp, ra_s, rb_s, t, lane);
+    if (sq) {
+      const int q = warp & 3, h = warp >> 2;
+      row0 = (q >> 1) * 56 + h * 32;
+      col0 = (q & 1) * 56;
+      mi_n = h ? 3 : 4;
+      nj_n = 7;
+      const int ra_q = row0 + row_perm(g), rb_q = col0 + row_perm(g);
+      if (h == 0)
+        df_mainloop<4, 7>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
+      else
+        df_mainloop<3, 7>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
+    } else if (small == 0) {
+      row0 = wm * kWarpM;
+      col0 = wn * kWarpN;
+      mi_n = kMI;
+      nj_n = kNJ;
+      df_mainloop<kMI, kNJ>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra, rb, t, lane);
+    } else {
+      row0 = 0;
+      col0 = warp * 16;
+      mi_n = small;
+      nj_n = 2;
+      const int ra_s = row_perm(g), rb_s = warp * 16 + row_perm(g);
+      if (small == 1)
+        df_mainloop<1, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+      else if (small == 2)
+        df_mainloop<2, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+      else if (small == 4)
+        df_mainloop<4, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+      else
+        df_mainloop<7, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+    }
 
-    // ---- epilogue: thread holds C[row0+8mi+pg][col0+8nj+pc0 / pc1] ----
+    // ---- epilogue: block e = mi * nj_n + nj holds C[row0+8mi+pg][col0+8nj+pc0 / pc1] ----
     // GEMM: store T; SYRK: accumulate into H slot; FWD / ADJ: raw tile into
     // z / ybar, then one elementwise pass (activation or gz / d) over it.
     double* raw = kind == kDfGemm ? J.c + J.c_point_stride * it.point
                 : kind == kDfSyrk ? J.c + J.slot_stride * it.slot + J.c_point_stride * it.point
                 : kind == kDfFwd  ? J.z : J.ybar;
     const int64_t ldr = kind >= kDfGemm ? J.ldc : J.ld;
-    if (kind == kDfSyrk) {
-      // all loads of the H slot first (the stores below could alias them, so
-      // the compiler would otherwise serialise load -> store per element)
-#pragma unroll
-      for (int mi = 0; mi < kMI; ++mi) {
-        const int r = it.tm * kBM + row0 + 8 * mi + pg;
-        if (r >= J.m_valid) continue;
-#pragma unroll
-        for (int nj = 0; nj < kNJ; ++nj) {
-          const int cb = it.tn * kBN + col0 + 8 * nj;
-          const double* src = raw + static_cast<int64_t>(r) * ldr + cb;
-          if (cb + pc0 < J.n_valid) acc[mi][nj][0] += __ldcg(src + pc0);
-          if (cb + pc1 < J.n_valid) acc[mi][nj][1] += __ldcg(src + pc1);
-        }
-      }
-    }
-#pragma unroll
-    for (int mi = 0; mi < kMI; ++mi) {
-      const int r = it.tm * kBM + row0 + 8 * mi + pg;
-      if (mi >= mi_n || r >= J.m_valid) continue;
-#pragma unroll
-      for (int nj = 0; nj < kNJ; ++nj) {
-        if (nj >= nj_n) continue;
-        const int cb = it.tn * kBN + col0 + 8 * nj;
-        double* dst = raw + static_cast<int64_t>(r) * ldr + cb;
-        if (cb + pc0 < J.n_valid) dst[pc0] = acc[mi][nj][0];
-        if (cb + pc1 < J.n_valid) dst[pc1] = acc[mi][nj][1];
-      }
-    }
+    const int rbase = it.tm * kBM + row0 + pg;
+    const int cbase = it.tn * J.b_tile + col0;
+    const bool rmw = kind == kDfSyrk;
+    if (sq)
+      df_store<4, 7>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
+    else if (small == 0)
+      df_store<kMI, kNJ>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
+    else
+      df_store<7, 2>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
     if (kind <= kDfAdj) {
       consumer_bar();  // the raw tile is complete (CTA-scope ordering of the stores)
       const int cols = min(kBN, J.n_valid - it.tn * kBN);

@@ -182,6 +182,7 @@ class DeviceNet {
  private:
   int dataflow_mode_ = -1;  // GBOPT_DATAFLOW: -1 auto, 0 off, 1 whenever the shape allows
   std::map<int, DfPlan> df_plans_;
+  bool df_square_ = true;  // square 112 x 112 SYRK tiles in the dataflow launch (GBOPT_DF_SQ)
   int df_group_ = 4;  // row blocks per raster group of the tangent GEMM items (GBOPT_DF_GROUP)
   void prof_begin(cudaStream_t st, int tag, double flops, double bytes);
   void after_launch(cudaStream_t st);
