@@ -211,6 +211,9 @@ class DeviceNet {
   CUtensorMap tm_t0_a_, tm_t0_b_;
   int2* syrk_tiles_ = nullptr;
   int n_syrk_tiles_ = 0;
+  int2* sq_tiles_ = nullptr;  // square 112 x 112 lower tiles (layer-by-layer SYRKs)
+  int n_sq_tiles_ = 0;
+  bool square_syrk_ = true;   // GBOPT_SQ=0: 112 x 128 SYRK tiles
   Workspace ws_;
   int ws_cap_ = 0;
   bool transposed_ = false;

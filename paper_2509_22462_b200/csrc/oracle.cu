@@ -184,6 +184,15 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   n_syrk_tiles_ = static_cast<int>(tiles.size());
   CK(cudaMalloc(&syrk_tiles_, sizeof(int2) * tiles.size()));
   CK(cudaMemcpy(syrk_tiles_, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice));
+  // square 112 x 112 lower tiles (tn <= tm) for the layer-by-layer SYRKs
+  std::vector<int2> sq;
+  for (int tm = 0; tm * kBM < n_; ++tm)
+    for (int tn = 0; tn <= tm; ++tn) sq.push_back(make_int2(tm, tn));
+  n_sq_tiles_ = static_cast<int>(sq.size());
+  CK(cudaMalloc(&sq_tiles_, sizeof(int2) * sq.size()));
+  CK(cudaMemcpy(sq_tiles_, sq.data(), sizeof(int2) * sq.size(), cudaMemcpyHostToDevice));
+  if (const char* e = std::getenv("GBOPT_SQ")) square_syrk_ = e[0] != '0';
+  if (streamk_ || hybrid_) square_syrk_ = false;  // the stream-K kernel has only 112 x 128 tiles
 }
 
 DeviceNet::~DeviceNet() {
@@ -196,6 +205,7 @@ DeviceNet::~DeviceNet() {
   }
   cudaFree(t0_);
   cudaFree(syrk_tiles_);
+  cudaFree(sq_tiles_);
   if (stream_) cudaStreamDestroy(stream_);
   if (stream2_) cudaStreamDestroy(stream2_);
   for (cudaEvent_t e : evpool_) cudaEventDestroy(e);
@@ -229,7 +239,7 @@ double* DeviceNet::ws_alloc(size_t n_doubles) {
 // Split-K factor of a layer's SYRK: enough CTAs to cover the SMs, at least
 // 8 k-blocks (128 of K) per split.
 int DeviceNet::syrk_split(int points, int k_blocks) const {
-  const int tiles = points * n_syrk_tiles_;
+  const int tiles = points * (square_syrk_ ? n_sq_tiles_ : n_syrk_tiles_);
   if (tiles >= sm_count_) return 1;
   return std::max(1, std::min(sm_count_ / tiles, k_blocks / 8));
 }
@@ -309,7 +319,7 @@ void DeviceNet::ensure_workspace(int batch) {
       w.sk_counters[s] = reinterpret_cast<int*>(ws_alloc((static_cast<size_t>(w.sk_counter_cap) + 1) / 2));
   }
   // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
-  w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, n_syrk_tiles_)) * kBM * kBN);
+  w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, std::max(n_syrk_tiles_, n_sq_tiles_))) * kBM * kBN);
   w.gemm_part = ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN);
   // final-layer skinny product: U [cap][n_pad][16], partials [chunks][cap][n_pad][16]
   const int64_t kfin = layers_[L - 1].cols;
@@ -831,13 +841,19 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       launch_sk(sb, jobs, true);
       return;
     }
+    if (square_syrk_) {  // 112 x 112 lower tiles, B through the 112-row box map
+      p.tiles = sq_tiles_;
+      p.n_tiles = n_sq_tiles_;
+      p.square = 1;
+    }
     prof_begin(sb, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
-    launch_nt(sb, tmap_a(l), tmap_b(l), p, nb * n_syrk_tiles_ * p.split);
+    launch_nt(sb, tmap_a(l), square_syrk_ ? tmap_a(l) : tmap_b(l), p, nb * p.n_tiles * p.split);
     if (p.split > 1) {
       prof_begin(sb, kTagSyrkReduce, 0, 0);
-      dim3 grid(8, nb * n_syrk_tiles_);
-      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, sb>>>(w.syrk_part, syrk_tiles_, n_syrk_tiles_, nb, p.split, w.h,
-                                                            n_pad_ * n_pad_, n_pad_, static_cast<int>(n_));
+      dim3 grid(8, nb * p.n_tiles);
+      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, sb>>>(w.syrk_part, p.tiles, p.n_tiles, nb, p.split, w.h,
+                                                            n_pad_ * n_pad_, n_pad_, static_cast<int>(n_),
+                                                            square_syrk_ ? kBM : kBN);
       after_launch(sb);
     }
   };
