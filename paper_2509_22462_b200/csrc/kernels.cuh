@@ -198,13 +198,25 @@ __host__ __device__ inline void decode_dense_tile(int local, int tiles_m, int ti
 // Row permutation within an 8-row DMMA block: g -> 2(g mod 4) + g/4.
 __device__ __forceinline__ int row_perm(int g) { return ((g & 3) << 1) | (g >> 2); }
 
+// Which DMMA blocks (mi, nj) of an MI x NJ warp layout a warp computes.
+// kBlkAll: all.  Square SYRK tiles: the two warps of an SM sub-partition
+// share a 7 x 7 quadrant as 25 + 24 blocks (kBlkSqLo: block rows 0-2 and
+// row 3 columns 0-3; kBlkSqHi, rows 3-6 seen from row 3: row 3 columns 4-6
+// and rows 4-6), so both keep the sub-partition's DMMA pipe busy to the end
+// of every k-step (a 28 + 21 split leaves the 28-block warp issuing alone).
+enum BlkSet : int { kBlkAll = 0, kBlkSqLo = 1, kBlkSqHi = 2 };
+template <int SET>
+__host__ __device__ constexpr bool blk_live(int mi, int nj) {
+  return SET == kBlkAll ? true : SET == kBlkSqLo ? (mi < 3 || nj < 4) : (mi > 0 || nj >= 4);
+}
+
 // The consumer k-loop of nt_mma_kernel for an MI x NJ warp layout
 // (accumulator block mi * NJ + nj); the per-k scale on B is read one
 // k-block ahead through the read-only path (it was written by an earlier
 // launch).
 constexpr int kNtAcc = kMI * kNJ;
 
-template <int MI, int NJ>
+template <int MI, int NJ, int SET = kBlkAll>
 __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char* smem, uint64_t* full,
                                             uint64_t* empty, int nkb, int kb_begin, const double* sp, int ra,
                                             int rb, int t, int lane) {
@@ -236,7 +248,8 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < NJ; ++nj) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
+        for (int nj = 0; nj < NJ; ++nj)
+          if (blk_live<SET>(mi, nj)) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -245,7 +258,7 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
 
 // Epilogue of one warp's MI x NJ blocks (first mi_n block rows live).
 // Tile-relative rows r0 + 8 mi (+ pg), columns c0 + 8 nj (+ pc0 / pc1).
-template <int MI, int NJ>
+template <int MI, int NJ, int SET = kBlkAll>
 __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const NtParams& p, int split_idx, int point,
                                          int tm, int tn, int tile_n, int r0, int c0, int mi_n, int pg, int pc0,
                                          int pc1) {
@@ -258,6 +271,7 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
       if (mi >= mi_n) continue;
 #pragma unroll
       for (int nj = 0; nj < NJ; ++nj) {
+        if (!blk_live<SET>(mi, nj)) continue;
         const int r = r0 + 8 * mi + pg;
         const int cb = c0 + 8 * nj;
         out[r * kBN + cb + pc0] = acc[mi * NJ + nj][0];
@@ -273,6 +287,7 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
     if (mi >= mi_n || r >= p.m_rows_valid) continue;
 #pragma unroll
     for (int nj = 0; nj < NJ; ++nj) {
+      if (!blk_live<SET>(mi, nj)) continue;
       const int cb = tn * tile_n + c0 + 8 * nj;
       double* dst = cbase + static_cast<int64_t>(r) * p.ldc + cb;
 #pragma unroll
@@ -287,8 +302,8 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
 // Square SYRK tiles (p.square): the tile is 112 x 112 (B rows tn * 112, a
 // 112-row B box) over the lower triangle -- 87.6% useful work at n = 784
 // against 76.7% for 112 x 128 tiles.  SM sub-partition q = warp & 3 owns the
-// 56 x 56 quadrant q, split between its two warps as 4 + 3 block rows x 7
-// block columns, so each sub-partition's DMMA pipe gets 49 blocks.
+// 56 x 56 quadrant q, split between its two warps as 25 + 24 of its 7 x 7
+// blocks (blk_live), so each sub-partition's DMMA pipe gets 49 blocks.
 __global__ void __launch_bounds__(kThreads, 1)
     nt_mma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const NtParams p) {
@@ -369,13 +384,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
   if (sq) {
     const int q = warp & 3, h = warp >> 2;
-    const int r0 = (q >> 1) * 56 + h * 32, c0 = (q & 1) * 56;
+    const int r0 = (q >> 1) * 56 + h * 24, c0 = (q & 1) * 56;
     if (h == 0) {
-      nt_mainloop<4, 7>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
-      nt_store<4, 7>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
+      nt_mainloop<4, 7, kBlkSqLo>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
+      nt_store<4, 7, kBlkSqLo>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
     } else {
-      nt_mainloop<3, 7>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
-      nt_store<4, 7>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, 3, pg, pc0, pc1);
+      nt_mainloop<4, 7, kBlkSqHi>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
+      nt_store<4, 7, kBlkSqHi>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
     }
   } else {
     const int wm = warp >> 2;  // 0..1
