@@ -130,8 +130,8 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // The consumer k-loop over [kb0, kb1).  Full tiles (tangent GEMM): the
 // 2 x 4 warp grid of nt_mma_kernel, 7 x 4 DMMA blocks per warp.  Square
 // SYRK tiles (112 x 112): SM sub-partition q = warp & 3 owns the 56 x 56
-// quadrant q, split between its two warps as 4 + 3 block rows x 7 block
-// columns (49 blocks per sub-partition: the DMMA pipes stay balanced, and
+// quadrant q, split between its two warps as 25 + 24 of its 7 x 7 blocks
+// (blk_live: both warps keep the pipe busy to the end of each k-step, and
 // no warp holds more than 28 accumulator blocks).  Point-row
 // tiles (FWD / ADJ, M = points <= 56): every warp takes 16 of the 128
 // columns and the MI live 8-row blocks, so no DMMA is issued for empty rows
@@ -139,7 +139,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // arrives in the stage (bulk copy by the producer).
 constexpr int kAcc = kMI * kNJ;  // 28 DMMA accumulator blocks per warp, in every layout
 
-template <int MI, int NJ>
+template <int MI, int NJ, int SET = kBlkAll>
 __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* smem, uint64_t* full,
                                             uint64_t* empty, uint32_t& gk, int kb0, int kb1, bool scaled,
                                             int ra, int rb, int t, int lane) {
@@ -161,7 +161,8 @@ __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* 
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < NJ; ++nj) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
+        for (int nj = 0; nj < NJ; ++nj)
+          if (blk_live<SET>(mi, nj)) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -170,36 +171,28 @@ __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* 
 
 // Epilogue of one warp's accumulator blocks (layout MI x NJ, the first mi_n
 // block rows live): block mi * NJ + nj holds C[rbase + 8 mi][cbase + 8 nj +
-// pc0 / pc1].  rmw: accumulate into C (SYRK H slots), with every load
-// issued before the first store (they could alias, so the compiler would
-// otherwise serialise load -> store per element).
-template <int MI, int NJ>
+// pc0 / pc1].  rmw: accumulate into C (SYRK H slots) with red.add: the slot
+// counter lets one item at a time touch a (slot, point, tile), so the
+// additions happen in layer order (deterministic).
+template <int MI, int NJ, int SET = kBlkAll>
 __device__ __forceinline__ void df_store(double (&acc)[kAcc][2], double* raw, int64_t ldr, int rbase, int cbase,
                                          int mi_n, int m_valid, int n_valid, int pc0, int pc1, bool rmw) {
-  if (rmw) {
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi) {
-      const int r = rbase + 8 * mi;
-      if (mi >= mi_n || r >= m_valid) continue;
-#pragma unroll
-      for (int nj = 0; nj < NJ; ++nj) {
-        const int cb = cbase + 8 * nj;
-        const double* src = raw + static_cast<int64_t>(r) * ldr + cb;
-        if (cb + pc0 < n_valid) acc[mi * NJ + nj][0] += __ldcg(src + pc0);
-        if (cb + pc1 < n_valid) acc[mi * NJ + nj][1] += __ldcg(src + pc1);
-      }
-    }
-  }
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi) {
     const int r = rbase + 8 * mi;
     if (mi >= mi_n || r >= m_valid) continue;
 #pragma unroll
     for (int nj = 0; nj < NJ; ++nj) {
+      if (!blk_live<SET>(mi, nj)) continue;
       const int cb = cbase + 8 * nj;
       double* dst = raw + static_cast<int64_t>(r) * ldr + cb;
-      if (cb + pc0 < n_valid) dst[pc0] = acc[mi * NJ + nj][0];
-      if (cb + pc1 < n_valid) dst[pc1] = acc[mi * NJ + nj][1];
+      if (rmw) {
+        if (cb + pc0 < n_valid) red_add_f64(dst + pc0, acc[mi * NJ + nj][0]);
+        if (cb + pc1 < n_valid) red_add_f64(dst + pc1, acc[mi * NJ + nj][1]);
+      } else {
+        if (cb + pc0 < n_valid) dst[pc0] = acc[mi * NJ + nj][0];
+        if (cb + pc1 < n_valid) dst[pc1] = acc[mi * NJ + nj][1];
+      }
     }
   }
 }
@@ -317,15 +310,15 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
     const int small = (kind <= kDfAdj && m_live <= 56) ? (m_live <= 8 ? 1 : m_live <= 16 ? 2 : m_live <= 32 ? 4 : 7) : 0;
     if (sq) {
       const int q = warp & 3, h = warp >> 2;
-      row0 = (q >> 1) * 56 + h * 32;
+      row0 = (q >> 1) * 56 + h * 24;
       col0 = (q & 1) * 56;
-      mi_n = h ? 3 : 4;
+      mi_n = 4;
       nj_n = 7;
       const int ra_q = row0 + row_perm(g), rb_q = col0 + row_perm(g);
       if (h == 0)
-        df_mainloop<4, 7>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
+        df_mainloop<4, 7, kBlkSqLo>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
       else
-        df_mainloop<3, 7>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
+        df_mainloop<4, 7, kBlkSqHi>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
     } else if (small == 0) {
       row0 = wm * kWarpM;
       col0 = wn * kWarpN;
@@ -358,8 +351,10 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
     const int rbase = it.tm * kBM + row0 + pg;
     const int cbase = it.tn * J.b_tile + col0;
     const bool rmw = kind == kDfSyrk;
-    if (sq)
-      df_store<4, 7>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
+    if (sq && (warp >> 2) == 0)
+      df_store<4, 7, kBlkSqLo>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
+    else if (sq)
+      df_store<4, 7, kBlkSqHi>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
     else if (small == 0)
       df_store<kMI, kNJ>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
     else

@@ -136,6 +136,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c_inner), "r"(c_outer)
       : "memory");
 }
+// *p += v at L2 without a return value.  Used where one launch (or one
+// dependency-ordered item) is the only writer of an element at a time, so
+// the order of the additions is fixed and the result deterministic; it
+// replaces a load -> add -> store chain that the compiler serialises per
+// element (the store may alias the next load).
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 // D = A(8x4, row) * B(4x8, col) + D on the FP64 tensor pipe (DMMA.8x8x4).
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -293,7 +301,12 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = h ? pc1 : pc0;
-        if (cb + c < p.b_rows_valid) dst[c] = (p.mode == kAccum ? dst[c] : 0.0) + acc[mi * NJ + nj][h];
+        if (cb + c < p.b_rows_valid) {
+          if (p.mode == kAccum)
+            red_add_f64(dst + c, acc[mi * NJ + nj][h]);
+          else
+            dst[c] = acc[mi * NJ + nj][h];
+        }
       }
     }
   }
