@@ -337,8 +337,8 @@ def run_b200(args):
         achieved = (fl / cnt) / (ms / cnt / 1e3) / 1e12
         traffic, tsrc = load_traffic()
         tr = None
-        if traffic and dom in traffic.get("per_launch_dram_bytes", {}):
-            tr = traffic["per_launch_dram_bytes"][dom]
+        per = traffic.get("per_launch_dram_bytes", {}) if traffic else {}
+        tr = per.get(f"{dom}@{args.config}")
         roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": tr,
                 "algorithmic_flops_per_launch": fl / cnt, "avg_launch_ms": ms / cnt,
