@@ -289,6 +289,7 @@ def run_b200(args):
         step()
     torch.cuda.synchronize()
     launches_per_step = net.last_launch_count
+    schedule = net.last_schedule  # auto: measured on the first evaluation (layer-by-layer graph or dataflow launch)
 
     with ClockSampler(local) as clk:
         if world > 1:
@@ -398,6 +399,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps),
+            "schedule": schedule,
             "clocks": clocks,
             "outputs_checked": ok,
             "kernel_breakdown": prof_summary,
