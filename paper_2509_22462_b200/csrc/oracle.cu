@@ -1654,6 +1654,22 @@ DfPlan& DeviceNet::dataflow_plan(int nb) {
     events.pop();
   }
 
+  // ---- self-check of the claim order (the kernel's deadlock freedom rests
+  // on it): every wait must be satisfiable by items claimed before the
+  // waiting one, and every counter must reach its largest target ----
+  {
+    std::vector<int> seen(static_cast<size_t>(nc), 0), total(static_cast<size_t>(nc), 0);
+    for (size_t i = 0; i < N; ++i) ++total[static_cast<size_t>(nodes[i].it.sig)];
+    for (size_t i = 0; i < N; ++i) {
+      const dev::DfItem& it = nodes[static_cast<size_t>(order[i])].it;
+      for (int k = 0; k < it.nwait; ++k)
+        if (seen[static_cast<size_t>(it.widx[k])] < it.wtgt[k])
+          throw StructuralError("dataflow: claim order violates a dependency (internal error)");
+      if (it.sig <= 0 || it.sig >= nc) throw StructuralError("dataflow: item without a valid signal counter");
+      ++seen[static_cast<size_t>(it.sig)];
+    }
+  }
+
   // ---- upload ----
   DfPlan plan;
   plan.nb = nb;
