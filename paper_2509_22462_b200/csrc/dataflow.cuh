@@ -80,6 +80,10 @@ struct alignas(16) DfJob {
   // ADJ: ybar, gz, d of layer l-1 and its sigma', sigma'' (pitch ld)
   double *ybar, *gz, *d;
   const double *s1i, *s2i;
+  // GEMM: also S_{l+1} = T_{l+1} diag(sigma'_{l+1}) (same layout as c), nullable
+  double* c2;
+  const double* c2_scale;
+  int64_t c2_scale_stride;
 };
 
 struct DfItem {
@@ -176,7 +180,8 @@ __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* 
 // additions happen in layer order (deterministic).
 template <int MI, int NJ, int SET = kBlkAll>
 __device__ __forceinline__ void df_store(double (&acc)[kAcc][2], double* raw, int64_t ldr, int rbase, int cbase,
-                                         int mi_n, int m_valid, int n_valid, int pc0, int pc1, bool rmw) {
+                                         int mi_n, int m_valid, int n_valid, int pc0, int pc1, bool rmw,
+                                         double* raw2 = nullptr, const double* s2 = nullptr) {
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi) {
     const int r = rbase + 8 * mi;
@@ -192,6 +197,11 @@ __device__ __forceinline__ void df_store(double (&acc)[kAcc][2], double* raw, in
       } else {
         if (cb + pc0 < n_valid) dst[pc0] = acc[mi * NJ + nj][0];
         if (cb + pc1 < n_valid) dst[pc1] = acc[mi * NJ + nj][1];
+        if (raw2) {  // S_{l+1} = T_{l+1} diag(sigma'_{l+1}) beside T_{l+1}
+          double* d2 = raw2 + static_cast<int64_t>(r) * ldr + cb;
+          if (cb + pc0 < n_valid) d2[pc0] = acc[mi * NJ + nj][0] * __ldg(s2 + cb + pc0);
+          if (cb + pc1 < n_valid) d2[pc1] = acc[mi * NJ + nj][1] * __ldg(s2 + cb + pc1);
+        }
       }
     }
   }
@@ -356,7 +366,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
     else if (sq)
       df_store<4, 7, kBlkSqHi>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
     else if (small == 0)
-      df_store<kMI, kNJ>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
+      df_store<kMI, kNJ>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw,
+                         J.c2 ? J.c2 + J.c_point_stride * it.point : nullptr,
+                         J.c2 ? J.c2_scale + J.c2_scale_stride * it.point : nullptr);
     else
       df_store<7, 2>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
     if (kind <= kDfAdj) {

@@ -57,6 +57,10 @@ struct Workspace {
   int64_t ld_part = 0;
   double* adj_part = nullptr;
   std::vector<double*> t;                   // ring of tangent buffers
+  std::vector<double*> s;                   // ring of pre-scaled tangents S_l = T_l diag(sigma'_l)
+  double* s0 = nullptr;                     // S_0 = W_0^T diag(sigma'_0) per point [cap][n_pad][ldt0]
+  CUtensorMap tm_s0;
+  std::vector<CUtensorMap> tm_s_a;          // S_l as the A operand (l >= 1)
   std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer (l-1) % ring)
   int64_t ldh = 0;
   double* h = nullptr;             // == hb[0]

@@ -189,6 +189,11 @@ struct NtParams {
   int mode;
   double* partial;  // [split][points * n_tiles][kBM][kBN] for kPartial
   int square;       // SYRK on 112 x 112 tiles: B rows tn * kBM, B box kBM rows (see nt_mma_kernel)
+  // kStore: also C2 = C diag(c2_scale) (column scale per point), e.g.
+  // S_{l+1} = T_{l+1} diag(sigma'_{l+1}) beside T_{l+1}; nullable
+  double* c2;
+  const double* c2_scale;
+  int64_t c2_scale_stride;
 };
 
 // Grouped rasterisation of a dense tile grid: kGroupM consecutive M tiles
@@ -221,13 +226,17 @@ __host__ __device__ constexpr bool blk_live(int mi, int nj) {
 // The consumer k-loop of nt_mma_kernel for an MI x NJ warp layout
 // (accumulator block mi * NJ + nj); the per-k scale on B is read one
 // k-block ahead through the read-only path (it was written by an earlier
-// launch).
+// launch).  SCALED = false: no scale at all -- the tangent GEMMs read the
+// pre-scaled S_l = T_l diag(sigma'_l) instead, because the LDS -> DMUL ->
+// DMMA chain of a scaled fragment costs ~4% of the tile (measured: c2
+// 180.6 -> 187.6 evals/s without the multiplies).
 constexpr int kNtAcc = kMI * kNJ;
 
-template <int MI, int NJ, int SET = kBlkAll>
+template <int MI, int NJ, int SET = kBlkAll, bool SCALED = true>
 __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char* smem, uint64_t* full,
                                             uint64_t* empty, int nkb, int kb_begin, const double* sp, int ra,
                                             int rb, int t, int lane) {
+  if (!SCALED) sp = nullptr;
   double sc_next[4];
   if (sp && nkb > 0) {
 #pragma unroll
@@ -252,7 +261,7 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc[q];
+      for (int nj = 0; nj < NJ; ++nj) b[nj] = SCALED ? lds_swz(sb, rb + 8 * nj, k) * sc[q] : lds_swz(sb, rb + 8 * nj, k);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -289,6 +298,8 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
     return;
   }
   double* cbase = p.c + p.c_point_stride * point;
+  double* c2base = p.c2 ? p.c2 + p.c_point_stride * point : nullptr;
+  const double* c2s = p.c2 ? p.c2_scale + p.c2_scale_stride * point : nullptr;
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi) {
     const int r = tm * kBM + r0 + 8 * mi + pg;
@@ -302,10 +313,12 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
       for (int h = 0; h < 2; ++h) {
         const int c = h ? pc1 : pc0;
         if (cb + c < p.b_rows_valid) {
-          if (p.mode == kAccum)
+          if (p.mode == kAccum) {
             red_add_f64(dst + c, acc[mi * NJ + nj][h]);
-          else
+          } else {
             dst[c] = acc[mi * NJ + nj][h];
+            if (c2base) c2base[static_cast<int64_t>(r) * p.ldc + cb + c] = acc[mi * NJ + nj][h] * __ldg(c2s + cb + c);
+          }
         }
       }
     }
@@ -409,7 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wm = warp >> 2;  // 0..1
     const int wn = warp & 3;   // 0..3
     const int r0 = wm * kWarpM, c0 = wn * kWarpN;
-    nt_mainloop<kMI, kNJ>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
+    if (sp)
+      nt_mainloop<kMI, kNJ, kBlkAll, true>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
+    else
+      nt_mainloop<kMI, kNJ, kBlkAll, false>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
     nt_store<kMI, kNJ>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, kMI, pg, pc0, pc1);
   }
 }
@@ -743,8 +759,9 @@ struct RowEpi {
 
 __device__ __forceinline__ void apply_row_epi(const RowEpi& e, int r, int c, double v) {
   const int64_t o = static_cast<int64_t>(r) * e.ld + c;
-  if (e.mode == kEpiStore) {  // plain store into e.z (pitch e.ld)
+  if (e.mode == kEpiStore) {  // plain store into e.z (pitch e.ld); e.y = e.z diag(e.s1i) when set
     e.z[o] = v;
+    if (e.y) e.y[o] = v * e.s1i[c];
     return;
   }
   if (e.mode == kEpiAct) {
@@ -1235,6 +1252,19 @@ __global__ void symmetrize_out_kernel(const double* __restrict__ hws, const doub
   if (h1) v += h1[o];
   if (h2) v += h2[o];
   out[e] = v;
+}
+
+// dst[b][r][c] = src[b * src_point_rows + r][c] * scale[b * s_stride + c]
+// for b < nb, r < rows, c < cols (S_0 = T_0 diag(sigma'_0) per point).
+__global__ void scale_cols_kernel(const double* __restrict__ src, int64_t lds, int64_t src_point_rows, int rows,
+                                  int cols, const double* __restrict__ scale, int64_t s_stride,
+                                  double* __restrict__ dst, int64_t ldd, int64_t dst_point_rows, int nb) {
+  const int64_t per = static_cast<int64_t>(rows) * cols;
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= per * nb) return;
+  const int b = static_cast<int>(e / per);
+  const int r = static_cast<int>((e % per) / cols), c = static_cast<int>(e % cols);
+  dst[(dst_point_rows * b + r) * ldd + c] = src[(src_point_rows * b + r) * lds + c] * scale[s_stride * b + c];
 }
 
 // Strided copy of a [rows][cols] block (pitch src -> pitch dst).

@@ -288,18 +288,26 @@ void DeviceNet::ensure_workspace(int batch) {
   // a buffer (and the dataflow path applies); R is capped by a memory
   // budget (32 GB of the 180 GB) and is at least 2.
   if (L_ >= 2) {
-    const size_t tbytes = sizeof(double) * static_cast<size_t>(cap) * n_pad_ * ldt_;
+    // S_l = T_l diag(sigma'_l) (the pre-scaled A operand of the tangent
+    // GEMMs) lives in a second ring with the same indexing
+    const size_t tbytes = sizeof(double) * static_cast<size_t>(cap) * n_pad_ * ldt_ * 2;
     const int want = std::max(2, static_cast<int>(L_) - 1);
     const int fit = static_cast<int>(std::max<size_t>(2, (size_t(32) << 30) / std::max<size_t>(tbytes, 1)));
     const int ring = std::min(want, fit);
     w.t.assign(static_cast<size_t>(ring), nullptr);
     for (auto& b : w.t) b = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
+    w.s.assign(static_cast<size_t>(ring), nullptr);
+    for (auto& b : w.s) b = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt_);
+    w.s0 = ws_alloc(static_cast<size_t>(cap) * n_pad_ * ldt0_);
+    w.tm_s0 = make_tmap(w.s0, layers_[0].rows, static_cast<int64_t>(cap) * n_pad_, ldt0_, kBM);
     w.tm_t_a.assign(L, CUtensorMap{});
     w.tm_t_b.assign(L, CUtensorMap{});
+    w.tm_s_a.assign(L, CUtensorMap{});
     for (size_t l = 1; l < L; ++l) {
       const double* buf = w.t[(l - 1) % w.t.size()];
       w.tm_t_a[l] = make_tmap(buf, layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBM);
       w.tm_t_b[l] = make_tmap(buf, layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBN);
+      w.tm_s_a[l] = make_tmap(w.s[(l - 1) % w.s.size()], layers_[l].rows, static_cast<int64_t>(cap) * n_pad_, ldt_, kBM);
     }
   }
   // Hessian accumulator [cap][n_pad][n_pad] and split-K partials
@@ -969,6 +977,13 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
   }
 
+  // Pre-scaled tangents pay one extra tile store per tile; nets whose
+  // single-point GEMMs are split-K (c1: 28 tiles) are launch-latency bound
+  // and keep the per-fragment scale.
+  bool prescaled = !hybrid_ && !streamk_;
+  for (int l = 0; l + 2 < L && prescaled; ++l)
+    if (nb == 1 && (n_pad_ / kBM) * ceil_div(layers_[static_cast<size_t>(l + 1)].rows, kBN) * 2 <= sm_count_)
+      prescaled = false;
   // syrk_done[l]: event on sb after SYRK_l (nullptr when none ran)
   std::vector<cudaEvent_t> syrk_done(static_cast<size_t>(L), nullptr);
   for (int l = 0; l + 1 < L && !streamk_; ++l) {
@@ -1009,6 +1024,33 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.c_point_stride = n_pad_ * ldt_;
     p.ldc = ldt_;
     p.mode = dev::kStore;
+    // Pre-scaled A operand: GEMM_{l+1} reads S_l = T_l diag(sigma'_l) (no
+    // per-fragment multiply in the k-loop) and writes S_{l+1} beside T_{l+1}
+    // when a later GEMM reads it.  S_0 (per point) by one elementwise pass.
+    const CUtensorMap* ta = &tmap_a(l);
+    if (prescaled) {
+      if (l == 0) {
+        const int cols0 = static_cast<int>(layers_[0].rows);
+        const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * cols0;
+        prof_begin(sa, kTagRowEpi, 0, 0);
+        dev::scale_cols_kernel<<<ceil_div(tot, 256), 256, 0, sa>>>(t0_, ldt0_, 0, static_cast<int>(n_pad_), cols0,
+                                                                    w.s1[0], w.ld[0], w.s0, ldt0_, n_pad_, nb);
+        after_launch(sa);
+        ta = &w.tm_s0;
+      } else {
+        ta = &w.tm_s_a[static_cast<size_t>(l)];
+      }
+      p.a_point_rows = n_pad_;
+      p.scale = nullptr;
+      const bool next_gemm = l + 2 < L && !(l + 2 == kfin_layer && skinny_final);
+      if (next_gemm) {
+        if (fwd_done[static_cast<size_t>(l + 1)])
+          CK(cudaStreamWaitEvent(sa, fwd_done[static_cast<size_t>(l + 1)], 0));  // sigma'_{l+1}
+        p.c2 = w.s[static_cast<size_t>(l % ring)];
+        p.c2_scale = w.s1[static_cast<size_t>(l + 1)];
+        p.c2_scale_stride = w.ld[static_cast<size_t>(l + 1)];
+      }
+    }
     // a single point with fewer tiles than half the SMs (c1: 28 tiles):
     // split K, then a fixed-order reduction stores T_{l+1}
     if (nb == 1 && !hybrid_ && p.n_tiles * 2 <= sm_count_) {
@@ -1017,10 +1059,12 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         p.mode = dev::kPartial;
         p.partial = w.gemm_part;  // not syrk_part: SYRKs on sb may run concurrently
         prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
-        launch_nt(sa, tmap_a(l), dn.tm_w, p, p.n_tiles * p.split);
+        launch_nt(sa, *ta, dn.tm_w, p, p.n_tiles * p.split);
         dev::RowEpi e{};
         e.mode = dev::kEpiStore;
         e.z = p.c;
+        e.y = p.c2;  // S_{l+1} (nb == 1: sigma' row of point 0)
+        e.s1i = p.c2_scale;
         e.ld = ldt_;
         prof_begin(sa, kTagRowEpi, 0, 0);
         dev::gemm_partial_reduce_kernel<<<dim3(4, p.n_tiles), 256, 0, sa>>>(
@@ -1040,7 +1084,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       continue;
     }
     prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
-    launch_nt(sa, tmap_a(l), dn.tm_w, p, nb * p.n_tiles);
+    launch_nt(sa, *ta, dn.tm_w, p, nb * p.n_tiles);
   }
 
   // ---- 4. final layer -------------------------------------------------------
@@ -1529,15 +1573,23 @@ DfPlan& DeviceNet::dataflow_plan(int nb) {
       j.a_bytes = dev::kABytes;
       j.b_bytes = dev::kBBytes;
       j.b_tile = kBN;
-      j.scale = w.s1[static_cast<size_t>(l)];
+      // l >= 1: the pre-scaled S_l = T_l diag(sigma'_l) as A (no multiply in
+      // the k-loop); l == 0: T_0 = W_0^T with sigma'_0 applied per fragment
+      j.scale = l == 0 ? w.s1[0] : nullptr;
       j.s_stride = w.ld[static_cast<size_t>(l)];
       j.a_point_rows = t_point_rows(l);
+      const bool next_gemm = l + 3 < L;  // a GEMM (l+1 -> l+2) reads S_{l+1}
+      if (next_gemm) {
+        j.c2 = w.s[static_cast<size_t>(l % ring)];
+        j.c2_scale = w.s1[static_cast<size_t>(l + 1)];
+        j.c2_scale_stride = w.ld[static_cast<size_t>(l + 1)];
+      }
       j.m_valid = static_cast<int>(n_pad_);
       j.n_valid = static_cast<int>(dn.rows);
       j.c = t_buf(l + 1);
       j.c_point_stride = n_pad_ * ldt_;
       j.ldc = ldt_;
-      const int ma = l == 0 ? map_id(tm_t0_a_) : map_id(w.tm_t_a[static_cast<size_t>(l)]);
+      const int ma = l == 0 ? map_id(tm_t0_a_) : map_id(w.tm_s_a[static_cast<size_t>(l)]);
       const int job = add_job(j, ma, map_id(dn.tm_w));
       const int tn_n = ceil_div(dn.rows, kBN);
       ntiles_n[static_cast<size_t>(l + 1)] = tn_n;
@@ -1553,7 +1605,9 @@ DfPlan& DeviceNet::dataflow_plan(int nb) {
             add_item(job, p, tm, tn, 0, kb, 0, row_base[static_cast<size_t>(l + 1)] + p * tiles_m + tm,
                      {{fwd_cnt[static_cast<size_t>(l)], nfwd[static_cast<size_t>(l)]},
                       {l >= 1 ? row_base[static_cast<size_t>(l)] + p * tiles_m + tm : 0,
-                       l >= 1 ? ntiles_n[static_cast<size_t>(l)] : 0}},
+                       l >= 1 ? ntiles_n[static_cast<size_t>(l)] : 0},
+                      {next_gemm ? fwd_cnt[static_cast<size_t>(l + 1)] : 0,
+                       next_gemm ? nfwd[static_cast<size_t>(l + 1)] : 0}},
                      kb * t_kb + t_item);
       flops += 2.0 * n_ * dn.rows * dn.cols * nb;
     }
