@@ -1256,14 +1256,13 @@ __global__ void symmetrize_out_kernel(const double* __restrict__ hws, const doub
 
 // dst[b][r][c] = src[b * src_point_rows + r][c] * scale[b * s_stride + c]
 // for b < nb, r < rows, c < cols (S_0 = T_0 diag(sigma'_0) per point).
+// Grid: x over columns, y = b * rows + r.
 __global__ void scale_cols_kernel(const double* __restrict__ src, int64_t lds, int64_t src_point_rows, int rows,
                                   int cols, const double* __restrict__ scale, int64_t s_stride,
                                   double* __restrict__ dst, int64_t ldd, int64_t dst_point_rows, int nb) {
-  const int64_t per = static_cast<int64_t>(rows) * cols;
-  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= per * nb) return;
-  const int b = static_cast<int>(e / per);
-  const int r = static_cast<int>((e % per) / cols), c = static_cast<int>(e % cols);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y / rows, r = blockIdx.y % rows;
+  if (c >= cols || b >= nb) return;
   dst[(dst_point_rows * b + r) * ldd + c] = src[(src_point_rows * b + r) * lds + c] * scale[s_stride * b + c];
 }
 

@@ -1029,19 +1029,26 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     // when a later GEMM reads it.  S_0 (per point) by one elementwise pass.
     const CUtensorMap* ta = &tmap_a(l);
     if (prescaled) {
-      if (l == 0) {
+      // S_0 (per point) costs one pass writing nb x n_pad x n_1 doubles; it
+      // pays for itself when the GEMM it feeds is wide: the saved multiply is
+      // ~4% of 2 nb n n_1 n_2 flops against 8 nb n n_1 bytes written, i.e.
+      // n_2 >~ 1400 (c2/c3: 5120 yes; c4/c5: 1024 no -- the first GEMM then
+      // keeps the per-fragment scale on the shared T_0).
+      const bool s0_pass = layers_[1].rows >= 2048;
+      if (l == 0 && s0_pass) {
         const int cols0 = static_cast<int>(layers_[0].rows);
-        const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * cols0;
         prof_begin(sa, kTagRowEpi, 0, 0);
-        dev::scale_cols_kernel<<<ceil_div(tot, 256), 256, 0, sa>>>(t0_, ldt0_, 0, static_cast<int>(n_pad_), cols0,
-                                                                    w.s1[0], w.ld[0], w.s0, ldt0_, n_pad_, nb);
+        dev::scale_cols_kernel<<<dim3(ceil_div(cols0, 256), static_cast<unsigned>(nb * n_pad_)), 256, 0, sa>>>(
+            t0_, ldt0_, 0, static_cast<int>(n_pad_), cols0, w.s1[0], w.ld[0], w.s0, ldt0_, n_pad_, nb);
         after_launch(sa);
         ta = &w.tm_s0;
-      } else {
+      } else if (l > 0) {
         ta = &w.tm_s_a[static_cast<size_t>(l)];
       }
-      p.a_point_rows = n_pad_;
-      p.scale = nullptr;
+      if (l > 0 || s0_pass) {
+        p.a_point_rows = n_pad_;
+        p.scale = nullptr;
+      }
       const bool next_gemm = l + 2 < L && !(l + 2 == kfin_layer && skinny_final);
       if (next_gemm) {
         if (fwd_done[static_cast<size_t>(l + 1)])
