@@ -143,9 +143,9 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // arrives in the stage (bulk copy by the producer).
 constexpr int kAcc = kMI * kNJ;  // 28 DMMA accumulator blocks per warp, in every layout
 
-template <int MI, int NJ, int SET = kBlkAll>
+template <int MI, int NJ, int SET = kBlkAll, bool SCALED = false>
 __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* smem, uint64_t* full,
-                                            uint64_t* empty, uint32_t& gk, int kb0, int kb1, bool scaled,
+                                            uint64_t* empty, uint32_t& gk, int kb0, int kb1,
                                             int ra, int rb, int t, int lane) {
   for (int kb = kb0; kb < kb1; ++kb, ++gk) {
     const int s = static_cast<int>(gk % kStages);
@@ -156,12 +156,15 @@ __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int k = 4 * q + t;
-      const double sc = scaled ? ss[k] : 1.0;
+      // the per-k scale (if any) goes on whichever operand has fewer fragments
+      constexpr bool kScaleA = SCALED && MI < NJ;
+      constexpr bool kScaleB = SCALED && !(MI < NJ);
+      const double sc = SCALED ? ss[k] : 1.0;
       double a[MI], b[NJ];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
+      for (int mi = 0; mi < MI; ++mi) a[mi] = kScaleA ? lds_swz(sa, ra + 8 * mi, k) * sc : lds_swz(sa, ra + 8 * mi, k);
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc;
+      for (int nj = 0; nj < NJ; ++nj) b[nj] = kScaleB ? lds_swz(sb, rb + 8 * nj, k) * sc : lds_swz(sb, rb + 8 * nj, k);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -326,15 +329,18 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
       nj_n = 7;
       const int ra_q = row0 + row_perm(g), rb_q = col0 + row_perm(g);
       if (h == 0)
-        df_mainloop<4, 7, kBlkSqLo>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
+        df_mainloop<4, 7, kBlkSqLo, true>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra_q, rb_q, t, lane);
       else
-        df_mainloop<4, 7, kBlkSqHi>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_q, rb_q, t, lane);
+        df_mainloop<4, 7, kBlkSqHi, true>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra_q, rb_q, t, lane);
     } else if (small == 0) {
       row0 = wm * kWarpM;
       col0 = wn * kWarpN;
       mi_n = kMI;
       nj_n = kNJ;
-      df_mainloop<kMI, kNJ>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra, rb, t, lane);
+      if (scaled)
+        df_mainloop<kMI, kNJ, kBlkAll, true>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra, rb, t, lane);
+      else
+        df_mainloop<kMI, kNJ, kBlkAll, false>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra, rb, t, lane);
     } else {
       row0 = 0;
       col0 = warp * 16;
@@ -342,13 +348,13 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
       nj_n = 2;
       const int ra_s = row_perm(g), rb_s = warp * 16 + row_perm(g);
       if (small == 1)
-        df_mainloop<1, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+        df_mainloop<1, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra_s, rb_s, t, lane);
       else if (small == 2)
-        df_mainloop<2, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+        df_mainloop<2, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra_s, rb_s, t, lane);
       else if (small == 4)
-        df_mainloop<4, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+        df_mainloop<4, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra_s, rb_s, t, lane);
       else
-        df_mainloop<7, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, scaled, ra_s, rb_s, t, lane);
+        df_mainloop<7, 2>(acc, smem, full, empty, gk, it.kb0, it.kb1, ra_s, rb_s, t, lane);
     }
 
     // ---- epilogue: block e = mi * nj_n + nj holds C[row0+8mi+pg][col0+8nj+pc0 / pc1] ----

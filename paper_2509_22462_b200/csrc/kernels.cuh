@@ -259,9 +259,13 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
       const int k = 4 * q + t;
       double a[MI], b[NJ];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
+      // the per-k scale goes on whichever operand has fewer fragments
+      constexpr bool kScaleA = SCALED && MI < NJ;
+      constexpr bool kScaleB = SCALED && !(MI < NJ);
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj) b[nj] = SCALED ? lds_swz(sb, rb + 8 * nj, k) * sc[q] : lds_swz(sb, rb + 8 * nj, k);
+      for (int mi = 0; mi < MI; ++mi) a[mi] = kScaleA ? lds_swz(sa, ra + 8 * mi, k) * sc[q] : lds_swz(sa, ra + 8 * mi, k);
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj) b[nj] = kScaleB ? lds_swz(sb, rb + 8 * nj, k) * sc[q] : lds_swz(sb, rb + 8 * nj, k);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
