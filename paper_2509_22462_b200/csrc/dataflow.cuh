@@ -146,12 +146,12 @@ constexpr int kAcc = kMI * kNJ;  // 28 DMMA accumulator blocks per warp, in ever
 template <int MI, int NJ, int SET = kBlkAll, bool SCALED = false>
 __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* smem, uint64_t* full,
                                             uint64_t* empty, uint32_t& gk, int kb0, int kb1,
-                                            int ra, int rb, int t, int lane) {
+                                            int ra, int rb, int t, int lane, int b_off = kABytes) {
   for (int kb = kb0; kb < kb1; ++kb, ++gk) {
     const int s = static_cast<int>(gk % kStages);
     mbar_wait(&full[s], (gk / kStages) & 1);
     const char* sa = smem + s * kDfStageBytes;
-    const char* sb = sa + kABytes;
+    const char* sb = sa + b_off;
     const double* ss = reinterpret_cast<const double*>(sa + kDfScaleOff);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -274,13 +274,15 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
         const int b_row0 = static_cast<int>(J.b_point_rows * it.point) + it.tn * J.b_tile;
         // the scale vector has >= 16 * k_blocks entries (zero padded)
         const double* sp = J.scale ? J.scale + J.s_stride * it.point : nullptr;
+        // diagonal square SYRK tile: B == A, one box per stage
+        const bool diag = J.kind == kDfSyrk && J.b_tile == kBM && it.tm == it.tn;
         for (int kb = it.kb0; kb < it.kb1; ++kb, ++gk) {
           const int s = static_cast<int>(gk % kStages);
           if (gk >= kStages) mbar_wait(&empty[s], ((gk / kStages) - 1) & 1);
           char* sa = smem + s * kDfStageBytes;
-          mbar_arrive_expect_tx(&full[s], J.a_bytes + J.b_bytes + (sp ? kBK * 8 : 0));
+          mbar_arrive_expect_tx(&full[s], J.a_bytes + (diag ? 0 : J.b_bytes) + (sp ? kBK * 8 : 0));
           tma_load_2d(sa, &P.maps[J.ta], &full[s], kb * kBK, a_row0);
-          tma_load_2d(sa + kABytes, &P.maps[J.tb], &full[s], kb * kBK, b_row0);
+          if (!diag) tma_load_2d(sa + kABytes, &P.maps[J.tb], &full[s], kb * kBK, b_row0);
           if (sp) bulk_load(sa + kDfScaleOff, sp + kb * kBK, kBK * 8, &full[s]);
         }
       }
@@ -321,7 +323,30 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
     const int sq = kind == kDfSyrk && J.b_tile == kBM;
     // point-row tiles (FWD / ADJ) with few points use the column-split warp layout
     const int small = (kind <= kDfAdj && m_live <= 56) ? (m_live <= 8 ? 1 : m_live <= 16 ? 2 : m_live <= 32 ? 4 : 7) : 0;
-    if (sq) {
+    const bool diag = sq && it.tm == it.tn;
+    if (diag) {
+      row0 = 8 * diag_r0(warp);
+      col0 = 0;
+      mi_n = diag_r1(warp) - diag_r0(warp);
+      nj_n = diag_r1(warp);
+#define GBB_DF_DIAG(W)                                                                                    \
+  case W:                                                                                                 \
+    df_mainloop<diag_r1(W) - diag_r0(W), diag_r1(W), kBlkLower + diag_r0(W), true>(                        \
+        acc, smem, full, empty, gk, it.kb0, it.kb1, 8 * diag_r0(W) + row_perm(g), row_perm(g), t, lane, 0); \
+    break;
+      switch (warp) {
+        GBB_DF_DIAG(0)
+        GBB_DF_DIAG(1)
+        GBB_DF_DIAG(2)
+        GBB_DF_DIAG(3)
+        GBB_DF_DIAG(4)
+        GBB_DF_DIAG(5)
+        GBB_DF_DIAG(6)
+        GBB_DF_DIAG(7)
+        default: break;
+      }
+#undef GBB_DF_DIAG
+    } else if (sq) {
       const int q = warp & 3, h = warp >> 2;
       row0 = (q >> 1) * 56 + h * 24;
       col0 = (q & 1) * 56;
@@ -367,7 +392,26 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
     const int rbase = it.tm * kBM + row0 + pg;
     const int cbase = it.tn * J.b_tile + col0;
     const bool rmw = kind == kDfSyrk;
-    if (sq && (warp >> 2) == 0)
+    if (diag) {
+#define GBB_DF_DIAG_ST(W)                                                                                 \
+  case W:                                                                                                 \
+    df_store<diag_r1(W) - diag_r0(W), diag_r1(W), kBlkLower + diag_r0(W)>(acc, raw, ldr, rbase, cbase,      \
+                                                                          mi_n, J.m_valid, J.n_valid, pc0, \
+                                                                          pc1, rmw);                       \
+    break;
+      switch (warp) {
+        GBB_DF_DIAG_ST(0)
+        GBB_DF_DIAG_ST(1)
+        GBB_DF_DIAG_ST(2)
+        GBB_DF_DIAG_ST(3)
+        GBB_DF_DIAG_ST(4)
+        GBB_DF_DIAG_ST(5)
+        GBB_DF_DIAG_ST(6)
+        GBB_DF_DIAG_ST(7)
+        default: break;
+      }
+#undef GBB_DF_DIAG_ST
+    } else if (sq && (warp >> 2) == 0)
       df_store<4, 7, kBlkSqLo>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
     else if (sq)
       df_store<4, 7, kBlkSqHi>(acc, raw, ldr, rbase, cbase, mi_n, J.m_valid, J.n_valid, pc0, pc1, rmw);
