@@ -283,9 +283,7 @@ gbopt_status gbopt_net_forward(const gbopt_net* net, const double* x, size_t n, 
   if (!dims_ok(net, n, m))
     return fail_argument("gbopt_net_forward: buffer lengths do not match the network dimensions");
   return guarded([&] {
-    std::vector<double> tmp(m);
-    net->net->device().evaluate_host(1, x, nullptr, tmp.data(), nullptr, nullptr, nullptr);
-    std::memcpy(y, tmp.data(), sizeof(double) * m);
+    net->net->device().evaluate_host(1, x, nullptr, y, nullptr, nullptr, nullptr);
   });
 }
 
@@ -296,9 +294,7 @@ gbopt_status gbopt_net_jacobian(const gbopt_net* net, const double* x, size_t n,
   if (static_cast<int64_t>(n) != net->net->input_dim() || static_cast<int64_t>(jac_len) != m * static_cast<int64_t>(n))
     return fail_argument("gbopt_net_jacobian: buffer lengths do not match the network dimensions");
   return guarded([&] {
-    std::vector<double> tmp(jac_len);
-    net->net->device().evaluate_host(1, x, nullptr, nullptr, tmp.data(), nullptr, nullptr);
-    std::memcpy(jac, tmp.data(), sizeof(double) * jac_len);
+    net->net->device().evaluate_host(1, x, nullptr, nullptr, jac, nullptr, nullptr);
   });
 }
 
@@ -309,9 +305,7 @@ gbopt_status gbopt_net_lagrangian_gradient(const gbopt_net* net, const double* x
   if (!dims_ok(net, n, m) || g_len != n)
     return fail_argument("gbopt_net_lagrangian_gradient: buffer lengths do not match the network dimensions");
   return guarded([&] {
-    std::vector<double> tmp(n);
-    net->net->device().evaluate_host(1, x, lambda, nullptr, nullptr, nullptr, tmp.data());
-    std::memcpy(g, tmp.data(), sizeof(double) * n);
+    net->net->device().evaluate_host(1, x, lambda, nullptr, nullptr, nullptr, g);
   });
 }
 
@@ -322,9 +316,7 @@ gbopt_status gbopt_net_lagrangian_hessian(const gbopt_net* net, const double* x,
   if (!dims_ok(net, n, m) || hess_len != n * n)
     return fail_argument("gbopt_net_lagrangian_hessian: buffer lengths do not match the network dimensions");
   return guarded([&] {
-    std::vector<double> tmp(hess_len);
-    net->net->device().evaluate_host(1, x, lambda, nullptr, nullptr, tmp.data(), nullptr);
-    std::memcpy(hess, tmp.data(), sizeof(double) * hess_len);
+    net->net->device().evaluate_host(1, x, lambda, nullptr, nullptr, hess, nullptr);
   });
 }
 

@@ -224,6 +224,8 @@ class DeviceNet {
   std::vector<void*> ws_allocs_;
   std::map<GraphKey, GraphEntry> graphs_;
   int64_t launches_ = 0, last_launches_ = 0;
+  double* stage_ = nullptr;  // pinned staging for results bound for pageable host buffers
+  size_t stage_cap_ = 0;
   bool last_dataflow_ = false;
 };
 

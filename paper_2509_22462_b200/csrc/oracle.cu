@@ -198,6 +198,7 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
 DeviceNet::~DeviceNet() {
   DeviceGuard g(ordinal_);
   free_workspace();
+  if (stage_) cudaFreeHost(stage_);
   for (auto& d : layers_) {
     cudaFree(d.w);
     cudaFree(d.b);
@@ -1247,11 +1248,48 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
     CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam, sizeof(double) * m_, sizeof(double) * m_, nb,
                          cudaMemcpyHostToDevice, stream_));
   run(stream_, nb, o);
-  if (y) CK(cudaMemcpyAsync(y, w.y_out, sizeof(double) * nb * m_, cudaMemcpyDeviceToHost, stream_));
-  if (jac) CK(cudaMemcpyAsync(jac, w.j_out, sizeof(double) * nb * m_ * n_, cudaMemcpyDeviceToHost, stream_));
-  if (hess) CK(cudaMemcpyAsync(hess, w.h_out, sizeof(double) * nb * n_ * n_, cudaMemcpyDeviceToHost, stream_));
-  if (grad) CK(cudaMemcpyAsync(grad, w.g_out, sizeof(double) * nb * n_, cudaMemcpyDeviceToHost, stream_));
+  // Results go to pinned caller buffers directly; pageable ones through a
+  // pinned staging area (a pageable D2H runs at a fraction of the PCIe rate)
+  // and are written only after the evaluation has completed.
+  struct Out {
+    double* dst;
+    const double* src;
+    size_t n;
+  };
+  const Out outs[4] = {{y, w.y_out, static_cast<size_t>(nb) * m_},
+                       {jac, w.j_out, static_cast<size_t>(nb) * m_ * n_},
+                       {hess, w.h_out, static_cast<size_t>(nb) * n_ * n_},
+                       {grad, w.g_out, static_cast<size_t>(nb) * n_}};
+  size_t staged = 0;
+  bool pinned[4] = {false, false, false, false};
+  for (int i = 0; i < 4; ++i) {
+    if (!outs[i].dst) continue;
+    cudaPointerAttributes a;
+    pinned[i] = cudaPointerGetAttributes(&a, outs[i].dst) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (!pinned[i]) staged += outs[i].n;
+  }
+  if (staged > stage_cap_) {
+    if (stage_) cudaFreeHost(stage_);
+    stage_ = nullptr;
+    stage_cap_ = 0;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_), sizeof(double) * staged, cudaHostAllocDefault));
+    stage_cap_ = staged;
+  }
+  size_t off = 0;
+  for (int i = 0; i < 4; ++i) {
+    if (!outs[i].dst) continue;
+    double* d = pinned[i] ? outs[i].dst : stage_ + off;
+    CK(cudaMemcpyAsync(d, outs[i].src, sizeof(double) * outs[i].n, cudaMemcpyDeviceToHost, stream_));
+    if (!pinned[i]) off += outs[i].n;
+  }
   CK(cudaStreamSynchronize(stream_));
+  off = 0;
+  for (int i = 0; i < 4; ++i) {
+    if (!outs[i].dst || pinned[i]) continue;
+    std::memcpy(outs[i].dst, stage_ + off, sizeof(double) * outs[i].n);
+    off += outs[i].n;
+  }
 }
 
 // Device-buffer entry: ordered after / before `user` stream, no host sync.
