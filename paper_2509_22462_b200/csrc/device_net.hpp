@@ -63,11 +63,7 @@ struct Workspace {
   std::vector<CUtensorMap> tm_s_a;          // S_l as the A operand (l >= 1)
   std::vector<CUtensorMap> tm_t_a, tm_t_b;  // per layer l >= 1 (buffer (l-1) % ring)
   int64_t ldh = 0;
-  double* h = nullptr;             // == hb[0]
-  std::vector<double*> hb;         // H accumulators (one per SYRK job of a stream-K launch)
-  double* sk_slots[2] = {nullptr, nullptr};  // stream-K pieces [2 * #SMs][kBM * kBN], per stream
-  int* sk_counters[2] = {nullptr, nullptr};  // per-tile arrival counters (self-resetting), per stream
-  int sk_counter_cap = 0;
+  double* h = nullptr;             // H accumulator [cap][n_pad][n_pad], lower triangle
   double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs; side stream)
   double* gemm_part = nullptr;  // split-K partials of single-point tangent GEMMs (main stream)
   CUtensorMap tm_x;                   // x as an A operand [cap][n]
@@ -158,11 +154,6 @@ class DeviceNet {
   void batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const DevLayer& d, bool transposed,
                   const void* epi, double* store);
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);
-  // One job of a persistent stream-K launch (nt_mma_sk_kernel); oracle.cu.
-  struct SkJobDesc;
-  void launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs, bool hybrid = true);
-  bool streamk_ = true;   // layer steps: GEMM_{l+1} + SYRKs in one launch
-  bool hybrid_ = false;   // two-stream schedule with hybrid DP/stream-K launches
   void enqueue(cudaStream_t st, int nb, const Outputs& o);
   // Persistent dataflow path (y, J, H at small batch): oracle.cu.
   bool dataflow_ok(int nb, const Outputs& o) const;

@@ -150,6 +150,9 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
+// Named barrier over the consumer warps only (the producer warp may have exited).
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32)); }
+
 // Element (r, k) of a 128B-swizzled [rows][16 doubles] TMA box (TMA's
 // SWIZZLE_128B: 16-byte chunk index XOR (row & 7)).  `base` must point into
 // shared memory via the __shared__ array so the compiler emits LDS.
@@ -275,7 +278,6 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
     for (int q = 0; q < 4; ++q) {
       const int k = 4 * q + t;
       double a[MI], b[NJ];
-#pragma unroll
       // the per-k scale goes on whichever operand has fewer fragments
       constexpr bool kScaleA = SCALED && MI < NJ;
       constexpr bool kScaleB = SCALED && !(MI < NJ);
@@ -473,292 +475,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     else
       nt_mainloop<kMI, kNJ, kBlkAll, false>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
     nt_store<kMI, kNJ>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, kMI, pg, pc0, pc1);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent stream-K NT MMA over up to kSkJobs jobs -- one "layer step":
-// the tangent GEMM_{l+1} and the SYRK(s) of earlier layers in ONE launch.
-// The jobs' (tile, k-block) iterations are linearised and cut into
-// gridDim.x (= #SMs) equal contiguous ranges, one per CTA, so there is no
-// wave quantisation and the SYRK tiles fill what the GEMM leaves.  A tile
-// whose k range is cut between CTAs is finished by the last CTA to arrive
-// (per-tile counter): every piece goes to a per-CTA slot and the last
-// arriver sums the slots in k order -- deterministic for a given shape and
-// grid -- then applies the job's epilogue.  No CTA ever waits on another.
-// ---------------------------------------------------------------------------
-constexpr int kSkJobs = 3;
-
-struct alignas(64) SkJob {
-  CUtensorMap tmA, tmB;  // per-job TMA views (A rows x K, B rows x K)
-  NtParams p;            // mode kStore (GEMM) or kAccum (SYRK); split unused
-  int tiles;             // points * tiles per point
-  int tile0;             // first global tile index of the job (counters)
-  int64_t iter0;         // first global iteration of the job
-};
-
-struct SkParams {
-  SkJob job[kSkJobs];
-  int n_jobs;
-  int64_t iters;   // total iterations (sum of tiles * k_blocks)
-  // Hybrid schedule: the first dp_waves * gridDim.x tiles of job 0 run
-  // data-parallel (CTA c takes tiles c, c + grid, ...: whole tiles, the
-  // grouped raster's L2 reuse intact); the iterations from sk0 on are cut
-  // stream-K.  The host keeps (iters - sk0) == 0 or >= gridDim.x so every
-  // CTA's stream-K range is non-empty.
-  int dp_waves;
-  int64_t sk0;
-  double* slots;   // [2 * gridDim.x][kBM * kBN] pieces of split tiles
-  int* counters;   // [total tiles]; zero on entry, reset to zero on exit
-};
-
-// First stream-K iteration of CTA `cta`.
-__device__ __forceinline__ int64_t sk_begin(const SkParams& P, int cta, int grid) {
-  return P.sk0 + ((P.iters - P.sk0) * cta) / grid;
-}
-// CTA whose stream-K range contains global iteration `it` (>= sk0).
-__device__ __forceinline__ int sk_cta_of(const SkParams& P, int grid, int64_t it) {
-  int c = static_cast<int>(((it - P.sk0) * grid) / (P.iters - P.sk0));
-  while (c + 1 < grid && sk_begin(P, c + 1, grid) <= it) ++c;
-  while (c > 0 && sk_begin(P, c, grid) > it) --c;
-  return c;
-}
-
-struct SkSeg {
-  int job, tile, kb0, nkb;
-  int64_t tile_it0, tile_it1;  // global iteration range of the whole tile
-};
-
-__device__ __forceinline__ SkSeg sk_segment(const SkParams& P, int64_t it, int64_t end) {
-  int j = 0;
-  while (j + 1 < P.n_jobs && it >= P.job[j + 1].iter0) ++j;
-  const SkJob& J = P.job[j];
-  const int kb = J.p.k_blocks;
-  const int64_t local = it - J.iter0;
-  SkSeg s;
-  s.job = j;
-  s.tile = static_cast<int>(local / kb);
-  s.kb0 = static_cast<int>(local % kb);
-  s.tile_it0 = J.iter0 + static_cast<int64_t>(s.tile) * kb;
-  s.tile_it1 = s.tile_it0 + kb;
-  s.nkb = static_cast<int>((end < s.tile_it1 ? end : s.tile_it1) - it);
-  return s;
-}
-
-__device__ __forceinline__ void sk_tile_coords(const NtParams& p, int tile, int& point, int& tm, int& tn) {
-  if (p.tiles != nullptr) {
-    point = tile / p.n_tiles;
-    const int2 t = p.tiles[tile % p.n_tiles];
-    tm = t.x;
-    tn = t.y;
-  } else {
-    const int per_point = p.tiles_m * p.tiles_n;
-    point = tile / per_point;
-    decode_dense_tile(tile % per_point, p.tiles_m, p.tiles_n, tm, tn);
-  }
-}
-
-// Store or accumulate one warp's fragment of a finished tile (see the
-// nt_mma_kernel epilogue for the permuted fragment layout).
-__device__ __forceinline__ void sk_epilogue(const NtParams& p, int point, int tm, int tn,
-                                            const double (&acc)[kMI][kNJ][2], int wm, int wn, int pg, int pc0,
-                                            int pc1) {
-  double* cbase = p.c + p.c_point_stride * point;
-#pragma unroll
-  for (int mi = 0; mi < kMI; ++mi) {
-    const int r = tm * kBM + wm * kWarpM + 8 * mi + pg;
-    if (r >= p.m_rows_valid) continue;
-#pragma unroll
-    for (int nj = 0; nj < kNJ; ++nj) {
-      const int cb = tn * kBN + wn * kWarpN + 8 * nj;
-      double* dst = cbase + static_cast<int64_t>(r) * p.ldc + cb;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = h ? pc1 : pc0;
-        if (cb + c < p.b_rows_valid) dst[c] = (p.mode == kAccum ? dst[c] : 0.0) + acc[mi][nj][h];
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32)); }
-
-__global__ void __launch_bounds__(kThreads, 1) nt_mma_sk_kernel(const __grid_constant__ SkParams P) {
-  extern __shared__ unsigned char smem_raw[];
-  char* smem = reinterpret_cast<char*>(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  __shared__ int s_last;
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int cta = blockIdx.x, grid = gridDim.x;
-  const int64_t skb = sk_begin(P, cta, grid);
-  const int64_t ske = sk_begin(P, cta + 1, grid);
-  const int64_t kb_dp = P.job[0].p.k_blocks;
-  // work range w: the w-th data-parallel tile of this CTA, then (w ==
-  // dp_waves) its stream-K slice
-  auto range_of = [&](int w, int64_t& r_beg, int64_t& r_end) {
-    if (w < P.dp_waves) {
-      r_beg = (static_cast<int64_t>(w) * grid + cta) * kb_dp;
-      r_end = r_beg + kb_dp;
-    } else {
-      r_beg = skb;
-      r_end = ske;
-    }
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  if (warp == kConsumerWarps) {
-    // ===== producer: walks the same segments, one TMA stage per k-block =====
-    if (lane == 0) {
-      for (int j = 0; j < P.n_jobs; ++j) {
-        tma_prefetch_desc(&P.job[j].tmA);
-        tma_prefetch_desc(&P.job[j].tmB);
-      }
-      int64_t gk = 0;  // k-blocks issued by this CTA (ring position)
-      for (int w = 0; w <= P.dp_waves; ++w) {
-      int64_t r_beg, r_end;
-      range_of(w, r_beg, r_end);
-      for (int64_t it = r_beg; it < r_end;) {
-        const SkSeg sg = sk_segment(P, it, r_end);
-        const SkJob& J = P.job[sg.job];
-        int point, tm, tn;
-        sk_tile_coords(J.p, sg.tile, point, tm, tn);
-        const int a_row0 = static_cast<int>(J.p.a_point_rows * point) + tm * kBM;
-        const int b_row0 = static_cast<int>(J.p.b_point_rows * point) + tn * kBN;
-        for (int i = 0; i < sg.nkb; ++i, ++gk) {
-          const int s = static_cast<int>(gk % kStages);
-          if (gk >= kStages) mbar_wait(&empty[s], static_cast<uint32_t>(((gk / kStages) - 1) & 1));
-          char* sa = smem + s * kStageBytes;
-          mbar_arrive_expect_tx(&full[s], kStageBytes);
-          const int kc = (sg.kb0 + i) * kBK;
-          tma_load_2d(sa, &J.tmA, &full[s], kc, a_row0);
-          tma_load_2d(sa + kABytes, &J.tmB, &full[s], kc, b_row0);
-        }
-        it += sg.nkb;
-      }
-      }
-    }
-    return;
-  }
-
-  // ===== consumers =====
-  const int wm = warp >> 2, wn = warp & 3;
-  const int g = lane >> 2, t = lane & 3;
-  const int ra = wm * kWarpM + row_perm(g);
-  const int rb = wn * kWarpN + row_perm(g);
-  const int pg = row_perm(g), pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
-  int64_t gk = 0;
-  for (int w = 0; w <= P.dp_waves; ++w) {
-  int64_t r_beg, r_end;  // (not rb: that is the B-fragment row base)
-  range_of(w, r_beg, r_end);
-  for (int64_t it = r_beg; it < r_end;) {
-    const SkSeg sg = sk_segment(P, it, r_end);
-    const NtParams& p = P.job[sg.job].p;
-    int point, tm, tn;
-    sk_tile_coords(p, sg.tile, point, tm, tn);
-    const double* sp = p.scale ? p.scale + p.s_stride * point : nullptr;
-    double acc[kMI][kNJ][2];
-#pragma unroll
-    for (int i = 0; i < kMI; ++i)
-#pragma unroll
-      for (int j = 0; j < kNJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    double sc_next[4];
-    if (sp) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sc_next[q] = __ldg(sp + sg.kb0 * kBK + 4 * q + t);
-    }
-    for (int i = 0; i < sg.nkb; ++i, ++gk) {
-      const int s = static_cast<int>(gk % kStages);
-      double sc[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sc[q] = sp ? sc_next[q] : 1.0;
-      if (sp && i + 1 < sg.nkb) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sc_next[q] = __ldg(sp + (sg.kb0 + i + 1) * kBK + 4 * q + t);
-      }
-      mbar_wait(&full[s], static_cast<uint32_t>((gk / kStages) & 1));
-      const char* sa = smem + s * kStageBytes;
-      const char* sb = sa + kABytes;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = 4 * q + t;
-        double a[kMI], b[kNJ];
-#pragma unroll
-        for (int mi = 0; mi < kMI; ++mi) a[mi] = lds_swz(sa, ra + 8 * mi, k);
-#pragma unroll
-        for (int nj = 0; nj < kNJ; ++nj) b[nj] = lds_swz(sb, rb + 8 * nj, k) * sc[q];
-#pragma unroll
-        for (int mi = 0; mi < kMI; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < kNJ; ++nj) dmma884(acc[mi][nj], a[mi], b[nj]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-
-    const bool whole = it == sg.tile_it0 && it + sg.nkb == sg.tile_it1;
-    if (whole) {
-      sk_epilogue(p, point, tm, tn, acc, wm, wn, pg, pc0, pc1);
-    } else {
-      // piece of a split tile: slot 2*cta (first segment of this CTA's range)
-      // or 2*cta+1 (last segment)
-      const int my_slot = 2 * cta + (it == skb ? 0 : 1);
-      double* out = P.slots + static_cast<int64_t>(my_slot) * kBM * kBN;
-#pragma unroll
-      for (int mi = 0; mi < kMI; ++mi)
-#pragma unroll
-        for (int nj = 0; nj < kNJ; ++nj) {
-          const int r = wm * kWarpM + 8 * mi + pg;
-          const int cb = wn * kWarpN + 8 * nj;
-          out[r * kBN + cb + pc0] = acc[mi][nj][0];
-          out[r * kBN + cb + pc1] = acc[mi][nj][1];
-        }
-      __threadfence();
-      consumer_bar();
-      const int c0 = sk_cta_of(P, grid, sg.tile_it0);
-      const int c1 = sk_cta_of(P, grid, sg.tile_it1 - 1);
-      int* cnt = P.counters + P.job[sg.job].tile0 + sg.tile;
-      if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1) == c1 - c0);
-      consumer_bar();
-      if (s_last) {
-        __threadfence();
-        // sum the pieces in k order (deterministic), then the epilogue
-#pragma unroll
-        for (int mi = 0; mi < kMI; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < kNJ; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-        for (int c = c0; c <= c1; ++c) {
-          // the piece of CTA c: its first segment (slot 2c) unless its range
-          // began before this tile (then the tile is its last segment)
-          const int slot = 2 * c + (sk_begin(P, c, grid) < sg.tile_it0 ? 1 : 0);
-          const double* in = P.slots + static_cast<int64_t>(slot) * kBM * kBN;
-#pragma unroll
-          for (int mi = 0; mi < kMI; ++mi)
-#pragma unroll
-            for (int nj = 0; nj < kNJ; ++nj) {
-              const int r = wm * kWarpM + 8 * mi + pg;
-              const int cb = wn * kWarpN + 8 * nj;
-              acc[mi][nj][0] += __ldcg(in + r * kBN + cb + pc0);
-              acc[mi][nj][1] += __ldcg(in + r * kBN + cb + pc1);
-            }
-        }
-        sk_epilogue(p, point, tm, tn, acc, wm, wn, pg, pc0, pc1);
-        if (threadIdx.x == 0) *cnt = 0;
-      }
-      consumer_bar();  // slots of this CTA may be rewritten only after this
-    }
-    it += sg.nkb;
-  }
   }
 }
 

@@ -106,19 +106,16 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   if (prop.major != 10) throw DeviceError(std::string("gbopt_b200 needs an sm_100 (B200) device, found ") + prop.name);
   sm_count_ = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
-  CK(cudaFuncSetAttribute(dev::nt_mma_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDfSmemBytes));
   if (const char* e = std::getenv("GBOPT_DATAFLOW")) dataflow_mode_ = e[0] == '0' ? 0 : 1;
   if (const char* e = std::getenv("GBOPT_DF_GROUP")) df_group_ = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("GBOPT_DF_SQ")) df_square_ = e[0] != '0';
   // (A maximal shared-memory carveout, tried so GEMV CTAs could co-reside with
-  // nt_mma, cost 2% on c2 -- 173.4 vs 177.3 evals/s -- and is not set.)
-  // Persistent stream-K layer steps (experimental, GBOPT_STREAMK=1): balanced
-  // but it loses the grouped raster's L2 reuse of W and starves the side
-  // stream; the default two-stream data-parallel schedule is faster on c2/c5
-  // (profiles/r01_notes.md).
-  streamk_ = std::getenv("GBOPT_STREAMK") != nullptr;
-  hybrid_ = std::getenv("GBOPT_HYBRID") != nullptr;
+  // nt_mma, cost 2% on c2 -- 173.4 vs 177.3 evals/s -- and is not set.  A
+  // persistent stream-K schedule of the layer steps was also built and
+  // measured slower -- 139-158 vs 177 evals/s on c2, profiles/r01_notes.md --
+  // and was removed; the dataflow launch (dataflow.cuh) is the persistent
+  // schedule.)
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   // Which stream gets the SMs first.  A layer's SYRK costs (n+1)/(2 n_{l-1})
@@ -192,7 +189,6 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaMalloc(&sq_tiles_, sizeof(int2) * sq.size()));
   CK(cudaMemcpy(sq_tiles_, sq.data(), sizeof(int2) * sq.size(), cudaMemcpyHostToDevice));
   if (const char* e = std::getenv("GBOPT_SQ")) square_syrk_ = e[0] != '0';
-  if (streamk_ || hybrid_) square_syrk_ = false;  // the stream-K kernel has only 112 x 128 tiles
 }
 
 DeviceNet::~DeviceNet() {
@@ -313,20 +309,7 @@ void DeviceNet::ensure_workspace(int batch) {
   }
   // Hessian accumulator [cap][n_pad][n_pad] and split-K partials
   w.ldh = n_pad_;
-  w.hb.assign(dev::kSkJobs, nullptr);
-  for (auto& b : w.hb) b = ws_alloc(static_cast<size_t>(cap) * n_pad_ * n_pad_);
-  w.h = w.hb[0];
-  // stream-K: two piece slots per CTA; one counter per tile of a launch
-  // (GEMM tiles of the widest layer + kSkJobs SYRK jobs)
-  for (int s = 0; s < 2; ++s) w.sk_slots[s] = ws_alloc(static_cast<size_t>(2) * sm_count_ * kBM * kBN);
-  {
-    int64_t wn = 1;
-    for (auto& d : layers_) wn = std::max(wn, d.rows);
-    const int64_t gemm_tiles = static_cast<int64_t>(cap) * (n_pad_ / kBM) * ceil_div(wn, kBN);
-    w.sk_counter_cap = static_cast<int>(gemm_tiles + static_cast<int64_t>(dev::kSkJobs) * cap * n_syrk_tiles_);
-    for (int s = 0; s < 2; ++s)
-      w.sk_counters[s] = reinterpret_cast<int*>(ws_alloc((static_cast<size_t>(w.sk_counter_cap) + 1) / 2));
-  }
+  w.h = ws_alloc(static_cast<size_t>(cap) * n_pad_ * n_pad_);
   // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
   w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, std::max(n_syrk_tiles_, n_sq_tiles_))) * kBM * kBN);
   w.gemm_part = ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN);
@@ -421,60 +404,6 @@ void DeviceNet::batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const
 // --------------------------------------------------------------------------
 // Launch helpers
 // --------------------------------------------------------------------------
-struct DeviceNet::SkJobDesc {
-  const CUtensorMap* ta = nullptr;
-  const CUtensorMap* tb = nullptr;
-  dev::NtParams p{};
-  int tiles = 0;
-  double flops = 0;
-};
-
-// One persistent stream-K launch over up to kSkJobs jobs: grid = #SMs (or
-// the iteration count if smaller), each CTA one contiguous slice of the
-// jobs' (tile, k-block) iterations.
-void DeviceNet::launch_sk(cudaStream_t st, const std::vector<SkJobDesc>& jobs, bool hybrid) {
-  if (jobs.empty()) return;
-  if (static_cast<int>(jobs.size()) > dev::kSkJobs) throw StructuralError("launch_sk: too many jobs");
-  dev::SkParams P;
-  std::memset(&P, 0, sizeof(P));
-  int64_t iters = 0;
-  int tiles = 0;
-  double flops = 0;
-  for (size_t i = 0; i < jobs.size(); ++i) {
-    dev::SkJob& J = P.job[i];
-    J.tmA = *jobs[i].ta;
-    J.tmB = *jobs[i].tb;
-    J.p = jobs[i].p;
-    J.tiles = jobs[i].tiles;
-    J.tile0 = tiles;
-    J.iter0 = iters;
-    iters += static_cast<int64_t>(jobs[i].tiles) * jobs[i].p.k_blocks;
-    tiles += jobs[i].tiles;
-    flops += jobs[i].flops;
-  }
-  if (tiles > ws_.sk_counter_cap) throw StructuralError("launch_sk: tile counter capacity exceeded");
-  P.n_jobs = static_cast<int>(jobs.size());
-  P.iters = iters;
-  // each stream has its own slots / counters: launches on sa and sb may overlap
-  const int set = st == stream2_ ? 1 : 0;
-  P.slots = ws_.sk_slots[set];
-  P.counters = ws_.sk_counters[set];
-  const int grid = static_cast<int>(std::min<int64_t>(sm_count_, iters));
-  // hybrid: whole waves of job 0 data-parallel, the rest stream-K; keep the
-  // stream-K part either empty or at least one iteration per CTA
-  int waves = hybrid ? jobs[0].tiles / grid : 0;
-  const int64_t kb0 = jobs[0].p.k_blocks;
-  while (waves > 0) {
-    const int64_t rest = iters - static_cast<int64_t>(waves) * grid * kb0;
-    if (rest == 0 || rest >= grid) break;
-    --waves;
-  }
-  P.dp_waves = waves;
-  P.sk0 = static_cast<int64_t>(waves) * grid * kb0;
-  prof_begin(st, kTagStep, flops, 0);
-  dev::nt_mma_sk_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(P);
-  after_launch(st);
-}
 void DeviceNet::launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p,
                           int grid) {
   dev::nt_mma_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
@@ -806,7 +735,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     return;
   }
   // ---- 3. tangent chain + Hessian SYRK ------------------------------------
-  if (want_h && !streamk_) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
+  if (want_h) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
   const int kfin_layer = L - 1;
   const bool skinny_final = m_ <= dev::kSkMB;
   // T_l lives in: l == 0 -> t0_ (broadcast over points), else ring buffer
@@ -838,18 +767,6 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     p.ldc = n_pad_;
     p.mode = p.split > 1 ? dev::kPartial : dev::kAccum;
     p.partial = w.syrk_part;
-    if (hybrid_) {  // whole waves data-parallel, the remainder stream-K: no split-K pass
-      p.split = 1;
-      p.mode = dev::kAccum;
-      std::vector<SkJobDesc> jobs(1);
-      jobs[0].ta = &tmap_a(l);
-      jobs[0].tb = &tmap_b(l);
-      jobs[0].p = p;
-      jobs[0].tiles = nb * n_syrk_tiles_;
-      jobs[0].flops = static_cast<double>(d.rows) * n_ * (n_ + 1) * nb;
-      launch_sk(sb, jobs, true);
-      return;
-    }
     if (square_syrk_) {  // 112 x 112 lower tiles, B through the 112-row box map
       p.tiles = sq_tiles_;
       p.n_tiles = n_sq_tiles_;
@@ -867,127 +784,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
   };
 
-  // GEMM producing T_{l+1} = T_l diag(sigma'_l) W_{l+1}^T
-  auto gemm_params = [&](int l) {
-    const DevLayer& dn = layers_[static_cast<size_t>(l + 1)];
-    dev::NtParams p{};
-    p.tiles = nullptr;
-    p.tiles_m = static_cast<int>(n_pad_ / kBM);
-    p.tiles_n = ceil_div(dn.rows, kBN);
-    p.n_tiles = p.tiles_m * p.tiles_n;
-    p.points = nb;
-    p.split = 1;
-    p.k_blocks = ceil_div(dn.cols, kBK);
-    p.a_point_rows = t_point_rows(l);
-    p.b_point_rows = 0;
-    p.b_rows_valid = static_cast<int>(dn.rows);
-    p.m_rows_valid = static_cast<int>(n_pad_);
-    p.scale = w.s1[l];
-    p.s_stride = w.ld[l];
-    p.c = t_buf(l + 1);
-    p.c_point_stride = n_pad_ * ldt_;
-    p.ldc = ldt_;
-    p.mode = dev::kStore;
-    return p;
-  };
-
-  if (streamk_) {
-    // Layer steps on sa, each ONE persistent stream-K launch: GEMM_{l+1}
-    // plus the SYRKs whose tangents and d_l are ready.  The first step runs
-    // GEMM_1 alone, beside the adjoint on sb (co-resident GEMVs); SYRK_0 and
-    // SYRK_1 join GEMM_2, SYRK_l joins GEMM_{l+1} after that, and the last
-    // SYRKs form a final balanced launch.  SYRK jobs of one launch write
-    // distinct H buffers (summed in a fixed order by the symmetrise pass).
-    if (want_h) {
-      for (int i = 0; i < dev::kSkJobs; ++i)
-        CK(cudaMemsetAsync(w.hb[static_cast<size_t>(i)], 0, sizeof(double) * nb * n_pad_ * n_pad_, sa));
-    }
-    bool adj_waited = false;
-    auto wait_adjoint = [&]() {
-      if (adj_waited) return;
-      adj_waited = true;
-      link(sb, sa);
-    };
-    std::vector<int> pending;  // SYRK layers with T ready, not yet run
-    auto syrk_desc = [&](int l, int hb) {
-      const DevLayer& d = layers_[static_cast<size_t>(l)];
-      SkJobDesc j;
-      j.ta = &tmap_a(l);
-      j.tb = &tmap_b(l);
-      j.p = dev::NtParams{};
-      j.p.tiles = syrk_tiles_;
-      j.p.n_tiles = n_syrk_tiles_;
-      j.p.points = nb;
-      j.p.split = 1;
-      j.p.k_blocks = ceil_div(d.rows, kBK);
-      j.p.a_point_rows = t_point_rows(l);
-      j.p.b_point_rows = t_point_rows(l);
-      j.p.b_rows_valid = static_cast<int>(n_);
-      j.p.m_rows_valid = static_cast<int>(n_);
-      j.p.scale = w.d[l];
-      j.p.s_stride = w.ld[l];
-      j.p.c = w.hb[static_cast<size_t>(hb)];
-      j.p.c_point_stride = n_pad_ * n_pad_;
-      j.p.ldc = n_pad_;
-      j.p.mode = dev::kAccum;
-      j.tiles = nb * n_syrk_tiles_;
-      j.flops = static_cast<double>(d.rows) * n_ * (n_ + 1) * nb;
-      return j;
-    };
-    auto flush = [&](std::vector<SkJobDesc>& jobs) {
-      // append pending SYRKs (each to its own H buffer) up to kSkJobs jobs
-      while (!pending.empty() && static_cast<int>(jobs.size()) < dev::kSkJobs) {
-        wait_adjoint();
-        int hb = 0;  // next free H buffer of this launch
-        for (const SkJobDesc& jj : jobs) hb += jj.p.mode == dev::kAccum ? 1 : 0;
-        jobs.push_back(syrk_desc(pending.front(), hb));
-        pending.erase(pending.begin());
-      }
-      if (!jobs.empty()) launch_sk(sa, jobs);
-      jobs.clear();
-    };
-    for (int l = 0; l + 1 < L; ++l) {
-      if (want_h && layers_[static_cast<size_t>(l)].act != kLinear) pending.push_back(l);
-      if (l + 1 == kfin_layer && skinny_final) break;
-      if (l >= 1 && fwd_done[static_cast<size_t>(l)])
-        CK(cudaStreamWaitEvent(sa, fwd_done[static_cast<size_t>(l)], 0));
-      const DevLayer& dn = layers_[static_cast<size_t>(l + 1)];
-      std::vector<SkJobDesc> jobs(1);
-      jobs[0].ta = &tmap_a(l);
-      jobs[0].tb = &dn.tm_w;
-      jobs[0].p = gemm_params(l);
-      jobs[0].tiles = nb * jobs[0].p.n_tiles;
-      jobs[0].flops = 2.0 * n_ * dn.rows * dn.cols * nb;
-      // the first step leaves the adjoint time to finish on sb
-      if (l == 0) {
-        launch_sk(sa, jobs);
-      } else {
-        // T_{l+1} overwrites T_{l+1-R}; that layer's SYRK ran in an earlier
-        // launch on this stream, except when the ring is shorter than the
-        // SYRK lag: then run the pending SYRKs first.
-        flush(jobs);
-      }
-    }
-    // a wide nonlinear (non-softmax) output layer gets a full SYRK too
-    if (want_h && !skinny_final && kfin_layer > 0 && !softmax_out &&
-        layers_[static_cast<size_t>(kfin_layer)].act != kLinear)
-      pending.push_back(kfin_layer);
-    while (!pending.empty()) {
-      std::vector<SkJobDesc> jobs;
-      flush(jobs);
-    }
-  }
-
   // Pre-scaled tangents pay one extra tile store per tile; nets whose
   // single-point GEMMs are split-K (c1: 28 tiles) are launch-latency bound
   // and keep the per-fragment scale.
-  bool prescaled = !hybrid_ && !streamk_;
+  bool prescaled = true;
   for (int l = 0; l + 2 < L && prescaled; ++l)
     if (nb == 1 && (n_pad_ / kBM) * ceil_div(layers_[static_cast<size_t>(l + 1)].rows, kBN) * 2 <= sm_count_)
       prescaled = false;
   // syrk_done[l]: event on sb after SYRK_l (nullptr when none ran)
   std::vector<cudaEvent_t> syrk_done(static_cast<size_t>(L), nullptr);
-  for (int l = 0; l + 1 < L && !streamk_; ++l) {
+  for (int l = 0; l + 1 < L; ++l) {
     // curvature of hidden layer l, on sb once T_l exists (T_0 is constant)
     if (want_h && layers_[static_cast<size_t>(l)].act != kLinear) {
       if (l > 0) link(sa, sb);
@@ -1061,7 +867,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
     // a single point with fewer tiles than half the SMs (c1: 28 tiles):
     // split K, then a fixed-order reduction stores T_{l+1}
-    if (nb == 1 && !hybrid_ && p.n_tiles * 2 <= sm_count_) {
+    if (nb == 1 && p.n_tiles * 2 <= sm_count_) {
       p.split = std::max(1, std::min(sm_count_ / p.n_tiles, p.k_blocks / 8));
       if (p.split > 1) {
         p.mode = dev::kPartial;
@@ -1080,16 +886,6 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         after_launch(sa);
         continue;
       }
-    }
-    if (hybrid_) {
-      std::vector<SkJobDesc> jobs(1);
-      jobs[0].ta = &tmap_a(l);
-      jobs[0].tb = &dn.tm_w;
-      jobs[0].p = p;
-      jobs[0].tiles = nb * p.n_tiles;
-      jobs[0].flops = 2.0 * n_ * dn.rows * dn.cols * nb;
-      launch_sk(sa, jobs, true);
-      continue;
     }
     prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
     launch_nt(sa, *ta, dn.tm_w, p, nb * p.n_tiles);
@@ -1125,12 +921,8 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     after_launch(sa);
   }
   if (want_h) {
-    // stream-K: every SYRK already ran on sa; else the SYRKs live on sb
-    cudaStream_t sh = streamk_ ? sa : sb;
-    if (streamk_)
-      link(sb, sa);  // d / softmax middle of the output layer (adjoint seed)
-    else
-      link(sa, sb);  // the final curvature needs U (sa)
+    cudaStream_t sh = sb;  // the SYRKs live on sb
+    link(sa, sb);          // the final curvature needs U (sa)
     if (df.act != kLinear) {
       if (softmax_out || skinny_final || kfin_layer == 0) {
         // K = m is small: direct lower-triangle update (dense middle for softmax)
@@ -1141,15 +933,14 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
                                                        softmax_out ? w.mid : nullptr, m_ * m_, static_cast<int>(n_),
                                                        static_cast<int>(m_), nb, w.h, n_pad_ * n_pad_, n_pad_);
         after_launch(sh);
-      } else if (!streamk_) {
+      } else {
         syrk(kfin_layer);
       }
     }
     const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
     prof_begin(sh, kTagSymmetrize, 0, 0);
-    dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, sh>>>(
-        w.h, streamk_ ? w.hb[1] : nullptr, streamk_ ? w.hb[2] : nullptr, n_pad_ * n_pad_, n_pad_,
-        static_cast<int>(n_), nb, o.h);
+    dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, sh>>>(w.h, nullptr, nullptr, n_pad_ * n_pad_, n_pad_,
+                                                                  static_cast<int>(n_), nb, o.h);
     after_launch(sh);
   }
   link(sb, sa);  // join: the evaluation ends on `st`
@@ -1341,7 +1132,7 @@ void DeviceNet::copy_intermediate(const char* name, int layer, int nb, double* o
 // ---------------------------------------------------------------------------
 // Shapes the dataflow launch can run (independent of the schedule mode).
 bool DeviceNet::dataflow_possible(int nb, const Outputs& o) const {
-  if (streamk_ || hybrid_ || !concurrent_) return false;
+  if (!concurrent_) return false;
   if (o.h == nullptr || o.g != nullptr) return false;  // the full (y, J, H) oracle only
   if (L_ < 2 || m_ > dev::kSkMB || layers_[static_cast<size_t>(L_ - 1)].act == kSoftmax) return false;
   if (6 * L_ + 1 > dev::kDfMaxMaps) return false;  // TMA descriptors in the kernel parameters
