@@ -667,12 +667,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
       for (int p0 = 0; p0 < nv;) {
         const int left = nv - p0;
-        const int pass = left >= 8 ? 8 : (left >= 4 ? 4 : 1);
-        prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * pass, 8.0 * d.rows * d.cols);
-        if (left >= 8) {
+        // one weight sweep per up to 16 vectors (reverse-mode J: m <= 16 seeds per point)
+        const int pass = left >= 9 ? 16 : (left >= 5 ? 8 : (left >= 2 ? 4 : 1));
+        prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * std::min(pass, left), 8.0 * d.rows * d.cols);
+        if (pass == 16) {
+          dev::adj_cols_kernel<16><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
+                                                                      nv, p0, w.adj_part, w.ld_part);
+        } else if (pass == 8) {
           dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
                                                                      nv, p0, w.adj_part, w.ld_part);
-        } else if (left >= 4) {
+        } else if (pass == 4) {
           dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
                                                                      nv, p0, w.adj_part, w.ld_part);
         } else {
