@@ -7,8 +7,9 @@
 //     1e-12 * max(1, max|A|) (StructuralError)            linalg.cpp:45-71
 //   * symmetric Ruiz equilibration, <= 20 rounds, tol 0.01  linalg.cpp:72-99
 //   * Bunch-Kaufman factorisation P S A S P^T = L D L^T of the equilibrated
-//     matrix -- cuSOLVER's dsytrf (a plain library factorisation: this row
-//     is outside the oracle's hot path)
+//     matrix -- ldlt_bk.cuh: one cooperative launch, left-looking, the
+//     reference's pivoting rule (alpha = (1 + sqrt 17) / 8); cuSOLVER's dsytrf
+//     only beyond n = 20000 (shared-memory limit of the native kernel)
 //   * inertia from the 1x1 / 2x2 pivot blocks with zero threshold
 //     1e-11 * max|S A S|                                     linalg.cpp:101-120
 //   * solve: refuses singular factorizations (SingularError); x = S y with
@@ -21,6 +22,9 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <string>
@@ -28,6 +32,7 @@
 
 #include "device_net.hpp"
 #include "ldlt.hpp"
+#include "ldlt_bk.cuh"
 
 namespace gbb {
 
@@ -112,9 +117,31 @@ int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t
 
 }  // namespace
 
+constexpr int64_t kNativeMaxN = 20000;
+
+// GBOPT_LDLT_TIMING=1: host wall time of the factorisation phases on stderr
+struct PhaseTimer {
+  bool on = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "ldlt: %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
+__global__ void bk_iota_kernel(int* perm, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) perm[i] = static_cast<int>(i);
+}
+
 Ldlt::~Ldlt() {
   if (dev_ >= 0) {
     DeviceGuard g(dev_);
+    for (void* p : {static_cast<void*>(d_l_), static_cast<void*>(d_bk_), static_cast<void*>(d_bki_)})
+      if (p) cudaFree(p);
     for (void* p : {static_cast<void*>(d_fact_), static_cast<void*>(d_ipiv_), static_cast<void*>(d_work_),
                     static_cast<void*>(d_info_), static_cast<void*>(d_rhs_), static_cast<void*>(d_input_),
                     static_cast<void*>(d_vec_), static_cast<void*>(d_ipiv64_), d_sbuf_})
@@ -143,6 +170,7 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   f->dev_ = device;
   DeviceGuard g(device);
   cudaStream_t st;
+  PhaseTimer pt;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   f->stream_ = st;
   const size_t bytes = sizeof(double) * static_cast<size_t>(n) * n;
@@ -155,6 +183,7 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   double* cmax = scale + n;
   double* scal = f->d_vec_ + 4 * n;  // 8 scalars
 
+  pt.mark("setup+upload", st);
   // checks (linalg.cpp:45-71)
   CK(cudaMemsetAsync(scal, 0, sizeof(double) * 3, st));
   ldlt_check_kernel<<<blocks_for(n * n, 256), 256, 0, st>>>(f->d_fact_, n, scal);
@@ -166,6 +195,7 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   if (chk[1] > 1e-12 * std::max(1.0, chk[0]))
     throw StructuralError("ldlt_factor: matrix is not symmetric (max deviation " + std::to_string(chk[1]) + ")");
 
+  pt.mark("checks", st);
   // Ruiz equilibration (linalg.cpp:72-99) on the device; the round control
   // (max |cmax - 1|) is a host reduction of n values per round.
   std::vector<double> h_cmax(static_cast<size_t>(n)), h_rs(static_cast<size_t>(n));
@@ -190,9 +220,100 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   for (int64_t i = 0; i < n; ++i) bmax = std::max(bmax, h_cmax[i]);  // cmax of the final matrix
   f->zero_thresh_ = 1e-11 * bmax;
   CK(cudaMemcpyAsync(scale, f->scale_.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  pt.mark("ruiz", st);
   if (keep_input) {
     CK(cudaMalloc(&f->d_input_, bytes));
     CK(cudaMemcpyAsync(f->d_input_, f->d_fact_, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+
+  auto classify = [&](double eig) {
+    if (std::fabs(eig) <= f->zero_thresh_) ++f->n_zero_;
+    else if (eig > 0.0) ++f->n_pos_;
+    else ++f->n_neg_;
+  };
+  auto classify_2x2 = [&](double p, double q, double r) {
+    const double mid = 0.5 * (p + r), rad = std::hypot(0.5 * (p - r), q);
+    classify(mid + rad);
+    classify(mid - rad);
+  };
+  pt.mark("keep-input", st);
+  if (n <= kNativeMaxN) {
+    // ---- native Bunch-Kaufman: one cooperative launch ----
+    f->native_ = true;
+    int sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const size_t smem = sizeof(double) * static_cast<size_t>(n);
+    CK(cudaFuncSetAttribute(bk::bk_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bk::bk_factor_kernel, bk::kThreads, smem));
+    if (per_sm < 1) throw DeviceError("ldlt_factor: the Bunch-Kaufman kernel does not fit on an SM");
+    // a grid barrier costs ~1.2 us whatever the grid size (tools/gridsync_probe.cu),
+    // so use every co-resident CTA up to about one row per warp
+    const int grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, (n + bk::kWarps - 1) / bk::kWarps)));
+    f->ldl_ = (n + 1) / 2 * 2;  // 16-byte rows
+    const size_t lbytes = sizeof(double) * static_cast<size_t>(n) * f->ldl_;
+    CK(cudaMalloc(&f->d_l_, 2 * lbytes));  // L | W = L D
+    CK(cudaMemsetAsync(f->d_l_, 0, 2 * lbytes, st));
+    CK(cudaMalloc(&f->d_bk_, sizeof(double) * (5 * static_cast<size_t>(n) +
+                                                std::max<size_t>(4 * static_cast<size_t>(grid), 32 * bk::kSlices))));
+    int solve_per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&solve_per_sm, bk::bk_solve_kernel, bk::kThreads, 0));
+    f->solve_grid_ = std::max(1, std::min(sms * std::max(solve_per_sm, 1), 32 * bk::kSlices / bk::kWarps));
+    CK(cudaMalloc(&f->d_bki_, sizeof(int) * 2 * static_cast<size_t>(n)));
+    bk_iota_kernel<<<blocks_for(n, 256), 256, 0, st>>>(f->d_bki_ + n, n);
+    CK(cudaGetLastError());
+    bk::Factor F;
+    F.a = f->d_fact_;
+    F.l = f->d_l_;
+    F.wd = f->d_l_ + static_cast<size_t>(n) * f->ldl_;
+    F.d = f->d_bk_;
+    F.e = F.d + n;
+    F.w = F.e + n;
+    F.wr = F.w + n;
+    F.part = F.wr + 2 * n;  // (z at wr + n is the solve's scratch)
+    F.part2 = F.part + 2 * grid;
+    F.piv = f->d_bki_;
+    F.perm = f->d_bki_ + n;
+    F.n = static_cast<int>(n);
+    F.ldl = static_cast<int>(f->ldl_);
+    CK(cudaMemsetAsync(F.e, 0, sizeof(double) * n, st));
+    void* args[] = {&F};
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    const bool timing = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
+    if (timing) {
+      CK(cudaEventCreate(&t0));
+      CK(cudaEventCreate(&t1));
+      CK(cudaEventRecord(t0, st));
+    }
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_factor_kernel), dim3(grid), dim3(bk::kThreads), args,
+                                   smem, st));
+    if (timing) {
+      CK(cudaEventRecord(t1, st));
+      CK(cudaEventSynchronize(t1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, t0, t1));
+      std::fprintf(stderr, "ldlt: n %lld grid %d per_sm %d bk_factor_kernel %.3f ms\n", static_cast<long long>(n), grid,
+                   per_sm, ms);
+      cudaEventDestroy(t0);
+      cudaEventDestroy(t1);
+    }
+    pt.mark("factor", st);
+    std::vector<double> dd(static_cast<size_t>(n)), ee(static_cast<size_t>(n));
+    std::vector<int> pv(static_cast<size_t>(n));
+    CK(cudaMemcpyAsync(dd.data(), F.d, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ee.data(), F.e, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pv.data(), F.piv, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t k = 0; k < n;) {
+      if (pv[static_cast<size_t>(k)] == 1) {
+        classify(dd[k]);
+        k += 1;
+      } else {
+        classify_2x2(dd[k], ee[k], dd[k + 1]);
+        k += 2;
+      }
+    }
+    return f;
   }
 
   // Bunch-Kaufman on the device (lower; row-major == column-major here)
@@ -223,20 +344,12 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   if (info < 0) throw DeviceError("ldlt_factor: dsytrf rejected argument " + std::to_string(-info));
   std::vector<int64_t> ipiv64(f->ipiv_.begin(), f->ipiv_.end());
   CK(cudaMemcpyAsync(f->d_ipiv64_, ipiv64.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
-  auto classify = [&](double eig) {
-    if (std::fabs(eig) <= f->zero_thresh_) ++f->n_zero_;
-    else if (eig > 0.0) ++f->n_pos_;
-    else ++f->n_neg_;
-  };
   for (int64_t k = 0; k < n;) {
     if (f->ipiv_[static_cast<size_t>(k)] > 0) {  // 1x1 block (LAPACK lower convention)
       classify(diag[k]);
       k += 1;
     } else {  // 2x2 block D(k:k+1, k:k+1), D(k+1,k) in the subdiagonal
-      const double p = diag[k], q = sub[k], r = diag[k + 1];
-      const double mid = 0.5 * (p + r), rad = std::hypot(0.5 * (p - r), q);
-      classify(mid + rad);
-      classify(mid - rad);
+      classify_2x2(diag[k], sub[k], diag[k + 1]);
       k += 2;
     }
   }
@@ -252,6 +365,22 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
 
 // in place on the device vector v: v <- (S A S)^{-1} v
 void Ldlt::solve_factored(double* d_v) const {
+  if (native_) {
+    const double* d = d_bk_;
+    double* z = d_bk_ + 4 * n_;
+    double* part = d_bk_ + 5 * n_;  // the factor's maxima slots, >= 32 * kSlices doubles
+    const double* l = d_l_;
+    int ldl = static_cast<int>(ldl_), n = static_cast<int>(n_);
+    const double* e = d + n_;
+    const int* piv = d_bki_;
+    const int* perm = d_bki_ + n_;
+    const double* bb = d_v;
+    double* x = d_v;
+    void* args[] = {&l, &ldl, &d, &e, &piv, &perm, &n, &bb, &z, &x, &part};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_solve_kernel), dim3(solve_grid_),
+                                   dim3(bk::kThreads), args, 0, stream_));
+    return;
+  }
   auto h = static_cast<cusolverDnHandle_t>(handle_);
   std::vector<char> hbuf(sws_host_);
   CS(cusolverDnXsytrs(h, CUBLAS_FILL_MODE_LOWER, n_, 1, CUDA_R_64F, d_fact_, n_, d_ipiv64_, CUDA_R_64F, d_v, n_,

@@ -50,6 +50,13 @@ class Ldlt {
   double* d_vec_ = nullptr;
   void* d_sbuf_ = nullptr;
   size_t sws_dev_ = 0, sws_host_ = 0;
+  // native Bunch-Kaufman (ldlt_bk.cuh): n <= kNativeMaxN
+  bool native_ = false;
+  double* d_l_ = nullptr;   // [n][ldl_] unit lower factor
+  int64_t ldl_ = 0;
+  int solve_grid_ = 1;
+  double* d_bk_ = nullptr;  // d[n] | e[n] | w[n] | wr[n] | z[n] | part[4 * grid]
+  int* d_bki_ = nullptr;    // piv[n] | perm[n]
 };
 
 }  // namespace gbb

@@ -1,0 +1,401 @@
+// Bunch-Kaufman LDL^T of a dense symmetric matrix on the device: one
+// cooperative (grid-synchronised) launch for the whole factorisation, one
+// single-CTA launch per solve.  Replaces cuSOLVER's dsytrf / sytrs for the
+// KKT row f3 (reference proj/src/linalg.cpp:101-287 factor, 393-438 solve).
+//
+// Factorisation, left-looking, one pivot (1x1 or 2x2) per step:
+//   column k of the updated matrix is  w = A(:, k) - L(:, 0:k) * (D L(k, 0:k)^T)
+//   (a GEMV over the rows of L; the original matrix A is only permuted, never
+//   updated), so a step touches L's rows below k once and needs no trailing
+//   update.  The Bunch-Kaufman test (alpha = (1 + sqrt 17) / 8) picks, from
+//   the column maximum lambda of w and -- when |w_k| < alpha lambda -- the
+//   updated column r of that maximum and its off-diagonal maximum sigma:
+//     1x1 at k;  1x1 at r (swap k <-> r);  or 2x2 at (k, r) (swap k+1 <-> r)
+//   exactly as LAPACK's dsytf2 / the reference's panel code.  Symmetric
+//   interchanges are applied to the trailing part of A, to the rows of L
+//   computed so far, and recorded in perm, so that on exit
+//       P A P^T = L D L^T,   (P b)_i = b[perm[i]].
+//   Per step: every CTA recomputes v = D L(k, 0:k)^T into shared memory; warps
+//   take rows i >= k; a grid-wide barrier publishes the column maxima, a
+//   second (only for non-trivial pivots) those of column r, a third the swap
+//   and the new L column(s).  Ties in the maxima resolve to the smallest row
+//   index, and every reduction has a fixed order: the factorisation is
+//   deterministic.
+//
+// Solve (x = P^T L^-T D^-1 L^-1 P b): one CTA, forward / backward
+// substitution in 32-row blocks (block updates by the whole CTA, the 32 x 32
+// triangle by one warp), block-diagonal D in between.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gbb {
+namespace bk {
+
+namespace cg = cooperative_groups;
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr double kAlpha = 0.64038820320220756872;  // (1 + sqrt(17)) / 8
+
+struct Factor {
+  double* a;      // [n][n] full symmetric (permuted in place; only rows/cols >= k are read at step k)
+  double* l;      // [n][ldl] unit lower factor, row-major (row i holds L(i, 0:i)); ldl even (16-B rows)
+  double* wd;     // [n][ldl] W = L D: row k of W is v = D L(k, 0:k)^T, the GEMV vector of step k
+                  // (W's new columns are the updated columns themselves, before the pivot division)
+  double* d;      // [n] D diagonal
+  double* e;      // [n] D subdiagonal (e[k] = D(k+1, k) of a 2x2 block, else 0)
+  int* piv;       // [n] 1: 1x1 block; 2 / -2: first / second row of a 2x2 block
+  int* perm;      // [n] P: row i of the factorisation is original row perm[i]
+  double* w;      // [n] updated column k
+  double* wr;     // [n] updated column r
+  double* part;   // [2 * grid] per-CTA maxima of column k (value, index as double)
+  double* part2;  // [2 * grid] the same for column r (separate: CTAs may still read part)
+  int n;
+  int ldl;
+};
+
+// (value, index) maximum with ties to the smaller index
+__device__ __forceinline__ void max_pair(double& v, int& i, double v2, int i2) {
+  if (v2 > v || (v2 == v && i2 >= 0 && (i < 0 || i2 < i))) {
+    v = v2;
+    i = i2;
+  }
+}
+
+// CTA-wide (value, index) maximum, result valid in every thread
+__device__ double cta_max(double v, int& idx, double* sv, int* si) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    max_pair(v, idx, v2, i2);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sv[warp] = v;
+    si[warp] = idx;
+  }
+  __syncthreads();
+  v = -1.0;
+  idx = -1;
+  for (int k = 0; k < kWarps; ++k) max_pair(v, idx, sv[k], si[k]);
+  return v;
+}
+
+// grid-wide (value, index) maximum over the per-CTA partials
+__device__ double grid_max(const double* part, int& idx, double* sv, int* si) {
+  double v = -1.0;
+  idx = -1;
+  for (int c = threadIdx.x; c < static_cast<int>(gridDim.x); c += kThreads)
+    max_pair(v, idx, __ldcg(part + 2 * c), static_cast<int>(__ldcg(part + 2 * c + 1)));
+  return cta_max(v, idx, sv, si);
+}
+
+// v[0:k] = W(row, 0:k) = (D L(row, 0:k)^T)^T into shared memory (16-byte loads)
+__device__ void d_times_lrow(const Factor& F, int row, int k, double* v) {
+  const double* wr = F.wd + static_cast<int64_t>(row) * F.ldl;
+  for (int j = 2 * threadIdx.x; j < k; j += 2 * kThreads) {
+    if (j + 1 < k) {
+      const double2 t = __ldcg(reinterpret_cast<const double2*>(wr + j));
+      v[j] = t.x;
+      v[j + 1] = t.y;
+    } else {
+      v[j] = __ldcg(wr + j);
+    }
+  }
+}
+
+// out[i] = A[i][col] - L(i, 0:k) . v for i >= k (one warp per row), and the
+// CTA's maximum of |out[i]| over i >= k, i != skip
+__device__ double column_update(const Factor& F, int col, int k, const double* v, double* out, int skip, int& idx,
+                                double* sv, int* si) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  double m = -1.0;
+  idx = -1;
+  for (int i = k + gw; i < F.n; i += nw) {
+    const double* li = F.l + static_cast<int64_t>(i) * F.ldl;
+    // 16-byte loads, four in flight per lane (the rows are latency-bound
+    // otherwise: one dependent load per 32 lanes per iteration)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = 2 * lane;
+    for (; j + 192 + 1 < k; j += 256) {
+      const double2 a0 = __ldcg(reinterpret_cast<const double2*>(li + j));
+      const double2 a1 = __ldcg(reinterpret_cast<const double2*>(li + j + 64));
+      const double2 a2 = __ldcg(reinterpret_cast<const double2*>(li + j + 128));
+      const double2 a3 = __ldcg(reinterpret_cast<const double2*>(li + j + 192));
+      const double2 v0 = *reinterpret_cast<const double2*>(v + j);
+      const double2 v1 = *reinterpret_cast<const double2*>(v + j + 64);
+      const double2 v2 = *reinterpret_cast<const double2*>(v + j + 128);
+      const double2 v3 = *reinterpret_cast<const double2*>(v + j + 192);
+      s0 = fma(a0.x, v0.x, fma(a0.y, v0.y, s0));
+      s1 = fma(a1.x, v1.x, fma(a1.y, v1.y, s1));
+      s2 = fma(a2.x, v2.x, fma(a2.y, v2.y, s2));
+      s3 = fma(a3.x, v3.x, fma(a3.y, v3.y, s3));
+    }
+    for (; j < k; j += 64) {
+      if (j + 1 < k) {
+        const double2 a0 = __ldcg(reinterpret_cast<const double2*>(li + j));
+        s0 = fma(a0.x, v[j], fma(a0.y, v[j + 1], s0));
+      } else {
+        s0 = fma(__ldcg(li + j), v[j], s0);
+      }
+    }
+    double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double wi = __ldcg(F.a + static_cast<int64_t>(i) * F.n + col) - s;
+    if (lane == 0) out[i] = wi;
+    if (i != skip) max_pair(m, idx, fabs(wi), i);
+  }
+  return cta_max(m, idx, sv, si);
+}
+
+__global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
+  extern __shared__ double smem[];
+  double* v = smem;               // [n]
+  __shared__ double sv[kWarps];
+  __shared__ int si[kWarps];
+  cg::grid_group grid = cg::this_grid();
+  const int n = F.n;
+  const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
+
+  for (int k = 0; k < n;) {
+    // ---- updated column k and its maximum below the diagonal ----
+    d_times_lrow(F, k, k, v);
+    __syncthreads();
+    int idx;
+    double m = column_update(F, k, k, v, F.w, k, idx, sv, si);
+    if (threadIdx.x == 0) {
+      F.part[2 * blockIdx.x] = m;
+      F.part[2 * blockIdx.x + 1] = idx;
+    }
+    grid.sync();
+    int r;
+    const double lambda = fmax(grid_max(F.part, r, sv, si), 0.0);
+    const double absakk = fabs(__ldcg(F.w + k));
+    int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
+    if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
+      // ---- updated column r and its off-diagonal maximum ----
+      __syncthreads();  // v is reused
+      d_times_lrow(F, r, k, v);
+      __syncthreads();
+      int idx2;
+      double m2 = column_update(F, r, k, v, F.wr, r, idx2, sv, si);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        F.part2[2 * blockIdx.x] = m2;
+        F.part2[2 * blockIdx.x + 1] = idx2;
+      }
+      grid.sync();
+      int r2;
+      const double sigma = fmax(grid_max(F.part2, r2, sv, si), 0.0);
+      if (absakk * sigma >= kAlpha * lambda * lambda)
+        kind = 0;
+      else if (fabs(__ldcg(F.wr + r)) >= kAlpha * sigma)
+        kind = 1;
+      else
+        kind = 2;
+    }
+    // ---- symmetric interchange p <-> r of the trailing A, of L's rows so
+    //      far, and of perm ----
+    const int p = kind == 1 ? k : kind == 2 ? k + 1 : -1;
+    if (p >= 0 && p != r) {
+      for (int j = k + tid; j < n; j += nt) {
+        if (j == p || j == r) continue;
+        double* ap = F.a + static_cast<int64_t>(p) * n;
+        double* ar = F.a + static_cast<int64_t>(r) * n;
+        double t = ap[j];
+        ap[j] = ar[j];
+        ar[j] = t;
+        t = F.a[static_cast<int64_t>(j) * n + p];
+        F.a[static_cast<int64_t>(j) * n + p] = F.a[static_cast<int64_t>(j) * n + r];
+        F.a[static_cast<int64_t>(j) * n + r] = t;
+      }
+      for (int j = tid; j < k; j += nt) {
+        double* lp = F.l + static_cast<int64_t>(p) * F.ldl;
+        double* lr = F.l + static_cast<int64_t>(r) * F.ldl;
+        double t = lp[j];
+        lp[j] = lr[j];
+        lr[j] = t;
+        double* wp = F.wd + static_cast<int64_t>(p) * F.ldl;
+        double* wq = F.wd + static_cast<int64_t>(r) * F.ldl;
+        t = wp[j];
+        wp[j] = wq[j];
+        wq[j] = t;
+      }
+      if (tid == 0) {
+        const double t = F.a[static_cast<int64_t>(p) * n + p];
+        F.a[static_cast<int64_t>(p) * n + p] = F.a[static_cast<int64_t>(r) * n + r];
+        F.a[static_cast<int64_t>(r) * n + r] = t;
+        const int pt = F.perm[p];
+        F.perm[p] = F.perm[r];
+        F.perm[r] = pt;
+      }
+    }
+    // ---- D block and the new column(s) of L (rows below the block) ----
+    // sigma_swap(i): index of row i before the interchange p <-> r
+    auto src = [&](int i) { return (p >= 0 && p != r) ? (i == p ? r : (i == r ? p : i)) : i; };
+    if (kind == 0) {
+      const double dk = __ldcg(F.w + k);
+      if (tid == 0) {
+        F.d[k] = dk;
+        F.e[k] = 0.0;
+        F.piv[k] = 1;
+        F.l[static_cast<int64_t>(k) * F.ldl + k] = 1.0;
+      }
+      for (int i = k + 1 + tid; i < n; i += nt) {
+        const double x = __ldcg(F.w + i);
+        F.l[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x / dk : 0.0;
+        F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
+      }
+    } else if (kind == 1) {
+      const double dk = __ldcg(F.wr + r);
+      if (tid == 0) {
+        F.d[k] = dk;
+        F.e[k] = 0.0;
+        F.piv[k] = 1;
+        F.l[static_cast<int64_t>(k) * F.ldl + k] = 1.0;
+      }
+      for (int i = k + 1 + tid; i < n; i += nt) {
+        const double x = __ldcg(F.wr + src(i));
+        F.l[static_cast<int64_t>(i) * F.ldl + k] = x / dk;
+        F.wd[static_cast<int64_t>(i) * F.ldl + k] = x;
+      }
+    } else {
+      const double a = __ldcg(F.w + k), b = __ldcg(F.w + r), c = __ldcg(F.wr + r);
+      const double det = a * c - b * b;
+      if (tid == 0) {
+        F.d[k] = a;
+        F.d[k + 1] = c;
+        F.e[k] = b;
+        F.e[k + 1] = 0.0;
+        F.piv[k] = 2;
+        F.piv[k + 1] = -2;
+        F.l[static_cast<int64_t>(k) * F.ldl + k] = 1.0;
+        F.l[static_cast<int64_t>(k + 1) * F.ldl + k] = 0.0;
+        F.l[static_cast<int64_t>(k + 1) * F.ldl + k + 1] = 1.0;
+        F.wd[static_cast<int64_t>(k + 1) * F.ldl + k] = b;  // (L D)(k+1, k) = 0 a + 1 b
+      }
+      for (int i = k + 2 + tid; i < n; i += nt) {
+        const int s = src(i);
+        const double x0 = __ldcg(F.w + s), x1 = __ldcg(F.wr + s);
+        // [L(i,k) L(i,k+1)] = [x0 x1] D^{-1},  D^{-1} = [[c, -b], [-b, a]] / det
+        F.l[static_cast<int64_t>(i) * F.ldl + k] = (x0 * c - x1 * b) / det;
+        F.l[static_cast<int64_t>(i) * F.ldl + k + 1] = (x1 * a - x0 * b) / det;
+        F.wd[static_cast<int64_t>(i) * F.ldl + k] = x0;
+        F.wd[static_cast<int64_t>(i) * F.ldl + k + 1] = x1;
+      }
+    }
+    grid.sync();
+    k += kind == 2 ? 2 : 1;
+  }
+}
+
+// x = P^T L^-T D^-1 L^-1 P b: one cooperative launch.  The substitutions
+// walk 32-row blocks; each block's update from the rows already solved is
+// spread over every warp of the grid (partials per (row, warp slice), summed
+// in a fixed order), then one warp solves the 32 x 32 triangle; two grid
+// barriers per block.
+constexpr int kSlices = 64;  // warp slices per row of a block update
+
+__global__ void __launch_bounds__(kThreads) bk_solve_kernel(const double* __restrict__ l, int ldl,
+                                                            const double* __restrict__ d, const double* __restrict__ e,
+                                                            const int* __restrict__ piv, const int* __restrict__ perm,
+                                                            int n, const double* b, double* z, double* x,
+                                                            double* part /* [32][kSlices] */) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
+  // z = P b
+  for (int i = tid; i < n; i += nt) z[i] = b[perm[i]];
+  grid.sync();
+  // ---- forward: L z = P b (unit lower) ----
+  for (int b0 = 0; b0 < n; b0 += 32) {
+    const int rows = min(32, n - b0);
+    // task (rr, sl): row b0 + rr, columns j = sl * 32 + lane + 32 * kSlices * t < b0
+    for (int task = gw; task < 32 * kSlices; task += nw) {
+      const int rr = task / kSlices, sl = task % kSlices;
+      double s = 0.0;
+      if (rr < rows) {
+        const double* li = l + static_cast<int64_t>(b0 + rr) * ldl;
+        for (int j = sl * 32 + lane; j < b0; j += 32 * kSlices) s = fma(__ldcg(li + j), __ldcg(z + j), s);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) part[task] = s;
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && warp == 0) {
+      double zi = 0.0;
+      if (lane < rows) {
+        double s = 0.0;
+        for (int sl = 0; sl < kSlices; ++sl) s += __ldcg(part + lane * kSlices + sl);  // fixed order
+        zi = __ldcg(z + b0 + lane) - s;
+      }
+      for (int j = 0; j < rows; ++j) {
+        const double zj = __shfl_sync(0xffffffffu, zi, j);
+        if (lane > j && lane < rows) zi -= __ldcg(l + static_cast<int64_t>(b0 + lane) * ldl + b0 + j) * zj;
+      }
+      if (lane < rows) z[b0 + lane] = zi;
+    }
+    grid.sync();
+  }
+  // ---- D ----
+  for (int i = tid; i < n; i += nt) {
+    if (piv[i] == 1) {
+      x[i] = __ldcg(z + i) / d[i];
+    } else {
+      const bool first = piv[i] == 2;
+      const int k = first ? i : i - 1;  // block (k, k+1)
+      const double a = d[k], bb = e[k], c = d[k + 1];
+      const double det = a * c - bb * bb;
+      const double z0 = __ldcg(z + k), z1 = __ldcg(z + k + 1);
+      x[i] = first ? (c * z0 - bb * z1) / det : (a * z1 - bb * z0) / det;
+    }
+  }
+  grid.sync();
+  // ---- backward: L^T y = x ----
+  const int nblk = (n + 31) / 32;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int b0 = bi * 32, b1 = min(n, b0 + 32), rows = b1 - b0;
+    // task (c, sl): column b0 + c of L over rows j >= b1 -- lanes take rows
+    for (int task = gw; task < 32 * kSlices; task += nw) {
+      const int c = task / kSlices, sl = task % kSlices;
+      double s = 0.0;
+      if (c < rows)
+        for (int j = b1 + sl * 32 + lane; j < n; j += 32 * kSlices)
+          s = fma(__ldcg(l + static_cast<int64_t>(j) * ldl + b0 + c), __ldcg(x + j), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) part[task] = s;
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && warp == 0) {
+      double yi = 0.0;
+      if (lane < rows) {
+        double s = 0.0;
+        for (int sl = 0; sl < kSlices; ++sl) s += __ldcg(part + lane * kSlices + sl);
+        yi = __ldcg(x + b0 + lane) - s;
+      }
+      for (int j = rows - 1; j >= 0; --j) {
+        const double yj = __shfl_sync(0xffffffffu, yi, j);
+        if (lane < j) yi -= __ldcg(l + static_cast<int64_t>(b0 + j) * ldl + b0 + lane) * yj;
+      }
+      if (lane < rows) x[b0 + lane] = yi;
+    }
+    grid.sync();
+  }
+  // ---- x_orig[perm[i]] = y_i (through z) ----
+  for (int i = tid; i < n; i += nt) z[perm[i]] = __ldcg(x + i);
+  grid.sync();
+  for (int i = tid; i < n; i += nt) x[i] = __ldcg(z + i);
+}
+
+}  // namespace bk
+}  // namespace gbb

@@ -114,3 +114,66 @@ class TestGpuLdlt:
         A = lo.matrix_with_spectrum(rng, [5, -4, 3, -2, 1, 0.5, -0.25])
         p = rng.permutation(7)
         assert gb.ldlt_factor(A).inertia == gb.ldlt_factor(A[np.ix_(p, p)]).inertia == (4, 3, 0)
+
+
+@pytest.mark.gpu
+class TestNativeBunchKaufman:
+    """The native pivoting kernel (ldlt_bk.cuh): matrices that force 2x2
+    pivots and 1x1 pivots with interchanges, against eigenvalues and the
+    oracle, plus solves through the same factors."""
+
+    @pytest.fixture(autouse=True)
+    def _gpu(self):
+        if not has_gpu():
+            pytest.skip("no GPU")
+
+    def test_zero_diagonal_forces_2x2_pivots(self):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(21)
+        n = 300
+        B = rng.uniform(-1, 1, (n, n))
+        A = 0.5 * (B + B.T)
+        np.fill_diagonal(A, 0.0)  # every first pivot test fails: 2x2 blocks or swaps
+        eig = np.linalg.eigvalsh(A)
+        f = gb.ldlt_factor(A)
+        assert f.inertia == (int((eig > 0).sum()), int((eig < 0).sum()), 0) == lo.inertia(A)
+        b = rng.uniform(-1, 1, n)
+        x = f.solve(b)
+        assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
+
+    def test_saddle_point_blocks(self):
+        """[[0, J^T], [J, 0]]: all pivots are 2x2 pairings across the blocks."""
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(22)
+        m = 70
+        J = rng.uniform(-1, 1, (m, m)) + 3 * np.eye(m)
+        K = np.block([[np.zeros((m, m)), J.T], [J, np.zeros((m, m))]])
+        f = gb.ldlt_factor(K)
+        assert f.inertia == (m, m, 0)
+        b = rng.uniform(-1, 1, 2 * m)
+        x = f.solve(b)
+        assert np.abs(K @ x - b).max() <= 1e-10 * np.abs(K).max() * max(1.0, np.abs(x).max())
+
+    @pytest.mark.parametrize("n", [1, 2, 31, 33, 1000])
+    def test_block_edges_and_larger_kkt(self, n):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(100 + n)
+        m = max(1, n // 4)
+        H = rng.uniform(-1, 1, (n, n))
+        H = 0.5 * (H + H.T) + np.diag(10.0 ** rng.uniform(-2, 6, n))
+        J = rng.uniform(-1, 1, (m, n))
+        K = np.block([[H, J.T], [J, -1e-8 * np.eye(m)]])
+        f = gb.ldlt_factor(K)
+        assert f.inertia == lo.inertia(K)
+        b = rng.uniform(-1, 1, n + m)
+        x = f.solve(b)
+        assert np.abs(K @ x - b).max() <= 1e-8 * (np.abs(K).max() * np.abs(x).max() + np.abs(b).max())
+
+    def test_deterministic(self):
+        import paper_2509_22462_b200 as gb
+        rng = np.random.default_rng(23)
+        A = lo.matrix_with_spectrum(rng, rng.uniform(-2, 2, 150))
+        b = rng.uniform(-1, 1, 150)
+        x0 = gb.ldlt_factor(A).solve(b)
+        for _ in range(3):
+            assert np.array_equal(gb.ldlt_factor(A).solve(b), x0)
