@@ -49,9 +49,11 @@ struct Factor {
   double* e;      // [n] D subdiagonal (e[k] = D(k+1, k) of a 2x2 block, else 0)
   int* piv;       // [n] 1: 1x1 block; 2 / -2: first / second row of a 2x2 block
   int* perm;      // [n] P: row i of the factorisation is original row perm[i]
-  double* w;      // [n] updated column k
+  double* w;      // [n] updated column k (ping-pong with w2 across look-ahead steps)
+  double* w2;     // [n]
   double* wr;     // [n] updated column r
-  double* part;   // [2 * grid] per-CTA maxima of column k (value, index as double)
+  double* part;   // [2 * grid] per-CTA maxima of column k (value, index as double); ping-pong with part3
+  double* part3;  // [2 * grid]
   double* part2;  // [2 * grid] the same for column r (separate: CTAs may still read part)
   int n;
   int ldl;
@@ -155,6 +157,61 @@ __device__ double column_update(const Factor& F, int col, int k, const double* v
   return cta_max(m, idx, sv, si);
 }
 
+// Look-ahead after a 1x1 pivot without interchange at k (the common case):
+// in one pass over the rows i > k, write column k of L and W
+// (L(i,k) = w_i / d_k, W(i,k) = w_i) and compute column k+1 of the next
+// step, w'_i = A(i,k+1) - L(i,0:k) W(k+1,0:k)^T - L(i,k) W(k+1,k), with the
+// new column applied as a rank-1 term from registers -- one grid barrier
+// per such pivot instead of two.  v[0:k] = W(k+1, 0:k) must be staged.
+__device__ double lookahead_update(const Factor& F, int k, double dk, const double* w, const double* v, double vk,
+                                   double* wn, int& idx, double* sv, int* si) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  double m = -1.0;
+  idx = -1;
+  for (int i = k + 1 + gw; i < F.n; i += nw) {
+    const double* li = F.l + static_cast<int64_t>(i) * F.ldl;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = 2 * lane;
+    for (; j + 192 + 1 < k; j += 256) {
+      const double2 a0 = __ldcg(reinterpret_cast<const double2*>(li + j));
+      const double2 a1 = __ldcg(reinterpret_cast<const double2*>(li + j + 64));
+      const double2 a2 = __ldcg(reinterpret_cast<const double2*>(li + j + 128));
+      const double2 a3 = __ldcg(reinterpret_cast<const double2*>(li + j + 192));
+      const double2 v0 = *reinterpret_cast<const double2*>(v + j);
+      const double2 v1 = *reinterpret_cast<const double2*>(v + j + 64);
+      const double2 v2 = *reinterpret_cast<const double2*>(v + j + 128);
+      const double2 v3 = *reinterpret_cast<const double2*>(v + j + 192);
+      s0 = fma(a0.x, v0.x, fma(a0.y, v0.y, s0));
+      s1 = fma(a1.x, v1.x, fma(a1.y, v1.y, s1));
+      s2 = fma(a2.x, v2.x, fma(a2.y, v2.y, s2));
+      s3 = fma(a3.x, v3.x, fma(a3.y, v3.y, s3));
+    }
+    for (; j < k; j += 64) {
+      if (j + 1 < k) {
+        const double2 a0 = __ldcg(reinterpret_cast<const double2*>(li + j));
+        s0 = fma(a0.x, v[j], fma(a0.y, v[j + 1], s0));
+      } else {
+        s0 = fma(__ldcg(li + j), v[j], s0);
+      }
+    }
+    double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double x = __ldcg(w + i);
+    const double lik = dk != 0.0 ? x / dk : 0.0;
+    s = fma(lik, vk, s);  // the new column k (fixed order: after the reduction)
+    const double wi = __ldcg(F.a + static_cast<int64_t>(i) * F.n + k + 1) - s;
+    if (lane == 0) {
+      F.l[static_cast<int64_t>(i) * F.ldl + k] = lik;
+      F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
+      wn[i] = wi;
+    }
+    if (i != k + 1) max_pair(m, idx, fabs(wi), i);
+  }
+  return cta_max(m, idx, sv, si);
+}
+
 __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
   extern __shared__ double smem[];
   double* v = smem;               // [n]
@@ -164,20 +221,26 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
   const int n = F.n;
   const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
 
+  int cur = 0;        // which of (w, part) / (w2, part3) holds the current column
+  bool pre = false;   // column k already computed (and its maxima published) by a look-ahead
   for (int k = 0; k < n;) {
-    // ---- updated column k and its maximum below the diagonal ----
-    d_times_lrow(F, k, k, v);
-    __syncthreads();
-    int idx;
-    double m = column_update(F, k, k, v, F.w, k, idx, sv, si);
-    if (threadIdx.x == 0) {
-      F.part[2 * blockIdx.x] = m;
-      F.part[2 * blockIdx.x + 1] = idx;
+    double* const wk = cur ? F.w2 : F.w;
+    double* const pk = cur ? F.part3 : F.part;
+    if (!pre) {
+      // ---- updated column k and its maximum below the diagonal ----
+      d_times_lrow(F, k, k, v);
+      __syncthreads();
+      int idx;
+      double m = column_update(F, k, k, v, wk, k, idx, sv, si);
+      if (threadIdx.x == 0) {
+        pk[2 * blockIdx.x] = m;
+        pk[2 * blockIdx.x + 1] = idx;
+      }
+      grid.sync();
     }
-    grid.sync();
     int r;
-    const double lambda = fmax(grid_max(F.part, r, sv, si), 0.0);
-    const double absakk = fabs(__ldcg(F.w + k));
+    const double lambda = fmax(grid_max(pk, r, sv, si), 0.0);
+    const double absakk = fabs(__ldcg(wk + k));
     int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
     if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
       // ---- updated column r and its off-diagonal maximum ----
@@ -201,6 +264,35 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
       else
         kind = 2;
     }
+    if (kind == 0 && k + 1 < n) {
+      // ---- look-ahead: column k of L / W and column k+1, one barrier ----
+      const double dk = __ldcg(wk + k);
+      __syncthreads();  // v is reused
+      d_times_lrow(F, k + 1, k, v);
+      __syncthreads();
+      const double vk = dk != 0.0 ? __ldcg(wk + k + 1) : 0.0;  // W(k+1, k)
+      double* const wn = cur ? F.w : F.w2;
+      double* const pn = cur ? F.part : F.part3;
+      int idx;
+      const double m = lookahead_update(F, k, dk, wk, v, vk, wn, idx, sv, si);
+      if (threadIdx.x == 0) {
+        pn[2 * blockIdx.x] = m;
+        pn[2 * blockIdx.x + 1] = idx;
+      }
+      if (tid == 0) {
+        F.d[k] = dk;
+        F.e[k] = 0.0;
+        F.piv[k] = 1;
+        F.l[static_cast<int64_t>(k) * F.ldl + k] = 1.0;
+        F.wd[static_cast<int64_t>(k) * F.ldl + k] = dk;
+      }
+      grid.sync();
+      cur ^= 1;
+      pre = true;
+      k += 1;
+      continue;
+    }
+    pre = false;
     // ---- symmetric interchange p <-> r of the trailing A, of L's rows so
     //      far, and of perm ----
     const int p = kind == 1 ? k : kind == 2 ? k + 1 : -1;
@@ -241,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
     // sigma_swap(i): index of row i before the interchange p <-> r
     auto src = [&](int i) { return (p >= 0 && p != r) ? (i == p ? r : (i == r ? p : i)) : i; };
     if (kind == 0) {
-      const double dk = __ldcg(F.w + k);
+      const double dk = __ldcg(wk + k);
       if (tid == 0) {
         F.d[k] = dk;
         F.e[k] = 0.0;
@@ -249,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
         F.l[static_cast<int64_t>(k) * F.ldl + k] = 1.0;
       }
       for (int i = k + 1 + tid; i < n; i += nt) {
-        const double x = __ldcg(F.w + i);
+        const double x = __ldcg(wk + i);
         F.l[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x / dk : 0.0;
         F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
       }
@@ -267,7 +359,7 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
         F.wd[static_cast<int64_t>(i) * F.ldl + k] = x;
       }
     } else {
-      const double a = __ldcg(F.w + k), b = __ldcg(F.w + r), c = __ldcg(F.wr + r);
+      const double a = __ldcg(wk + k), b = __ldcg(wk + r), c = __ldcg(F.wr + r);
       const double det = a * c - b * b;
       if (tid == 0) {
         F.d[k] = a;
@@ -283,7 +375,7 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
       }
       for (int i = k + 2 + tid; i < n; i += nt) {
         const int s = src(i);
-        const double x0 = __ldcg(F.w + s), x1 = __ldcg(F.wr + s);
+        const double x0 = __ldcg(wk + s), x1 = __ldcg(F.wr + s);
         // [L(i,k) L(i,k+1)] = [x0 x1] D^{-1},  D^{-1} = [[c, -b], [-b, a]] / det
         F.l[static_cast<int64_t>(i) * F.ldl + k] = (x0 * c - x1 * b) / det;
         F.l[static_cast<int64_t>(i) * F.ldl + k + 1] = (x1 * a - x0 * b) / det;
