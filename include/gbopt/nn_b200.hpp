@@ -176,6 +176,20 @@ class NeuralNet {
                            jac ? jac->data.data() : nullptr, hess ? hess->data.data() : nullptr));
   }
 
+  // Fused evaluation with the Hessian as its packed lower triangle in row
+  // order (hess_lower[a (a + 1) / 2 + c] = H(a, c), c <= a), packed on the
+  // device: the value order of the reduced-space Hessian callback.
+  void oracle_lower(const RealVec& x, const RealVec& lambda, RealVec* y, DenseMat* jac, RealVec* hess_lower) const {
+    check_len(x, input_dim(), "oracle_lower");
+    check_len(lambda, output_dim(), "oracle_lower");
+    const int64_t n = input_dim(), m = output_dim();
+    if (y) y->assign(static_cast<size_t>(m), 0.0);
+    if (jac) *jac = DenseMat(m, n);
+    hess_lower->assign(static_cast<size_t>(n * (n + 1) / 2), 0.0);
+    check(gbopt_net_oracle_lower(h_.get(), 1, x.data(), x.size(), lambda.data(), lambda.size(), y ? y->data() : nullptr,
+                                 jac ? jac->data.data() : nullptr, hess_lower->data(), hess_lower->size()));
+  }
+
   const gbopt_net* handle() const { return h_.get(); }
 
  private:
@@ -257,15 +271,13 @@ class ReducedSpaceOracle {
     for (size_t i = 0; i < lam.size(); ++i) neg[i] = -lam[i];
     if (!same_x(xb, h_x_) || neg != h_lam_) {
       const RealVec x = head(xb);
-      net_.oracle(x, neg, &y_, &jac_, &hess_);
+      // packed on the device in the pattern's value order
+      net_.oracle_lower(x, neg, &y_, &jac_, &hess_lower_);
       y_x_ = j_x_ = h_x_ = x;
       h_lam_ = neg;
       ++evals_;
     }
-    values.resize(static_cast<size_t>(n_ * (n_ + 1) / 2));
-    size_t k = 0;
-    for (int64_t a = 0; a < n_; ++a)
-      for (int64_t b = 0; b <= a; ++b) values[k++] = hess_(a, b);
+    values = hess_lower_;
   }
 
   // Number of device evaluations issued so far.
@@ -279,8 +291,8 @@ class ReducedSpaceOracle {
 
   NeuralNet net_;
   int64_t n_ = 0, m_ = 0, evals_ = 0;
-  RealVec y_x_, j_x_, h_x_, h_lam_, y_;
-  DenseMat jac_, hess_;
+  RealVec y_x_, j_x_, h_x_, h_lam_, y_, hess_lower_;
+  DenseMat jac_;
 };
 
 }  // namespace b200

@@ -194,6 +194,18 @@ gbopt_status gbopt_net_oracle_batched(const gbopt_net* net, size_t batch,
                                       const double* Lambda, size_t m,
                                       double* Y, double* J, double* H);
 
+/* As gbopt_net_oracle_batched, but the Hessian comes back as the packed
+ * lower triangle, row by row: Hl[b * n (n + 1) / 2 + a (a + 1) / 2 + c] =
+ * H_b(a, c) for c <= a -- the value order of the reduced-space Lagrangian-
+ * Hessian callback (proj/src/formulations.cpp:298-315, 332-340; for
+ * non-ascending host indices the reference flips the (row, col) pattern
+ * entries, not the values).  Packed on the device: half the transfer, no
+ * host gather.  hl_len = batch * n * (n + 1) / 2; Y and J may be NULL. */
+gbopt_status gbopt_net_oracle_lower(const gbopt_net* net, size_t batch,
+                                    const double* X, size_t n,
+                                    const double* Lambda, size_t m, double* Y,
+                                    double* J, double* Hl, size_t hl_len);
+
 /* Same as gbopt_net_oracle_batched on DEVICE pointers of the bound device,
  * enqueued on `stream` (a cudaStream_t, or NULL for the legacy default
  * stream) and NOT synchronised: the caller orders work on `stream`.  This

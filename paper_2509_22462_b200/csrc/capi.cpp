@@ -337,6 +337,20 @@ gbopt_status gbopt_net_oracle_batched(const gbopt_net* net, size_t batch, const 
   });
 }
 
+gbopt_status gbopt_net_oracle_lower(const gbopt_net* net, size_t batch, const double* X, size_t n,
+                                    const double* Lambda, size_t m, double* Y, double* J, double* Hl,
+                                    size_t hl_len) {
+  if (net == nullptr || X == nullptr || Lambda == nullptr || Hl == nullptr)
+    return fail_argument("gbopt_net_oracle_lower: net, X, Lambda and Hl must be non-null");
+  if (!dims_ok(net, n, m)) return fail_argument("gbopt_net_oracle_lower: lengths do not match the network dimensions");
+  if (batch == 0 || batch > (1u << 30)) return fail_argument("gbopt_net_oracle_lower: batch out of range");
+  if (hl_len != batch * n * (n + 1) / 2)
+    return fail_argument("gbopt_net_oracle_lower: Hl must hold batch * n * (n + 1) / 2 values");
+  return guarded([&] {
+    net->net->device().evaluate_host(static_cast<int>(batch), X, Lambda, Y, J, Hl, nullptr, true);
+  });
+}
+
 gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net, size_t batch, const double* dX, size_t n,
                                              const double* dLambda, size_t m, double* dY, double* dJ, double* dH,
                                              void* stream) {

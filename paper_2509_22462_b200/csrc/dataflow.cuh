@@ -482,5 +482,19 @@ __global__ void symmetrize_slots_kernel(const double* __restrict__ hws, int slot
   out[e] = v;
 }
 
+// Packed lower triangle of H in row order (the reduced-space pattern order,
+// formulations.cpp:298-315): out[b][a (a + 1) / 2 + c] = sum_q H_q[b][a][c]
+// for c <= a.  Grid (ceil(n / 256), n, nb).
+__global__ void pack_lower_kernel(const double* __restrict__ hws, int slots, int64_t slot_stride,
+                                  int64_t h_point_stride, int64_t ldh, int n, double* __restrict__ out) {
+  const int a = blockIdx.y, b = blockIdx.z;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > a) return;
+  const int64_t o = h_point_stride * b + static_cast<int64_t>(a) * ldh + c;
+  double v = 0.0;
+  for (int q = 0; q < slots; ++q) v += hws[slot_stride * q + o];
+  out[static_cast<int64_t>(b) * n * (n + 1) / 2 + static_cast<int64_t>(a) * (a + 1) / 2 + c] = v;
+}
+
 }  // namespace dev
 }  // namespace gbb

@@ -93,8 +93,9 @@ struct ProfResult {
 struct Outputs {
   double* y = nullptr;  // [nb][m]
   double* j = nullptr;  // [nb][m][n]
-  double* h = nullptr;  // [nb][n][n]
+  double* h = nullptr;  // [nb][n][n], or [nb][n (n + 1) / 2] packed lower rows when h_packed
   double* g = nullptr;  // [nb][n]
+  bool h_packed = false;
 };
 
 // One persistent dataflow launch (dataflow.cuh) for a batch size: the
@@ -125,7 +126,8 @@ class DeviceNet {
   bool last_dataflow() const { return last_dataflow_; }
 
   // Host buffers in/out (synchronous).  Any output may be null.
-  void evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess, double* grad);
+  void evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess, double* grad,
+                     bool hess_packed = false);
   // Copies an intermediate per-layer vector of the most recent evaluation
   // ("z", "y", "s1", "s2", "ybar", "gz", "d") for `nb` points into out
   // (nb x rows(l), row-major).  Synchronous; for white-box tests.
@@ -137,7 +139,7 @@ class DeviceNet {
                        cudaStream_t user);
 
  private:
-  using GraphKey = std::tuple<int, double*, double*, double*, double*, bool>;
+  using GraphKey = std::tuple<int, double*, double*, double*, double*, bool, bool>;
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;

@@ -943,8 +943,12 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
     const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
     prof_begin(sh, kTagSymmetrize, 0, 0);
-    dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, sh>>>(w.h, nullptr, nullptr, n_pad_ * n_pad_, n_pad_,
-                                                                  static_cast<int>(n_), nb, o.h);
+    if (o.h_packed)
+      dev::pack_lower_kernel<<<dim3(ceil_div(n_, 256), static_cast<unsigned>(n_), nb), 256, 0, sh>>>(
+          w.h, 1, 0, n_pad_ * n_pad_, n_pad_, static_cast<int>(n_), o.h);
+    else
+      dev::symmetrize_out_kernel<<<ceil_div(tot, 256), 256, 0, sh>>>(w.h, nullptr, nullptr, n_pad_ * n_pad_, n_pad_,
+                                                                    static_cast<int>(n_), nb, o.h);
     after_launch(sh);
   }
   link(sb, sa);  // join: the evaluation ends on `st`
@@ -992,7 +996,7 @@ void DeviceNet::autotune(cudaStream_t st, int nb, const Outputs& o) {
 
 void DeviceNet::dispatch(cudaStream_t st, int nb, const Outputs& o) {
   last_dataflow_ = dataflow_ok(nb, o);
-  const GraphKey key{nb, o.y, o.j, o.h, o.g, last_dataflow_};
+  const GraphKey key{nb, o.y, o.j, o.h, o.g, last_dataflow_, o.h_packed};
   if (!net_.use_graphs) {
     launches_ = 0;
     enqueue(st, nb, o);
@@ -1027,7 +1031,7 @@ void DeviceNet::dispatch(cudaStream_t st, int nb, const Outputs& o) {
 
 // Host-buffer entry: copy in, evaluate, copy out, synchronise.
 void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess,
-                              double* grad) {
+                              double* grad, bool hess_packed) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
   Workspace& w = ws_;
@@ -1036,6 +1040,7 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   o.j = jac ? w.j_out : nullptr;
   o.h = hess ? w.h_out : nullptr;
   o.g = grad ? w.g_out : nullptr;
+  o.h_packed = hess_packed;
   prepare(nb, o);
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
                        cudaMemcpyHostToDevice, stream_));
@@ -1053,7 +1058,7 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   };
   const Out outs[4] = {{y, w.y_out, static_cast<size_t>(nb) * m_},
                        {jac, w.j_out, static_cast<size_t>(nb) * m_ * n_},
-                       {hess, w.h_out, static_cast<size_t>(nb) * n_ * n_},
+                       {hess, w.h_out, static_cast<size_t>(nb) * (hess_packed ? n_ * (n_ + 1) / 2 : n_ * n_)},
                        {grad, w.g_out, static_cast<size_t>(nb) * n_}};
   size_t staged = 0;
   bool pinned[4] = {false, false, false, false};
@@ -1647,6 +1652,10 @@ void DeviceNet::enqueue_dataflow(cudaStream_t st, int nb, const Outputs& o) {
   }
   const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
   prof_begin(st, kTagSymmetrize, 0, 0);
+  if (o.h_packed)
+    dev::pack_lower_kernel<<<dim3(ceil_div(n_, 256), static_cast<unsigned>(n_), nb), 256, 0, st>>>(
+        P.hslots, P.slots, P.slot_stride, n_pad_ * n_pad_, n_pad_, static_cast<int>(n_), o.h);
+  else
   dev::symmetrize_slots_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(P.hslots, P.slots, P.slot_stride, n_pad_ * n_pad_,
                                                                    n_pad_, static_cast<int>(n_), nb, o.h);
   after_launch(st);

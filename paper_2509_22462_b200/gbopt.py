@@ -74,6 +74,7 @@ _net_oracle = _fn("gbopt_net_oracle", _status, _vp, _dp, _sz, _dp, _sz, _dp, _dp
 _net_oracle_batched = _fn("gbopt_net_oracle_batched", _status, _vp, _sz, _dp, _sz, _dp, _sz, _dp, _dp, _dp)
 _net_oracle_batched_device = _fn("gbopt_net_oracle_batched_device", _status, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp,
                                  _vp, _vp)
+_net_oracle_lower = _fn("gbopt_net_oracle_lower", _status, _vp, _sz, _dp, _sz, _dp, _sz, _dp, _dp, _dp, _sz)
 _net_last_launch_count = _fn("gbopt_net_last_launch_count", _i64, _vp)
 _net_set_schedule = _fn("gbopt_net_set_schedule", _status, _vp, ctypes.c_int)
 _net_last_schedule = _fn("gbopt_net_last_schedule", ctypes.c_int, _vp)
@@ -347,6 +348,19 @@ class NeuralNet:
         _check(_net_oracle(self._h, _dptr(x), x.size, _dptr(lam), m if lam is None else lam.size,
                            _dptr(y), _dptr(j), _dptr(h)))
         return y, j, h
+
+    def oracle_lower(self, x, lam, want_y=True, want_j=True):
+        """(y, J, Hl) at one point with the Hessian as its packed lower triangle in
+        row order (Hl[a (a + 1) / 2 + c] = H[a, c], c <= a): the value order of the
+        reduced-space Lagrangian-Hessian callback, packed on the device."""
+        x, lam = _vec(x), _vec(lam)
+        n, m = self.input_dim, self.output_dim
+        y = np.empty(m) if want_y else None
+        j = np.empty((m, n)) if want_j else None
+        hl = np.empty(n * (n + 1) // 2)
+        _check(_net_oracle_lower(self._h, 1, _dptr(x), x.size, _dptr(lam), lam.size, _dptr(y), _dptr(j), _dptr(hl),
+                                 hl.size))
+        return y, j, hl
 
     def oracle_batched(self, X, Lam, want_y=True, want_j=True, want_h=True, out=None):
         """B independent points with the shared weights: X (B x n), Lam (B x m).

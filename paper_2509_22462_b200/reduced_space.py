@@ -81,9 +81,11 @@ class ReducedSpaceBlock:
         x = np.asarray(xb, dtype=np.float64)[:self.n]
         neg = -np.asarray(lam, dtype=np.float64)
         if self._hx is None or not np.array_equal(x, self._hx) or not np.array_equal(neg, self._hl):
-            y, j, h = self.net.oracle(x, neg)
-            self._y, self._j, self._h = y, j, h
+            # the device packs the lower triangle in the pattern's value order
+            # (a flipped (r, c) pattern entry has the same value: H is symmetric)
+            y, j, hv = self.net.oracle_lower(x, neg)
+            self._y, self._j, self._h = y, j, hv
             self._yx = self._jx = self._hx = x.copy()
             self._hl = neg.copy()
             self.evaluations += 1
-        return self._h[self.hess_rows, self.hess_cols]
+        return self._h.copy()

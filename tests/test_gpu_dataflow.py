@@ -161,3 +161,31 @@ def test_c2_dataflow_parity():
     assert orc.rel_err(j, ref.jacobian(wl.X[0])) <= TOL
     assert orc.rel_err(h, ref.lagrangian_hessian(wl.X[0], wl.Lam[0])) <= TOL
     assert np.array_equal(h, h.T)
+
+
+@pytest.mark.parametrize("schedule", ["layered", "dataflow"])
+@pytest.mark.parametrize("widths,hid,fin,seed", [
+    ([5, 7, 4], "tanh", "tanh", 1),
+    ([130, 200, 150, 12], "softplus", "linear", 2),
+    ([113, 129, 300, 129, 5], "sigmoid", "linear", 3),
+])
+def test_oracle_lower_packs_the_full_hessian(schedule, widths, hid, fin, seed):
+    """gbopt_net_oracle_lower: the Hessian packed on the device in the
+    reduced-space callback's value order equals the full Hessian's lower
+    triangle bit for bit (same kernels, only the epilogue differs), and y, J
+    match the full call."""
+    net = gb.random_net(widths, hid, fin, seed).set_schedule(schedule).bind_device(0)
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, widths[0])
+    lam = rng.normal(0, 1, widths[-1])
+    y, j, h = net.oracle(x, lam)
+    yl, jl, hl = net.oracle_lower(x, lam)
+    n = widths[0]
+    rows, cols = np.tril_indices(n)
+    assert np.array_equal(hl, h[rows, cols])
+    assert np.array_equal(yl, y) and np.array_equal(jl, j)
+    ref = to_oracle(net).lagrangian_hessian(x, lam)
+    assert orc.rel_err(hl, ref[rows, cols]) <= TOL
+    # Hessian only
+    _, _, hl2 = net.oracle_lower(x, lam, want_y=False, want_j=False)
+    assert np.array_equal(hl2, hl)
