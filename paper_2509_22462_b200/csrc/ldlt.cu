@@ -254,12 +254,13 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
     const size_t lbytes = sizeof(double) * static_cast<size_t>(n) * f->ldl_;
     CK(cudaMalloc(&f->d_l_, 2 * lbytes));  // L | W = L D
     CK(cudaMemsetAsync(f->d_l_, 0, 2 * lbytes, st));
-    // d | e | w | wr | z (solve scratch) | w2 | maxima (part, part3, part2; the solve's partials)
-    CK(cudaMalloc(&f->d_bk_, sizeof(double) * (6 * static_cast<size_t>(n) +
-                                                std::max<size_t>(6 * static_cast<size_t>(grid), 32 * bk::kSlices))));
     int solve_per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&solve_per_sm, bk::bk_solve_kernel, bk::kThreads, 0));
     f->solve_grid_ = std::max(1, std::min(sms * std::max(solve_per_sm, 1), 32 * bk::kSlices / bk::kWarps));
+    // d | e | w | wr | z (solve scratch) | w2 | maxima (part, part3, part2; the solve's partials)
+    CK(cudaMalloc(&f->d_bk_, sizeof(double) * (6 * static_cast<size_t>(n) +
+                                                std::max<size_t>({6 * static_cast<size_t>(grid), 32 * bk::kSlices,
+                                                                  32 * static_cast<size_t>(f->solve_grid_)}))));
     CK(cudaMalloc(&f->d_bki_, sizeof(int) * 2 * static_cast<size_t>(n)));
     bk_iota_kernel<<<blocks_for(n, 256), 256, 0, st>>>(f->d_bki_ + n, n);
     CK(cudaGetLastError());
@@ -371,7 +372,7 @@ void Ldlt::solve_factored(double* d_v) const {
   if (native_) {
     const double* d = d_bk_;
     double* z = d_bk_ + 4 * n_;
-    double* part = d_bk_ + 6 * n_;  // the factor's maxima slots, >= 32 * kSlices doubles
+    double* part = d_bk_ + 6 * n_;  // the factor's maxima slots, >= 32 * max(kSlices, solve grid) doubles
     const double* l = d_l_;
     int ldl = static_cast<int>(ldl_), n = static_cast<int>(n_);
     const double* e = d + n_;

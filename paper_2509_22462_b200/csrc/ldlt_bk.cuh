@@ -22,9 +22,10 @@
 //   index, and every reduction has a fixed order: the factorisation is
 //   deterministic.
 //
-// Solve (x = P^T L^-T D^-1 L^-1 P b): one CTA, forward / backward
-// substitution in 32-row blocks (block updates by the whole CTA, the 32 x 32
-// triangle by one warp), block-diagonal D in between.
+// Solve (x = P^T L^-T D^-1 L^-1 P b): one cooperative launch, forward /
+// backward substitution in 32-row blocks (block updates by the whole grid,
+// the 32 x 32 triangle by one warp from shared memory), block-diagonal D in
+// between.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -390,51 +391,79 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
 
 // x = P^T L^-T D^-1 L^-1 P b: one cooperative launch.  The substitutions
 // walk 32-row blocks; each block's update from the rows already solved is
-// spread over every warp of the grid (partials per (row, warp slice), summed
-// in a fixed order), then one warp solves the 32 x 32 triangle; two grid
-// barriers per block.
-constexpr int kSlices = 64;  // warp slices per row of a block update
+// spread over every warp of the grid (fixed-order partial sums), then CTA 0
+// reduces the partials and one warp solves the 32 x 32 triangle from shared
+// memory (the diagonal tile is staged before the barrier, so its loads
+// overlap the partial sums); two grid barriers per block.
+//   forward  (row rr of the block, lanes along columns j < b0):
+//            tasks (rr, slice), part[rr * kSlices + slice]
+//   backward (column c = lane of the block, warps along rows j >= b1):
+//            per-CTA sums, part[cta * 32 + c]
+constexpr int kSlices = 64;  // warp slices per row of a forward block update
+
+__device__ __forceinline__ void stage_diag_tile(const double* __restrict__ l, int ldl, int b0, int rows, int lane,
+                                                double (*tile)[33]) {
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r)
+    tile[r][lane] = (r < rows && lane < rows) ? __ldcg(l + static_cast<int64_t>(b0 + r) * ldl + b0 + lane) : 0.0;
+}
 
 __global__ void __launch_bounds__(kThreads) bk_solve_kernel(const double* __restrict__ l, int ldl,
                                                             const double* __restrict__ d, const double* __restrict__ e,
                                                             const int* __restrict__ piv, const int* __restrict__ perm,
                                                             int n, const double* b, double* z, double* x,
-                                                            double* part /* [32][kSlices] */) {
+                                                            double* part /* >= max(32 kSlices, 32 grid) */) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ double tile[32][33];
+  __shared__ double red[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
+  const bool lead = blockIdx.x == 0;
   // z = P b
   for (int i = tid; i < n; i += nt) z[i] = b[perm[i]];
   grid.sync();
   // ---- forward: L z = P b (unit lower) ----
   for (int b0 = 0; b0 < n; b0 += 32) {
     const int rows = min(32, n - b0);
+    if (lead && warp == 0) stage_diag_tile(l, ldl, b0, rows, lane, tile);
     // task (rr, sl): row b0 + rr, columns j = sl * 32 + lane + 32 * kSlices * t < b0
     for (int task = gw; task < 32 * kSlices; task += nw) {
       const int rr = task / kSlices, sl = task % kSlices;
-      double s = 0.0;
+      double s0 = 0.0, s1 = 0.0;
       if (rr < rows) {
         const double* li = l + static_cast<int64_t>(b0 + rr) * ldl;
-        for (int j = sl * 32 + lane; j < b0; j += 32 * kSlices) s = fma(__ldcg(li + j), __ldcg(z + j), s);
+        int j = sl * 32 + lane;
+        for (; j + 32 * kSlices < b0; j += 64 * kSlices) {
+          s0 = fma(__ldcg(li + j), __ldcg(z + j), s0);
+          s1 = fma(__ldcg(li + j + 32 * kSlices), __ldcg(z + j + 32 * kSlices), s1);
+        }
+        if (j < b0) s0 = fma(__ldcg(li + j), __ldcg(z + j), s0);
       }
+      double s = s0 + s1;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) part[task] = s;
     }
     grid.sync();
-    if (blockIdx.x == 0 && warp == 0) {
-      double zi = 0.0;
-      if (lane < rows) {
-        double s = 0.0;
-        for (int sl = 0; sl < kSlices; ++sl) s += __ldcg(part + lane * kSlices + sl);  // fixed order
-        zi = __ldcg(z + b0 + lane) - s;
+    if (lead) {
+      // warp w sums slices [8w, 8w + 8) of row `lane`; warp 0 the warps (fixed order)
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kSlices / kWarps; ++q) s += __ldcg(part + lane * kSlices + warp * (kSlices / kWarps) + q);
+      red[warp][lane] = s;
+      __syncthreads();
+      if (warp == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) t += red[w][lane];
+        double zi = lane < rows ? __ldcg(z + b0 + lane) - t : 0.0;
+        for (int j = 0; j < rows; ++j) {
+          const double zj = __shfl_sync(0xffffffffu, zi, j);
+          if (lane > j) zi -= tile[lane][j] * zj;
+        }
+        if (lane < rows) z[b0 + lane] = zi;
       }
-      for (int j = 0; j < rows; ++j) {
-        const double zj = __shfl_sync(0xffffffffu, zi, j);
-        if (lane > j && lane < rows) zi -= __ldcg(l + static_cast<int64_t>(b0 + lane) * ldl + b0 + j) * zj;
-      }
-      if (lane < rows) z[b0 + lane] = zi;
     }
     grid.sync();
   }
@@ -456,30 +485,43 @@ __global__ void __launch_bounds__(kThreads) bk_solve_kernel(const double* __rest
   const int nblk = (n + 31) / 32;
   for (int bi = nblk - 1; bi >= 0; --bi) {
     const int b0 = bi * 32, b1 = min(n, b0 + 32), rows = b1 - b0;
-    // task (c, sl): column b0 + c of L over rows j >= b1 -- lanes take rows
-    for (int task = gw; task < 32 * kSlices; task += nw) {
-      const int c = task / kSlices, sl = task % kSlices;
-      double s = 0.0;
-      if (c < rows)
-        for (int j = b1 + sl * 32 + lane; j < n; j += 32 * kSlices)
-          s = fma(__ldcg(l + static_cast<int64_t>(j) * ldl + b0 + c), __ldcg(x + j), s);
+    if (lead && warp == 0) stage_diag_tile(l, ldl, b0, rows, lane, tile);
+    // column b0 + lane of L over rows j >= b1, rows strided over the grid's warps
+    double s0 = 0.0, s1 = 0.0;
+    if (lane < rows) {
+      int j = b1 + gw;
+      for (; j + nw < n; j += 2 * nw) {
+        s0 = fma(__ldcg(l + static_cast<int64_t>(j) * ldl + b0 + lane), __ldcg(x + j), s0);
+        s1 = fma(__ldcg(l + static_cast<int64_t>(j + nw) * ldl + b0 + lane), __ldcg(x + j + nw), s1);
+      }
+      if (j < n) s0 = fma(__ldcg(l + static_cast<int64_t>(j) * ldl + b0 + lane), __ldcg(x + j), s0);
+    }
+    red[warp][lane] = s0 + s1;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) part[task] = s;
+      for (int w = 0; w < kWarps; ++w) t += red[w][lane];
+      part[blockIdx.x * 32 + lane] = t;
     }
     grid.sync();
-    if (blockIdx.x == 0 && warp == 0) {
-      double yi = 0.0;
-      if (lane < rows) {
-        double s = 0.0;
-        for (int sl = 0; sl < kSlices; ++sl) s += __ldcg(part + lane * kSlices + sl);
-        yi = __ldcg(x + b0 + lane) - s;
+    if (lead) {
+      const int g = gridDim.x;
+      double s = 0.0;
+      for (int q = warp; q < g; q += kWarps) s += __ldcg(part + q * 32 + lane);
+      red[warp][lane] = s;
+      __syncthreads();
+      if (warp == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) t += red[w][lane];
+        double yi = lane < rows ? __ldcg(x + b0 + lane) - t : 0.0;
+        for (int j = rows - 1; j >= 0; --j) {
+          const double yj = __shfl_sync(0xffffffffu, yi, j);
+          if (lane < j) yi -= tile[j][lane] * yj;
+        }
+        if (lane < rows) x[b0 + lane] = yi;
       }
-      for (int j = rows - 1; j >= 0; --j) {
-        const double yj = __shfl_sync(0xffffffffu, yi, j);
-        if (lane < j) yi -= __ldcg(l + static_cast<int64_t>(b0 + j) * ldl + b0 + lane) * yj;
-      }
-      if (lane < rows) x[b0 + lane] = yi;
     }
     grid.sync();
   }

@@ -6,8 +6,9 @@ def kkt(n, m, seed):
     H = rng.uniform(-1, 1, (n, n)); H = 0.5 * (H + H.T) + np.diag(10.0 ** rng.uniform(-2, 6, n))
     J = rng.uniform(-1, 1, (m, n))
     return np.block([[H, J.T], [J, -1e-8 * np.eye(m)]]), rng.uniform(-1, 1, n + m)
-for n in (784, 2000, 4000, 8000):
-    K, b = kkt(n, n // 8, n)
-    f = gb.ldlt_factor(K); f.solve(b)
-    t0 = time.perf_counter(); f = gb.ldlt_factor(K); t1 = time.perf_counter(); x = f.solve(b); t2 = time.perf_counter()
-    print(K.shape[0], "factor %.2f ms solve %.2f ms" % ((t1 - t0) * 1e3, (t2 - t1) * 1e3), "resid", np.abs(K @ x - b).max())
+if __name__ == "__main__":
+  for n in [int(v) for v in sys.argv[1:]] or (784, 2000, 4000, 8000):
+      K, b = kkt(n, n // 8, n)
+      f = gb.ldlt_factor(K); f.solve(b)
+      t0 = time.perf_counter(); f = gb.ldlt_factor(K); t1 = time.perf_counter(); x = f.solve(b); t2 = time.perf_counter()
+      print(K.shape[0], "factor %.2f ms solve %.2f ms" % ((t1 - t0) * 1e3, (t2 - t1) * 1e3), "resid", np.abs(K @ x - b).max())
