@@ -298,6 +298,57 @@ gbopt_status gbopt_ldlt_solve(const gbopt_ldlt* f, const double* b, size_t n,
                               double* x);
 void gbopt_ldlt_free(gbopt_ldlt* f);
 
+/* ---- KKT assembly and inertia correction -------------
+ * The reference assembles the IPM's dense Newton system in C++ only
+ * (assemble_kkt / inertia_correct, proj/include/gbopt/ipm.hpp:80-118,
+ * proj/src/ipm.cpp:466-557) -- no C entry exists; these are the C-ABI form,
+ * with the system kept on the device between the calls.
+ *
+ * gbopt_kkt_create analyses one NLP's pattern once: n variables, m
+ * constraints, the Lagrangian-Hessian triplets (hess_rows/cols, nnz_h;
+ * mirrored, duplicates summed) and the Jacobian triplets (jac_rows/cols,
+ * nnz_j).  An index out of range is GBOPT_ERR_STRUCTURAL.
+ *
+ * gbopt_kkt_assemble (assemble_kkt, ipm.cpp:466-518) scatters one
+ * iteration's values: x, lower (-inf = unbounded), z, grad_f: n entries;
+ * lambda, g: m; hess_values: nnz_h; jac_values: nnz_j.  The matrix
+ * [[H + Sigma + delta_w I, J^T], [J, -delta_c I]] (Sigma_ii = z_i / (x_i -
+ * lower_i) on bounded rows) and rhs [-grad_f - J^T lambda + mu / (x -
+ * lower); -g] equal the reference's bit for bit (same additions in the same
+ * order; products rounded separately).
+ *
+ * gbopt_kkt_matrix / gbopt_kkt_rhs copy them out ((n+m)^2 row-major / n+m).
+ *
+ * gbopt_kkt_inertia_correct (inertia_correct, ipm.cpp:520-557) factors
+ * the device-resident matrix with delta_w = delta_w_start, then delta0, then
+ * *= delta_growth (and delta_c = 1e-8 .. 1e-2 while zero pivots persist with
+ * m > 0) until the inertia is (n, m, 0); the factorisation (keep_input on)
+ * goes to *fact (free with gbopt_ldlt_free), the shifts to *delta_w and
+ * *delta_c.  GBOPT_ERR_SINGULAR once delta_w exceeds delta_max.
+ *
+ * gbopt_kkt_solve: fact.solve(rhs) with the assembled right-hand side
+ * (sol: n + m entries). */
+typedef struct gbopt_kkt gbopt_kkt;
+gbopt_status gbopt_kkt_create(size_t n, size_t m, const int64_t* hess_rows,
+                              const int64_t* hess_cols, size_t nnz_h,
+                              const int64_t* jac_rows, const int64_t* jac_cols,
+                              size_t nnz_j, gbopt_kkt** out);
+gbopt_status gbopt_kkt_assemble(gbopt_kkt* kkt, const double* x,
+                                const double* lower, const double* z,
+                                const double* lambda, const double* grad_f,
+                                const double* g, const double* jac_values,
+                                const double* hess_values, double mu,
+                                double delta_w, double delta_c);
+gbopt_status gbopt_kkt_matrix(const gbopt_kkt* kkt, double* out, size_t len);
+gbopt_status gbopt_kkt_rhs(const gbopt_kkt* kkt, double* out, size_t len);
+gbopt_status gbopt_kkt_inertia_correct(const gbopt_kkt* kkt, double delta0,
+                                       double delta_growth, double delta_max,
+                                       double delta_w_start, gbopt_ldlt** fact,
+                                       double* delta_w, double* delta_c);
+gbopt_status gbopt_kkt_solve(const gbopt_kkt* kkt, const gbopt_ldlt* fact,
+                             double* sol, size_t len);
+void gbopt_kkt_free(gbopt_kkt* kkt);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

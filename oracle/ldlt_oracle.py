@@ -71,3 +71,68 @@ def matrix_with_spectrum(rng, eigs):
     q = q * np.sign(np.diag(r))[None, :]
     a = q @ np.diag(eigs) @ q.T
     return 0.5 * (a + a.T)
+
+
+# ---- KKT assembly and inertia correction (ipm.cpp:466-557) ----------------
+
+K_DELTA_C = 1e-8      # ipm.cpp:23
+K_DELTA_C_MAX = 1e-2  # ipm.cpp:24
+
+
+def assemble_kkt(x, lower, z, lam, grad_f, g, jac_rows, jac_cols, jac_values, hess_rows, hess_cols, hess_values,
+                 mu, delta_w=0.0, delta_c=0.0):
+    """ipm.cpp:466-518, element by element in the reference's order: the
+    Hessian triplets (mirrored off the diagonal), then Sigma and delta_w on
+    the (1,1) diagonal, then the Jacobian triplets into both off-diagonal
+    blocks, then -delta_c; rhs = [-grad_f - J^T lambda (+ mu / (x - lower));
+    -g] with J^T lambda as jac_t_lambda (ipm.cpp:33-42).  Python floats:
+    every operation rounds once, like the reference built without FMA
+    contraction.  Returns (mat, rhs)."""
+    x, lower, z = (np.asarray(v, dtype=np.float64) for v in (x, lower, z))
+    n, m = x.size, np.asarray(g).size
+    mat = [[0.0] * (n + m) for _ in range(n + m)]
+    for r, c, v in zip(hess_rows, hess_cols, hess_values):
+        mat[r][c] += float(v)
+        if r != c:
+            mat[c][r] += float(v)
+    for i in range(n):
+        if np.isfinite(lower[i]):
+            mat[i][i] += float(z[i]) / (float(x[i]) - float(lower[i]))
+        if delta_w != 0.0:
+            mat[i][i] += delta_w
+    for r, c, v in zip(jac_rows, jac_cols, jac_values):
+        mat[n + r][c] += float(v)
+        mat[c][n + r] += float(v)
+    if delta_c != 0.0:
+        for i in range(m):
+            mat[n + i][n + i] -= delta_c
+    jt = [0.0] * n
+    for r, c, v in zip(jac_rows, jac_cols, jac_values):
+        jt[c] += float(v) * float(lam[r])
+    rhs = [-float(grad_f[i]) - jt[i] for i in range(n)]
+    for i in range(n):
+        if np.isfinite(lower[i]):
+            rhs[i] += mu / (float(x[i]) - float(lower[i]))
+    rhs += [-float(v) for v in g]
+    return np.array(mat, dtype=np.float64).reshape(n + m, n + m), np.array(rhs, dtype=np.float64)
+
+
+def inertia_correct(mat, n, m, delta0=1e-4, delta_growth=10.0, delta_max=1e40, delta_w_start=0.0):
+    """ipm.cpp:520-557 with this module's inertia(): returns (delta_w,
+    delta_c, inertia) of the first shifted matrix with inertia (n, m, 0)."""
+    delta_w, delta_c = delta_w_start, 0.0
+    while True:
+        t = np.array(mat, dtype=np.float64, copy=True)
+        if delta_w != 0.0:
+            t[np.arange(n), np.arange(n)] += delta_w
+        if delta_c != 0.0:
+            t[n + np.arange(m), n + np.arange(m)] -= delta_c
+        got = inertia(t)
+        if got == (n, m, 0):
+            return delta_w, delta_c, got
+        if got[2] > 0 and m > 0 and delta_c < K_DELTA_C_MAX:
+            delta_c = K_DELTA_C if delta_c == 0.0 else delta_c * 1e2
+            continue
+        delta_w = delta0 if delta_w == 0.0 else delta_w * delta_growth
+        if delta_w > delta_max:
+            raise OracleError("inertia correction: regularization exceeded the configured maximum")

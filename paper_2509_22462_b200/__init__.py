@@ -10,5 +10,6 @@ from .gbopt import (  # noqa: F401
     GboptError, StructuralError, NumericError, SingularError, IoError, FormatError, DimensionError,
     TruncatedError, RangeError, ArgumentError, DeviceError,
     NeuralNet, Prng, load_weights, save_weights, random_net, random_net_ex, LdltFactorization, ldlt_factor,
+    KktPattern, KktSystem, assemble_kkt, IpmOptions, CorrectedFactorization, inertia_correct,
     device_count, last_error, version, LIB_PATH,
 )

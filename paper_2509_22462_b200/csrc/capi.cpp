@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "device_net.hpp"
+#include "kkt.hpp"
 #include "ldlt.hpp"
 #include "net.hpp"
 
@@ -29,6 +30,10 @@ struct gbopt_prng {
 
 struct gbopt_ldlt {
   std::unique_ptr<gbb::Ldlt> f;
+};
+
+struct gbopt_kkt {
+  std::unique_ptr<gbb::Kkt> k;
 };
 
 namespace {
@@ -449,5 +454,75 @@ gbopt_status gbopt_ldlt_solve(const gbopt_ldlt* f, const double* b, size_t n, do
 }
 
 void gbopt_ldlt_free(gbopt_ldlt* f) { delete f; }
+
+/* ---- KKT assembly and inertia correction ---------------------------------- */
+
+gbopt_status gbopt_kkt_create(size_t n, size_t m, const int64_t* hess_rows, const int64_t* hess_cols, size_t nnz_h,
+                              const int64_t* jac_rows, const int64_t* jac_cols, size_t nnz_j, gbopt_kkt** out) {
+  if (out == nullptr || ((hess_rows == nullptr || hess_cols == nullptr) && nnz_h > 0) ||
+      ((jac_rows == nullptr || jac_cols == nullptr) && nnz_j > 0))
+    return fail_argument("gbopt_kkt_create: null argument");
+  return guarded([&] {
+    auto h = std::make_unique<gbopt_kkt>();
+    h->k = std::make_unique<gbb::Kkt>(static_cast<int64_t>(n), static_cast<int64_t>(m), hess_rows, hess_cols, nnz_h,
+                                      jac_rows, jac_cols, nnz_j);
+    *out = h.release();
+  });
+}
+
+gbopt_status gbopt_kkt_assemble(gbopt_kkt* kkt, const double* x, const double* lower, const double* z,
+                                const double* lambda, const double* grad_f, const double* g, const double* jac_values,
+                                const double* hess_values, double mu, double delta_w, double delta_c) {
+  if (kkt == nullptr) return fail_argument("gbopt_kkt_assemble: null system");
+  const auto& k = *kkt->k;
+  const bool nv = k.n_var() > 0, mv = k.n_con() > 0;
+  if ((nv && (!x || !lower || !z || !grad_f)) || (mv && (!lambda || !g)) || (k.nnz_h() > 0 && !hess_values) ||
+      (k.nnz_j() > 0 && !jac_values))
+    return fail_argument("gbopt_kkt_assemble: null argument");
+  return guarded([&] {
+    kkt->k->assemble(x, lower, z, lambda, grad_f, g, jac_values, hess_values, mu, delta_w, delta_c);
+  });
+}
+
+gbopt_status gbopt_kkt_matrix(const gbopt_kkt* kkt, double* out, size_t len) {
+  if (kkt == nullptr) return fail_argument("gbopt_kkt_matrix: null system");
+  const size_t dim = static_cast<size_t>(kkt->k->dim());
+  if (len != dim * dim || (out == nullptr && len > 0)) return fail_argument("gbopt_kkt_matrix: out must hold (n+m)^2");
+  return guarded([&] { kkt->k->matrix(out); });
+}
+
+gbopt_status gbopt_kkt_rhs(const gbopt_kkt* kkt, double* out, size_t len) {
+  if (kkt == nullptr) return fail_argument("gbopt_kkt_rhs: null system");
+  if (len != static_cast<size_t>(kkt->k->dim()) || (out == nullptr && len > 0))
+    return fail_argument("gbopt_kkt_rhs: out must hold n+m");
+  return guarded([&] { kkt->k->rhs(out); });
+}
+
+gbopt_status gbopt_kkt_inertia_correct(const gbopt_kkt* kkt, double delta0, double delta_growth, double delta_max,
+                                       double delta_w_start, gbopt_ldlt** fact, double* delta_w, double* delta_c) {
+  if (kkt == nullptr || fact == nullptr) return fail_argument("gbopt_kkt_inertia_correct: null argument");
+  if (!(delta_growth > 1.0)) return fail_argument("gbopt_kkt_inertia_correct: delta_growth must be > 1");
+  return guarded([&] {
+    auto c = kkt->k->inertia_correct(delta0, delta_growth, delta_max, delta_w_start);
+    auto h = std::make_unique<gbopt_ldlt>();
+    h->f = std::move(c.fact);
+    if (delta_w) *delta_w = c.delta_w;
+    if (delta_c) *delta_c = c.delta_c;
+    *fact = h.release();
+  });
+}
+
+gbopt_status gbopt_kkt_solve(const gbopt_kkt* kkt, const gbopt_ldlt* fact, double* sol, size_t len) {
+  if (kkt == nullptr || fact == nullptr) return fail_argument("gbopt_kkt_solve: null argument");
+  if (len != static_cast<size_t>(kkt->k->dim()) || (sol == nullptr && len > 0))
+    return fail_argument("gbopt_kkt_solve: sol must hold n+m");
+  if (fact->f->dim() != kkt->k->dim()) return fail_argument("gbopt_kkt_solve: factorization of another size");
+  return guarded([&] {
+    const std::vector<double> r = kkt->k->solve(*fact->f);
+    std::copy(r.begin(), r.end(), sol);
+  });
+}
+
+void gbopt_kkt_free(gbopt_kkt* kkt) { delete kkt; }
 
 }  // extern "C"

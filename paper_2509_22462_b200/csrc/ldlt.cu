@@ -113,6 +113,19 @@ __global__ void ldlt_residual_kernel(const double* __restrict__ a, int64_t n, co
   }
 }
 
+// A(i, i) += delta_w for i < n_var; A(i, i) -= delta_c for i >= n_var
+// (each only when non-zero)
+__global__ void ldlt_shift_diag_kernel(double* __restrict__ a, int64_t n, int64_t n_var, double delta_w,
+                                       double delta_c) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i < n_var) {
+    if (delta_w != 0.0) a[i * n + i] += delta_w;
+  } else if (delta_c != 0.0) {
+    a[i * n + i] -= delta_c;
+  }
+}
+
 int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t>((work + per - 1) / per, 4096)); }
 
 }  // namespace
@@ -152,6 +165,16 @@ Ldlt::~Ldlt() {
 }
 
 std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, int device) {
+  return factor_impl(a, false, n, n, 0.0, 0.0, keep_input, device, nullptr);
+}
+
+std::unique_ptr<Ldlt> Ldlt::factor_device(const double* d_a, int64_t n, int64_t n_var, double delta_w,
+                                          double delta_c, bool keep_input, int device, cudaStream_t src) {
+  return factor_impl(d_a, true, n, n_var, delta_w, delta_c, keep_input, device, src);
+}
+
+std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t n, int64_t n_var, double delta_w,
+                                        double delta_c, bool keep_input, int device, cudaStream_t src) {
   if (n < 0) throw StructuralError("ldlt_factor: negative dimension");
   auto f = std::unique_ptr<Ldlt>(new Ldlt());
   f->n_ = n;
@@ -177,7 +200,18 @@ std::unique_ptr<Ldlt> Ldlt::factor(const double* a, int64_t n, bool keep_input, 
   CK(cudaMalloc(&f->d_fact_, bytes));
   CK(cudaMalloc(&f->d_vec_, sizeof(double) * (4 * n + 8)));  // rs | scale | cmax | x ... | scalars
   CK(cudaMalloc(&f->d_rhs_, sizeof(double) * n));
-  CK(cudaMemcpyAsync(f->d_fact_, a, bytes, cudaMemcpyHostToDevice, st));
+  if (on_device) {
+    // try_mat = A + delta_w I (head) - delta_c I (tail), ipm.cpp:529-536:
+    // the shifts only when non-zero, one rounding each, as the reference
+    if (src) CK(cudaStreamSynchronize(src));
+    CK(cudaMemcpyAsync(f->d_fact_, a, bytes, cudaMemcpyDeviceToDevice, st));
+    if (delta_w != 0.0 || delta_c != 0.0) {
+      ldlt_shift_diag_kernel<<<blocks_for(n, 256), 256, 0, st>>>(f->d_fact_, n, n_var, delta_w, delta_c);
+      CK(cudaGetLastError());
+    }
+  } else {
+    CK(cudaMemcpyAsync(f->d_fact_, a, bytes, cudaMemcpyHostToDevice, st));
+  }
   double* rs = f->d_vec_;
   double* scale = rs + n;
   double* cmax = scale + n;
@@ -397,13 +431,33 @@ std::vector<double> Ldlt::solve(const double* b, int64_t len) const {
                           std::to_string(n_));
   if (n_zero_ > 0)
     throw SingularError("ldlt_solve: matrix is singular (" + std::to_string(n_zero_) + " zero pivots)");
+  std::vector<double> bs(static_cast<size_t>(n_));
+  for (int64_t i = 0; i < n_; ++i) bs[i] = scale_[i] * b[i];
+  return solve_scaled(std::move(bs));
+}
+
+std::vector<double> Ldlt::solve_device(const double* d_b, int64_t len, cudaStream_t src) const {
+  if (len != n_)
+    throw StructuralError("ldlt_solve: right-hand side has size " + std::to_string(len) + ", expected " +
+                          std::to_string(n_));
+  if (n_zero_ > 0)
+    throw SingularError("ldlt_solve: matrix is singular (" + std::to_string(n_zero_) + " zero pivots)");
+  std::vector<double> b(static_cast<size_t>(n_));
+  if (n_ > 0) {
+    DeviceGuard g(dev_);
+    CK(cudaMemcpyAsync(b.data(), d_b, sizeof(double) * n_, cudaMemcpyDeviceToHost, src));
+    CK(cudaStreamSynchronize(src));
+  }
+  return solve(b.data(), len);
+}
+
+// x = S (S A S)^{-1} bs for bs = S b (host), refined as the reference
+std::vector<double> Ldlt::solve_scaled(std::vector<double> bs) const {
   const int64_t n = n_;
   std::vector<double> x(static_cast<size_t>(n));
   if (n == 0) return x;
   DeviceGuard g(dev_);
   cudaStream_t st = stream_;
-  std::vector<double> bs(static_cast<size_t>(n));
-  for (int64_t i = 0; i < n; ++i) bs[i] = scale_[i] * b[i];
   double b_norm = 0.0;
   for (double v : bs) b_norm = std::max(b_norm, std::fabs(v));
   double* d_bs = d_vec_;            // reuse: rs slot

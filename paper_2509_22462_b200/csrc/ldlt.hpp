@@ -18,6 +18,12 @@ class Ldlt {
   // `device` (-1: current).  keep_input retains the equilibrated matrix on
   // the device for iterative refinement in solve().
   static std::unique_ptr<Ldlt> factor(const double* a, int64_t n, bool keep_input, int device = -1);
+  // The same from a device-resident row-major matrix `d_a` (left unchanged),
+  // factoring d_a + delta_w I (first n_var rows) - delta_c I (the rest): the
+  // reference's inertia-correction trial matrix (ipm.cpp:529-536).  `src`
+  // is the stream that produced d_a; the factorisation waits for it.
+  static std::unique_ptr<Ldlt> factor_device(const double* d_a, int64_t n, int64_t n_var, double delta_w,
+                                             double delta_c, bool keep_input, int device, cudaStream_t src);
   ~Ldlt();
   Ldlt(const Ldlt&) = delete;
   Ldlt& operator=(const Ldlt&) = delete;
@@ -27,9 +33,15 @@ class Ldlt {
   int64_t n_neg() const { return n_neg_; }
   int64_t n_zero() const { return n_zero_; }
   std::vector<double> solve(const double* b, int64_t len) const;
+  // solve with a device-resident right-hand side (len == dim(); `src` is
+  // the stream that produced it), the result in host memory
+  std::vector<double> solve_device(const double* d_b, int64_t len, cudaStream_t src) const;
 
  private:
   Ldlt() = default;
+  static std::unique_ptr<Ldlt> factor_impl(const double* a, bool on_device, int64_t n, int64_t n_var, double delta_w,
+                                           double delta_c, bool keep_input, int device, cudaStream_t src);
+  std::vector<double> solve_scaled(std::vector<double> bs) const;
   void solve_factored(double* d_v) const;
   void refine_add_kernel_launch(double* d_x, const double* d_r, int64_t n, cudaStream_t st) const;
 

@@ -90,6 +90,16 @@ _ldlt_factor = _fn("gbopt_ldlt_factor", _status, _dp, _sz, ctypes.c_int, ctypes.
 _ldlt_inertia = _fn("gbopt_ldlt_inertia", _status, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64))
 _ldlt_solve = _fn("gbopt_ldlt_solve", _status, _vp, _dp, _sz, _dp)
 _ldlt_free = _fn("gbopt_ldlt_free", None, _vp)
+_i64p = ctypes.POINTER(_i64)
+_kkt_create = _fn("gbopt_kkt_create", _status, _sz, _sz, _i64p, _i64p, _sz, _i64p, _i64p, _sz, ctypes.POINTER(_vp))
+_kkt_assemble = _fn("gbopt_kkt_assemble", _status, _vp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, ctypes.c_double,
+                    ctypes.c_double, ctypes.c_double)
+_kkt_matrix = _fn("gbopt_kkt_matrix", _status, _vp, _dp, _sz)
+_kkt_rhs = _fn("gbopt_kkt_rhs", _status, _vp, _dp, _sz)
+_kkt_inertia_correct = _fn("gbopt_kkt_inertia_correct", _status, _vp, ctypes.c_double, ctypes.c_double,
+                           ctypes.c_double, ctypes.c_double, ctypes.POINTER(_vp), _dp, _dp)
+_kkt_solve = _fn("gbopt_kkt_solve", _status, _vp, _vp, _dp, _sz)
+_kkt_free = _fn("gbopt_kkt_free", None, _vp)
 _net_debug_intermediate = _fn("gbopt_net_debug_intermediate", _status, _vp, ctypes.c_char_p, _i64, _sz, _dp, _sz)
 
 # ---------------------------------------------------------------------------
@@ -472,6 +482,117 @@ class LdltFactorization:
 
 def ldlt_factor(A, keep_input: bool = True) -> LdltFactorization:
     return LdltFactorization(A, keep_input)
+
+
+def _idx(v):
+    return np.ascontiguousarray(np.asarray(v, dtype=np.int64).reshape(-1))
+
+
+def _ip(a):
+    return a.ctypes.data_as(_i64p) if a.size else None
+
+
+class KktPattern:
+    """One NLP's KKT sparsity (Lagrangian-Hessian and Jacobian triplets),
+    analysed once; assemble() then builds each IPM iteration's dense Newton
+    system on the device (gbopt_kkt_*; reference assemble_kkt,
+    proj/src/ipm.cpp:466-518)."""
+
+    def __init__(self, n: int, m: int, hess_rows, hess_cols, jac_rows, jac_cols):
+        hr, hc, jr, jc = _idx(hess_rows), _idx(hess_cols), _idx(jac_rows), _idx(jac_cols)
+        if hr.size != hc.size or jr.size != jc.size:
+            raise StructuralError("kkt: row and column triplet lists differ in length")
+        h = _vp()
+        _check(_kkt_create(n, m, _ip(hr), _ip(hc), hr.size, _ip(jr), _ip(jc), jr.size, ctypes.byref(h)))
+        self._h = h
+        self.n_var, self.n_con = int(n), int(m)
+        self.nnz_h, self.nnz_j = hr.size, jr.size
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _kkt_free(h)
+            self._h = None
+
+    def assemble(self, x, lower, z, lam, grad_f, g, jac_values, hess_values, mu, delta_w=0.0, delta_c=0.0):
+        n, m = self.n_var, self.n_con
+        args = []
+        for name, v, size in (("x", x, n), ("lower", lower, n), ("z", z, n), ("lambda", lam, m),
+                              ("grad_f", grad_f, n), ("g", g, m), ("jac_values", jac_values, self.nnz_j),
+                              ("hess_values", hess_values, self.nnz_h)):
+            a = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+            if a.size != size:
+                raise StructuralError(f"assemble_kkt: {name} has size {a.size}, expected {size}")
+            args.append(a)
+        self._keep = args
+        _check(_kkt_assemble(self._h, *[_dptr(a) if a.size else None for a in args], float(mu), float(delta_w),
+                             float(delta_c)))
+        return KktSystem(self)
+
+
+class KktSystem:
+    """The assembled system, resident on the device (reference KktSystem,
+    proj/include/gbopt/ipm.hpp:80-87); .mat / .rhs copy it out."""
+
+    def __init__(self, pattern: KktPattern):
+        self.pattern = pattern
+        self.n_var, self.n_con = pattern.n_var, pattern.n_con
+
+    @property
+    def mat(self):
+        d = self.n_var + self.n_con
+        out = np.empty((d, d))
+        _check(_kkt_matrix(self.pattern._h, _dptr(out), out.size))
+        return out
+
+    @property
+    def rhs(self):
+        out = np.empty(self.n_var + self.n_con)
+        _check(_kkt_rhs(self.pattern._h, _dptr(out), out.size))
+        return out
+
+    def solve(self, fact: "LdltFactorization"):
+        """fact.solve(rhs) with the device-resident right-hand side."""
+        out = np.empty(self.n_var + self.n_con)
+        _check(_kkt_solve(self.pattern._h, fact._h, _dptr(out), out.size))
+        return out
+
+
+def assemble_kkt(x, lower, z, lam, grad_f, g, jac_rows, jac_cols, jac_values, hess_rows, hess_cols, hess_values, mu,
+                 delta_w=0.0, delta_c=0.0) -> KktSystem:
+    """Reference assemble_kkt (proj/include/gbopt/ipm.hpp:89-102) with the
+    same argument order; the pattern analysis is redone per call (use
+    KktPattern across iterations)."""
+    n, m = np.asarray(x).size, np.asarray(g).size
+    pat = KktPattern(n, m, hess_rows, hess_cols, jac_rows, jac_cols)
+    return pat.assemble(x, lower, z, lam, grad_f, g, jac_values, hess_values, mu, delta_w, delta_c)
+
+
+class IpmOptions:
+    """The regularisation fields of the reference IpmOptions
+    (proj/include/gbopt/ipm.hpp:21-23)."""
+
+    def __init__(self, delta0=1e-4, delta_growth=10.0, delta_max=1e40):
+        self.delta0, self.delta_growth, self.delta_max = delta0, delta_growth, delta_max
+
+
+class CorrectedFactorization:
+    def __init__(self, fact, delta_w, delta_c):
+        self.fact, self.delta_w, self.delta_c = fact, delta_w, delta_c
+
+
+def inertia_correct(kkt: KktSystem, opts: IpmOptions = None, delta_w_start: float = 0.0) -> CorrectedFactorization:
+    """Reference inertia_correct (proj/src/ipm.cpp:520-557) on the device-
+    resident matrix: SingularError once delta_w exceeds opts.delta_max."""
+    opts = opts or IpmOptions()
+    h = _vp()
+    dw, dc = ctypes.c_double(), ctypes.c_double()
+    _check(_kkt_inertia_correct(kkt.pattern._h, opts.delta0, opts.delta_growth, opts.delta_max, delta_w_start,
+                                ctypes.byref(h), ctypes.byref(dw), ctypes.byref(dc)))
+    f = LdltFactorization.__new__(LdltFactorization)
+    f._h = h
+    f.dim = kkt.n_var + kkt.n_con
+    return CorrectedFactorization(f, dw.value, dc.value)
 
 
 def load_weights(path: str) -> NeuralNet:
