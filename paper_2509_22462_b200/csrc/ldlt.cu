@@ -27,12 +27,15 @@
 #include <cstdlib>
 #include <cmath>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "device_net.hpp"
 #include "ldlt.hpp"
 #include "ldlt_bk.cuh"
+#include "ldlt_bkc.cuh"
 
 namespace gbb {
 
@@ -126,6 +129,57 @@ __global__ void ldlt_shift_diag_kernel(double* __restrict__ a, int64_t n, int64_
   }
 }
 
+// Device buffers of finished factorisations are kept for reuse (exact size
+// match, per device, up to kPoolCap bytes): the IPM's inertia correction
+// factors same-sized trial matrices back to back, and cudaMalloc / cudaFree
+// of the multi-MB buffers cost more than a small factorisation's kernels.
+struct BufPool {
+  std::mutex m;
+  std::multimap<std::pair<int, size_t>, void*> free;
+  size_t cached = 0;
+};
+constexpr size_t kPoolCap = size_t(4) << 30;
+BufPool& buf_pool() {
+  static BufPool* pool = new BufPool;  // never destroyed: no teardown-order issues at exit
+  return *pool;
+}
+void* pool_alloc(int dev, size_t bytes) {
+  BufPool& pool = buf_pool();
+  {
+    std::lock_guard<std::mutex> lock(pool.m);
+    auto it = pool.free.find({dev, bytes});
+    if (it != pool.free.end()) {
+      void* p = it->second;
+      pool.free.erase(it);
+      pool.cached -= bytes;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  CK(cudaMalloc(&p, bytes));
+  return p;
+}
+void pool_release(int dev, size_t bytes, void* p) {
+  BufPool& pool = buf_pool();
+  std::lock_guard<std::mutex> lock(pool.m);
+  if (pool.cached + bytes <= kPoolCap) {
+    pool.free.emplace(std::make_pair(dev, bytes), p);
+    pool.cached += bytes;
+  } else {
+    cudaFree(p);
+  }
+}
+
+}  // namespace
+
+template <class T>
+void Ldlt::palloc(T** ptr, size_t bytes) {
+  *ptr = static_cast<T*>(pool_alloc(dev_, bytes));
+  pooled_.emplace_back(static_cast<void*>(*ptr), bytes);
+}
+
+namespace {
+
 int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t>((work + per - 1) / per, 4096)); }
 
 }  // namespace
@@ -153,12 +207,7 @@ __global__ void bk_iota_kernel(int* perm, int64_t n) {
 Ldlt::~Ldlt() {
   if (dev_ >= 0) {
     DeviceGuard g(dev_);
-    for (void* p : {static_cast<void*>(d_l_), static_cast<void*>(d_bk_), static_cast<void*>(d_bki_)})
-      if (p) cudaFree(p);
-    for (void* p : {static_cast<void*>(d_fact_), static_cast<void*>(d_ipiv_), static_cast<void*>(d_work_),
-                    static_cast<void*>(d_info_), static_cast<void*>(d_rhs_), static_cast<void*>(d_input_),
-                    static_cast<void*>(d_vec_), static_cast<void*>(d_ipiv64_), d_sbuf_})
-      if (p) cudaFree(p);
+    for (const auto& pb : pooled_) pool_release(dev_, pb.second, pb.first);
     if (handle_) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(handle_));
     if (stream_) cudaStreamDestroy(stream_);
   }
@@ -197,9 +246,9 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   f->stream_ = st;
   const size_t bytes = sizeof(double) * static_cast<size_t>(n) * n;
-  CK(cudaMalloc(&f->d_fact_, bytes));
-  CK(cudaMalloc(&f->d_vec_, sizeof(double) * (4 * n + 8)));  // rs | scale | cmax | x ... | scalars
-  CK(cudaMalloc(&f->d_rhs_, sizeof(double) * n));
+  f->palloc(&f->d_fact_, bytes);
+  f->palloc(&f->d_vec_, sizeof(double) * (4 * n + 8));  // rs | scale | cmax | x ... | scalars
+  f->palloc(&f->d_rhs_, sizeof(double) * n);
   if (on_device) {
     // try_mat = A + delta_w I (head) - delta_c I (tail), ipm.cpp:529-536:
     // the shifts only when non-zero, one rounding each, as the reference
@@ -256,7 +305,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
   CK(cudaMemcpyAsync(scale, f->scale_.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
   pt.mark("ruiz", st);
   if (keep_input) {
-    CK(cudaMalloc(&f->d_input_, bytes));
+    f->palloc(&f->d_input_, bytes);
     CK(cudaMemcpyAsync(f->d_input_, f->d_fact_, bytes, cudaMemcpyDeviceToDevice, st));
   }
 
@@ -286,16 +335,16 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
         std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, (n + bk::kWarps - 1) / bk::kWarps)));
     f->ldl_ = (n + 1) / 2 * 2;  // 16-byte rows
     const size_t lbytes = sizeof(double) * static_cast<size_t>(n) * f->ldl_;
-    CK(cudaMalloc(&f->d_l_, 2 * lbytes));  // L | W = L D
+    f->palloc(&f->d_l_, 2 * lbytes);  // L | W = L D
     CK(cudaMemsetAsync(f->d_l_, 0, 2 * lbytes, st));
     int solve_per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&solve_per_sm, bk::bk_solve_kernel, bk::kThreads, 0));
     f->solve_grid_ = std::max(1, std::min(sms * std::max(solve_per_sm, 1), 32 * bk::kSlices / bk::kWarps));
     // d | e | w | wr | z (solve scratch) | w2 | maxima (part, part3, part2; the solve's partials)
-    CK(cudaMalloc(&f->d_bk_, sizeof(double) * (6 * static_cast<size_t>(n) +
+    f->palloc(&f->d_bk_, sizeof(double) * (6 * static_cast<size_t>(n) +
                                                 std::max<size_t>({6 * static_cast<size_t>(grid), 32 * bk::kSlices,
-                                                                  32 * static_cast<size_t>(f->solve_grid_)}))));
-    CK(cudaMalloc(&f->d_bki_, sizeof(int) * 2 * static_cast<size_t>(n)));
+                                                                  32 * static_cast<size_t>(f->solve_grid_)})));
+    f->palloc(&f->d_bki_, sizeof(int) * 2 * static_cast<size_t>(n));
     bk_iota_kernel<<<blocks_for(n, 256), 256, 0, st>>>(f->d_bki_ + n, n);
     CK(cudaGetLastError());
     bk::Factor F;
@@ -315,6 +364,114 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     F.n = static_cast<int>(n);
     F.ldl = static_cast<int>(f->ldl_);
     CK(cudaMemsetAsync(F.e, 0, sizeof(double) * n, st));
+    // small n: the whole lower triangle in one cluster's shared memory
+    // (ldlt_bkc.cuh), one cluster barrier per pivot
+    const char* env_cl = std::getenv("GBOPT_LDLT_CLUSTER");
+    bool use_cluster = env_cl == nullptr || std::atoi(env_cl) != 0;
+    const int64_t cl_smem = bkc::smem_bytes(static_cast<int>(n));
+    int smem_optin = 0;
+    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    cudaFuncAttributes fa = {};
+    CK(cudaFuncGetAttributes(&fa, bkc::bkc_factor_kernel));
+    smem_optin -= static_cast<int>(fa.sharedSizeBytes);  // dynamic part available beside the static arrays
+    // measured crossover (tools/ldlt_split.py, GBOPT_LDLT_CLUSTER=0/1): the
+    // cluster kernel wins below ~800 (n = 112: 0.37 vs 1.06 ms, 337: 1.57 vs
+    // 2.35, 562: 3.41 vs 4.03) and ties at 804 (6.21 ms each)
+    constexpr int64_t kClusterMaxN = 800;
+    use_cluster = use_cluster && cl_smem <= smem_optin && (env_cl != nullptr || n <= kClusterMaxN);
+    if (use_cluster) {
+      static thread_local int cluster_ok = -1;  // per thread: attributes set for this process's device
+      if (cluster_ok < 0) {
+        cluster_ok = 0;
+        if (cudaFuncSetAttribute(bkc::bkc_factor_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess &&
+            cudaFuncSetAttribute(bkc::bkc_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin) ==
+                cudaSuccess) {
+          cudaLaunchConfig_t q = {};
+          q.gridDim = dim3(bkc::kCtas);
+          q.blockDim = dim3(bkc::kThreads);
+          q.dynamicSmemBytes = static_cast<size_t>(smem_optin);
+          cudaLaunchAttribute qa[1];
+          qa[0].id = cudaLaunchAttributeClusterDimension;
+          qa[0].val.clusterDim.x = bkc::kCtas;
+          qa[0].val.clusterDim.y = 1;
+          qa[0].val.clusterDim.z = 1;
+          q.attrs = qa;
+          q.numAttrs = 1;
+          int clusters = 0;
+          const cudaError_t oe = cudaOccupancyMaxActiveClusters(&clusters, bkc::bkc_factor_kernel, &q);
+          if (oe == cudaSuccess && clusters > 0) cluster_ok = 1;
+          if (std::getenv("GBOPT_LDLT_TIMING"))
+            std::fprintf(stderr, "ldlt: cluster occupancy query %s, %d clusters\n", cudaGetErrorString(oe), clusters);
+        } else if (std::getenv("GBOPT_LDLT_TIMING")) {
+          std::fprintf(stderr, "ldlt: cluster attributes rejected: %s\n", cudaGetErrorString(cudaGetLastError()));
+        }
+        cudaGetLastError();
+      }
+      use_cluster = cluster_ok == 1;
+    }
+    f->cluster_ = use_cluster;
+    if (use_cluster) {
+      bkc::Params P;
+      P.a = f->d_fact_;
+      P.l = f->d_l_;
+      P.ldl = static_cast<int>(f->ldl_);
+      P.d = F.d;
+      P.e = F.e;
+      P.piv = F.piv;
+      P.perm = F.perm;
+      P.n = static_cast<int>(n);
+      P.trace = nullptr;
+      const bool timing = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
+      if (timing) {
+        CK(cudaMalloc(&P.trace, sizeof(long long) * 6 * n));
+        CK(cudaMemsetAsync(P.trace, 0, sizeof(long long) * 6 * n, st));
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(bkc::kCtas);
+      cfg.blockDim = dim3(bkc::kThreads);
+      cfg.dynamicSmemBytes = static_cast<size_t>(cl_smem);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = bkc::kCtas;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaEvent_t c0 = nullptr, c1 = nullptr;
+      if (timing) {
+        CK(cudaEventCreate(&c0));
+        CK(cudaEventCreate(&c1));
+        CK(cudaEventRecord(c0, st));
+      }
+      CK(cudaLaunchKernelEx(&cfg, bkc::bkc_factor_kernel, P));
+      if (timing) {
+        CK(cudaEventRecord(c1, st));
+        CK(cudaEventSynchronize(c1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c0, c1));
+        std::fprintf(stderr, "ldlt: n %lld cluster bkc_factor_kernel %.3f ms (smem %lld B)\n",
+                     static_cast<long long>(n), ms, static_cast<long long>(cl_smem));
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+        std::vector<long long> tr(6 * static_cast<size_t>(n));
+        CK(cudaMemcpy(tr.data(), P.trace, sizeof(long long) * tr.size(), cudaMemcpyDeviceToHost));
+        CK(cudaFree(P.trace));
+        double ph[5] = {0, 0, 0, 0, 0};
+        int steps = 0;
+        for (int64_t k = 0; k < n; ++k) {
+          const long long* t = tr.data() + 6 * k;
+          if (t[0] == 0 || t[5] == 0) continue;
+          for (int i = 0; i < 5; ++i) ph[i] += static_cast<double>(t[i + 1] - t[i]);
+          ++steps;
+        }
+        if (steps)
+          std::fprintf(stderr, "ldlt: cluster per-step clocks (%d steps): decide %.0f swap %.0f update %.0f bcast %.0f "
+                       "barrier %.0f\n", steps, ph[0] / steps, ph[1] / steps, ph[2] / steps, ph[3] / steps,
+                       ph[4] / steps);
+      }
+    }
     void* args[] = {&F};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     const bool timing = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
@@ -323,8 +480,9 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       CK(cudaEventCreate(&t1));
       CK(cudaEventRecord(t0, st));
     }
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_factor_kernel), dim3(grid), dim3(bk::kThreads), args,
-                                   smem, st));
+    if (!use_cluster)
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_factor_kernel), dim3(grid), dim3(bk::kThreads),
+                                     args, smem, st));
     if (timing) {
       CK(cudaEventRecord(t1, st));
       CK(cudaEventSynchronize(t1));
@@ -359,12 +517,12 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
   CS(cusolverDnCreate(&h));
   f->handle_ = h;
   CS(cusolverDnSetStream(h, st));
-  CK(cudaMalloc(&f->d_ipiv_, sizeof(int) * n));
-  CK(cudaMalloc(&f->d_ipiv64_, sizeof(int64_t) * n));
-  CK(cudaMalloc(&f->d_info_, sizeof(int)));
+  f->palloc(&f->d_ipiv_, sizeof(int) * n);
+  f->palloc(&f->d_ipiv64_, sizeof(int64_t) * n);
+  f->palloc(&f->d_info_, sizeof(int));
   int lwork = 0;
   CS(cusolverDnDsytrf_bufferSize(h, static_cast<int>(n), f->d_fact_, static_cast<int>(n), &lwork));
-  CK(cudaMalloc(&f->d_work_, sizeof(double) * std::max(lwork, 1)));
+  f->palloc(&f->d_work_, sizeof(double) * std::max(lwork, 1));
   CS(cusolverDnDsytrf(h, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), f->d_fact_, static_cast<int>(n), f->d_ipiv_,
                       f->d_work_, lwork, f->d_info_));
   // only the pivot blocks come back: diagonal and first subdiagonal
@@ -396,7 +554,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
                                  f->d_rhs_, n, &dws, &hws));
   f->sws_dev_ = std::max<size_t>(dws, 8);
   f->sws_host_ = std::max<size_t>(hws, 8);
-  CK(cudaMalloc(&f->d_sbuf_, f->sws_dev_));
+  f->palloc(&f->d_sbuf_, f->sws_dev_);
   CK(cudaStreamSynchronize(st));
   return f;
 }

@@ -43,6 +43,10 @@ class Ldlt {
                                            double delta_c, bool keep_input, int device, cudaStream_t src);
   std::vector<double> solve_scaled(std::vector<double> bs) const;
   void solve_factored(double* d_v) const;
+  // device buffer from the reuse pool (ldlt.cu), returned to it by ~Ldlt
+  template <class T>
+  void palloc(T** ptr, size_t bytes);
+  std::vector<std::pair<void*, size_t>> pooled_;
   void refine_add_kernel_launch(double* d_x, const double* d_r, int64_t n, cudaStream_t st) const;
 
   int64_t n_ = 0, n_pos_ = 0, n_neg_ = 0, n_zero_ = 0;
@@ -64,6 +68,7 @@ class Ldlt {
   size_t sws_dev_ = 0, sws_host_ = 0;
   // native Bunch-Kaufman (ldlt_bk.cuh): n <= kNativeMaxN
   bool native_ = false;
+  bool cluster_ = false;  // factored by the one-cluster kernel (ldlt_bkc.cuh)
   double* d_l_ = nullptr;   // [n][ldl_] unit lower factor
   int64_t ldl_ = 0;
   int solve_grid_ = 1;

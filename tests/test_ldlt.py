@@ -177,3 +177,46 @@ class TestNativeBunchKaufman:
         x0 = gb.ldlt_factor(A).solve(b)
         for _ in range(3):
             assert np.array_equal(gb.ldlt_factor(A).solve(b), x0)
+
+
+@pytest.mark.gpu
+class TestClusterAndGridFactorisations:
+    """The one-cluster right-looking kernel (ldlt_bkc.cuh, default for
+    n <= 800) and the cooperative-grid left-looking kernel (ldlt_bk.cuh) on
+    the same matrices: same inertia as the oracle, accurate solves through
+    each (GBOPT_LDLT_CLUSTER forces the path)."""
+
+    @pytest.fixture(autouse=True)
+    def _gpu(self):
+        if not has_gpu():
+            pytest.skip("no GPU")
+
+    @pytest.mark.parametrize("path", ["1", "0"])
+    @pytest.mark.parametrize("case", ["zero_diag", "saddle", "kkt", "rank_deficient", "tiny"])
+    def test_paths_agree_with_oracle(self, monkeypatch, path, case):
+        import paper_2509_22462_b200 as gb
+        monkeypatch.setenv("GBOPT_LDLT_CLUSTER", path)
+        rng = np.random.default_rng(hash(case) % 1000)
+        if case == "zero_diag":
+            B = rng.uniform(-1, 1, (257, 257))
+            A = 0.5 * (B + B.T)
+            np.fill_diagonal(A, 0.0)
+        elif case == "saddle":
+            J = rng.uniform(-1, 1, (90, 90)) + 3 * np.eye(90)
+            A = np.block([[np.zeros((90, 90)), J.T], [J, np.zeros((90, 90))]])
+        elif case == "kkt":
+            n, m = 600, 150
+            H = rng.uniform(-1, 1, (n, n))
+            H = 0.5 * (H + H.T) + np.diag(10.0 ** rng.uniform(-2, 6, n))
+            Jm = rng.uniform(-1, 1, (m, n))
+            A = np.block([[H, Jm.T], [Jm, -1e-8 * np.eye(m)]])
+        elif case == "rank_deficient":
+            A = lo.matrix_with_spectrum(rng, np.r_[rng.uniform(1, 3, 40), -rng.uniform(1, 3, 30), np.zeros(3)])
+        else:
+            A = np.array([[0.0, 2.0, 1.0], [2.0, 0.0, 0.5], [1.0, 0.5, -1.0]])
+        f = gb.ldlt_factor(A)
+        assert f.inertia == lo.inertia(A)
+        if f.inertia[2] == 0:
+            b = rng.uniform(-1, 1, A.shape[0])
+            x = f.solve(b)
+            assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
