@@ -36,6 +36,7 @@
 #include "ldlt.hpp"
 #include "ldlt_bk.cuh"
 #include "ldlt_bkc.cuh"
+#include "ldlt_bkp.cuh"
 
 namespace gbb {
 
@@ -364,10 +365,85 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     F.n = static_cast<int>(n);
     F.ldl = static_cast<int>(f->ldl_);
     CK(cudaMemsetAsync(F.e, 0, sizeof(double) * n, st));
+    // Kernel choice (GBOPT_LDLT_KERNEL = panel | cluster | grid forces one):
+    //   panel   (ldlt_bkp.cuh): blocked; CTA 0 factors nb-column panels in
+    //           shared memory, the grid applies rank-nb updates -- n <= 2048
+    //           when a panel of nb >= 4 columns fits in shared memory;
+    //   cluster (ldlt_bkc.cuh): the lower triangle in one cluster's shared
+    //           memory, one pivot per step;
+    //   grid    (ldlt_bk.cuh):  left-looking, every SM, any n <= 20000.
+    const char* env_k = std::getenv("GBOPT_LDLT_KERNEL");
+    const std::string want = env_k ? env_k : "";
+    int smem_optin_dev = 0;
+    CK(cudaDeviceGetAttribute(&smem_optin_dev, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    int pnb = 0;
+    {
+      cudaFuncAttributes pa = {};
+      CK(cudaFuncGetAttributes(&pa, bkp::bkp_factor_kernel));
+      const int64_t avail = smem_optin_dev - static_cast<int64_t>(pa.sharedSizeBytes);
+      for (int nb = bkp::kMaxNb; nb >= 4; --nb)
+        if (bkp::smem_bytes(static_cast<int>(n), nb) <= avail) {
+          pnb = nb;
+          break;
+        }
+    }
+    const bool use_panel = pnb > 0 && n <= bkp::kThreads * bkp::kMaxRowsPerThread && (want.empty() || want == "panel");
+    f->panel_ = use_panel;
+    if (use_panel) {
+      const size_t psmem = static_cast<size_t>(bkp::smem_bytes(static_cast<int>(n), pnb));
+      CK(cudaFuncSetAttribute(bkp::bkp_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(psmem)));
+      int pper = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pper, bkp::bkp_factor_kernel, bkp::kThreads, psmem));
+      if (pper < 1) throw DeviceError("ldlt_factor: the blocked kernel does not fit on an SM");
+      f->palloc(&f->d_pan_, sizeof(double) * (bkp::kMaxNb * static_cast<size_t>(n) + 3 * bkp::kMaxNb + 8));
+      bkp::Params P;
+      P.a = f->d_fact_;
+      P.lcols = f->d_l_ + static_cast<size_t>(n) * f->ldl_;  // the W half of d_l_: n x n scratch
+      P.l = f->d_l_;
+      P.ldl = static_cast<int>(f->ldl_);
+      P.d = F.d;
+      P.e = F.e;
+      P.piv = F.piv;
+      P.perm = F.perm;
+      P.pan_w = f->d_pan_;
+      P.pan_g = f->d_pan_ + bkp::kMaxNb * static_cast<size_t>(n);
+      P.ctl = reinterpret_cast<int*>(P.pan_g + 3 * bkp::kMaxNb);
+      P.n = static_cast<int>(n);
+      P.nb = pnb;
+      P.trace = nullptr;
+      void* pargs[] = {&P};
+      cudaEvent_t c0 = nullptr, c1 = nullptr;
+      const bool timing = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
+      if (timing) {
+        CK(cudaMalloc(&P.trace, sizeof(long long) * 8));
+        CK(cudaEventCreate(&c0));
+        CK(cudaEventCreate(&c1));
+        CK(cudaEventRecord(c0, st));
+      }
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bkp::bkp_factor_kernel), dim3(sms * std::min(pper, 1)),
+                                     dim3(bkp::kThreads), pargs, psmem, st));
+      if (timing) {
+        CK(cudaEventRecord(c1, st));
+        CK(cudaEventSynchronize(c1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c0, c1));
+        long long tr[8];
+        CK(cudaMemcpy(tr, P.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+        CK(cudaFree(P.trace));
+        std::fprintf(stderr,
+                     "ldlt: n %lld panel nb %d bkp_factor_kernel %.3f ms; CTA-0 clocks: column %lld, column r %lld, "
+                     "pivot %lld, publish %lld, sync %lld, update %lld, sync %lld, loop %lld\n",
+                     static_cast<long long>(n), pnb, ms, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[6], tr[7]);
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+      }
+    }
     // small n: the whole lower triangle in one cluster's shared memory
     // (ldlt_bkc.cuh), one cluster barrier per pivot
     const char* env_cl = std::getenv("GBOPT_LDLT_CLUSTER");
-    bool use_cluster = env_cl == nullptr || std::atoi(env_cl) != 0;
+    bool use_cluster = !use_panel && (want.empty() || want == "cluster") &&
+                       (env_cl == nullptr || std::atoi(env_cl) != 0);
     const int64_t cl_smem = bkc::smem_bytes(static_cast<int>(n));
     int smem_optin = 0;
     CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -378,9 +454,11 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     // cluster kernel wins below ~800 (n = 112: 0.37 vs 1.06 ms, 337: 1.57 vs
     // 2.35, 562: 3.41 vs 4.03) and ties at 804 (6.21 ms each)
     constexpr int64_t kClusterMaxN = 800;
-    use_cluster = use_cluster && cl_smem <= smem_optin && (env_cl != nullptr || n <= kClusterMaxN);
+    use_cluster = use_cluster && cl_smem <= smem_optin && (want == "cluster" || n <= kClusterMaxN);
     if (use_cluster) {
-      static thread_local int cluster_ok = -1;  // per thread: attributes set for this process's device
+      // function attributes are per device: check (and set) once per device and thread
+      static thread_local std::map<int, int> cluster_ok_by_dev;
+      int& cluster_ok = cluster_ok_by_dev.try_emplace(device, -1).first->second;
       if (cluster_ok < 0) {
         cluster_ok = 0;
         if (cudaFuncSetAttribute(bkc::bkc_factor_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
@@ -480,7 +558,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       CK(cudaEventCreate(&t1));
       CK(cudaEventRecord(t0, st));
     }
-    if (!use_cluster)
+    if (!use_cluster && !use_panel)
       CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_factor_kernel), dim3(grid), dim3(bk::kThreads),
                                      args, smem, st));
     if (timing) {

@@ -68,7 +68,9 @@ class Ldlt {
   size_t sws_dev_ = 0, sws_host_ = 0;
   // native Bunch-Kaufman (ldlt_bk.cuh): n <= kNativeMaxN
   bool native_ = false;
-  bool cluster_ = false;  // factored by the one-cluster kernel (ldlt_bkc.cuh)
+  bool cluster_ = false;
+  bool panel_ = false;  // factored by the blocked kernel (ldlt_bkp.cuh)  // factored by the one-cluster kernel (ldlt_bkc.cuh)
+  double* d_pan_ = nullptr;  // blocked kernel (ldlt_bkp.cuh): panel L / W columns, control, inverse permutation
   double* d_l_ = nullptr;   // [n][ldl_] unit lower factor
   int64_t ldl_ = 0;
   int solve_grid_ = 1;

@@ -180,22 +180,23 @@ class TestNativeBunchKaufman:
 
 
 @pytest.mark.gpu
-class TestClusterAndGridFactorisations:
-    """The one-cluster right-looking kernel (ldlt_bkc.cuh, default for
-    n <= 800) and the cooperative-grid left-looking kernel (ldlt_bk.cuh) on
-    the same matrices: same inertia as the oracle, accurate solves through
-    each (GBOPT_LDLT_CLUSTER forces the path)."""
+class TestFactorisationKernels:
+    """The three native factorisation kernels on the same matrices -- blocked
+    (ldlt_bkp.cuh, default for n <= 2048), one-cluster right-looking
+    (ldlt_bkc.cuh) and cooperative-grid left-looking (ldlt_bk.cuh): same
+    inertia as the oracle, accurate solves through each
+    (GBOPT_LDLT_KERNEL forces the path)."""
 
     @pytest.fixture(autouse=True)
     def _gpu(self):
         if not has_gpu():
             pytest.skip("no GPU")
 
-    @pytest.mark.parametrize("path", ["1", "0"])
+    @pytest.mark.parametrize("path", ["panel", "cluster", "grid"])
     @pytest.mark.parametrize("case", ["zero_diag", "saddle", "kkt", "rank_deficient", "tiny"])
     def test_paths_agree_with_oracle(self, monkeypatch, path, case):
         import paper_2509_22462_b200 as gb
-        monkeypatch.setenv("GBOPT_LDLT_CLUSTER", path)
+        monkeypatch.setenv("GBOPT_LDLT_KERNEL", path)
         rng = np.random.default_rng(hash(case) % 1000)
         if case == "zero_diag":
             B = rng.uniform(-1, 1, (257, 257))
