@@ -186,6 +186,7 @@ int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t
 }  // namespace
 
 constexpr int64_t kNativeMaxN = 20000;
+constexpr int64_t kCtaSolveMaxN = 3000;  // one-CTA substitution below (n 804: 0.20 vs 0.44 ms; 4500: 3.08 vs 2.45)
 
 // GBOPT_LDLT_TIMING=1: host wall time of the factorisation phases on stderr
 struct PhaseTimer {
@@ -650,6 +651,15 @@ void Ldlt::solve_factored(double* d_v) const {
     const int* perm = d_bki_ + n_;
     const double* bb = d_v;
     double* x = d_v;
+    // one CTA up to kCtaSolveMaxN (measured: tools/ldlt_solve_probe.py),
+    // the grid-wide version beyond; GBOPT_LDLT_SOLVE = cta | grid forces one
+    const char* env_s = std::getenv("GBOPT_LDLT_SOLVE");
+    const bool cta = env_s ? std::string(env_s) == "cta" : n_ <= kCtaSolveMaxN;
+    if (cta) {
+      bk::bk_solve_cta_kernel<<<1, bk::kCtaThreads, 0, stream_>>>(l, ldl, d, e, piv, perm, n, bb, z, x);
+      CK(cudaGetLastError());
+      return;
+    }
     void* args[] = {&l, &ldl, &d, &e, &piv, &perm, &n, &bb, &z, &x, &part};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_solve_kernel), dim3(solve_grid_),
                                    dim3(bk::kThreads), args, 0, stream_));

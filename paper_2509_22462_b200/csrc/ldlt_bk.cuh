@@ -531,5 +531,105 @@ __global__ void __launch_bounds__(kThreads) bk_solve_kernel(const double* __rest
   for (int i = tid; i < n; i += nt) x[i] = __ldcg(z + i);
 }
 
+// The same substitutions in ONE CTA of kCtaThreads threads (small and
+// medium n): the grid version pays two grid barriers per 32-row block,
+// here a block costs two CTA barriers; L (n^2 / 2 words per direction) is
+// streamed from L2 by one SM.  Per block: the 32 x b0 (forward) or
+// (n - b1) x 32 (backward) update with coalesced row segments -- forward:
+// warp w takes row b0 + w, lanes along j; backward: warps take rows j,
+// lanes the block's 32 columns, partial sums reduced through shared memory
+// in a fixed order -- then warp 0 solves the 32 x 32 triangle from a tile
+// staged in shared memory.
+constexpr int kCtaThreads = 1024;
+constexpr int kCtaWarps = kCtaThreads / 32;
+
+__global__ void __launch_bounds__(kCtaThreads) bk_solve_cta_kernel(const double* __restrict__ l, int ldl,
+                                                                   const double* __restrict__ d,
+                                                                   const double* __restrict__ e,
+                                                                   const int* __restrict__ piv,
+                                                                   const int* __restrict__ perm, int n,
+                                                                   const double* b, double* z, double* x) {
+  __shared__ double tile[32][33];
+  __shared__ double red[kCtaWarps][33];
+  __shared__ double sblk[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n; i += kCtaThreads) z[i] = b[perm[i]];
+  __syncthreads();
+  // ---- forward: L z = P b ----
+  for (int b0 = 0; b0 < n; b0 += 32) {
+    const int rows = min(32, n - b0);
+    // warp w: row b0 + w, sum over j < b0; also stage the diagonal tile row
+    if (warp < rows) {
+      const double* li = l + static_cast<int64_t>(b0 + warp) * ldl;
+      double s0 = 0.0, s1 = 0.0;
+      int j = lane;
+      for (; j + 32 < b0; j += 64) {
+        s0 = fma(__ldcg(li + j), z[j], s0);
+        s1 = fma(__ldcg(li + j + 32), z[j + 32], s1);
+      }
+      if (j < b0) s0 = fma(__ldcg(li + j), z[j], s0);
+      double s = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      tile[warp][lane] = lane < rows ? __ldcg(li + b0 + lane) : 0.0;
+      if (lane == 0) sblk[warp] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double zi = lane < rows ? z[b0 + lane] - sblk[lane] : 0.0;
+      for (int j = 0; j < rows; ++j) {
+        const double zj = __shfl_sync(0xffffffffu, zi, j);
+        if (lane > j) zi -= tile[lane][j] * zj;
+      }
+      if (lane < rows) z[b0 + lane] = zi;
+    }
+    __syncthreads();
+  }
+  // ---- D ----
+  for (int i = threadIdx.x; i < n; i += kCtaThreads) {
+    if (piv[i] == 1) {
+      x[i] = z[i] / d[i];
+    } else {
+      const bool first = piv[i] == 2;
+      const int k = first ? i : i - 1;
+      const double a = d[k], bb = e[k], c = d[k + 1];
+      const double det = a * c - bb * bb;
+      const double z0 = z[k], z1 = z[k + 1];
+      x[i] = first ? (c * z0 - bb * z1) / det : (a * z1 - bb * z0) / det;
+    }
+  }
+  __syncthreads();
+  // ---- backward: L^T y = x ----
+  for (int b0 = ((n - 1) / 32) * 32; b0 >= 0; b0 -= 32) {
+    const int b1 = min(n, b0 + 32), rows = b1 - b0;
+    double s0 = 0.0, s1 = 0.0;
+    if (lane < rows) {
+      int j = b1 + warp;
+      for (; j + kCtaWarps < n; j += 2 * kCtaWarps) {
+        s0 = fma(__ldcg(l + static_cast<int64_t>(j) * ldl + b0 + lane), x[j], s0);
+        s1 = fma(__ldcg(l + static_cast<int64_t>(j + kCtaWarps) * ldl + b0 + lane), x[j + kCtaWarps], s1);
+      }
+      if (j < n) s0 = fma(__ldcg(l + static_cast<int64_t>(j) * ldl + b0 + lane), x[j], s0);
+    }
+    red[warp][lane] = s0 + s1;
+    if (warp < rows) tile[warp][lane] = lane < rows ? __ldcg(l + static_cast<int64_t>(b0 + warp) * ldl + b0 + lane) : 0.0;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kCtaWarps; ++w) t += red[w][lane];  // fixed order
+      double yi = lane < rows ? x[b0 + lane] - t : 0.0;
+      for (int j = rows - 1; j >= 0; --j) {
+        const double yj = __shfl_sync(0xffffffffu, yi, j);
+        if (lane < j) yi -= tile[j][lane] * yj;
+      }
+      if (lane < rows) x[b0 + lane] = yi;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += kCtaThreads) z[perm[i]] = x[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kCtaThreads) x[i] = z[i];
+}
+
 }  // namespace bk
 }  // namespace gbb

@@ -221,3 +221,25 @@ class TestFactorisationKernels:
             b = rng.uniform(-1, 1, A.shape[0])
             x = f.solve(b)
             assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("solve", ["cta", "grid"])
+def test_substitution_kernels_agree(monkeypatch, solve):
+    """One-CTA and grid-wide substitutions (GBOPT_LDLT_SOLVE) on the same
+    factors: accurate solves, 2x2 pivots included."""
+    if not has_gpu():
+        pytest.skip("no GPU")
+    import paper_2509_22462_b200 as gb
+    monkeypatch.setenv("GBOPT_LDLT_SOLVE", solve)
+    rng = np.random.default_rng(41)
+    for n in (1, 33, 257, 700):
+        B = rng.uniform(-1, 1, (n, n))
+        A = 0.5 * (B + B.T)
+        np.fill_diagonal(A, 0.0 if n > 1 else 2.0)
+        f = gb.ldlt_factor(A)
+        if f.inertia[2]:
+            continue
+        b = rng.uniform(-1, 1, n)
+        x = f.solve(b)
+        assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
