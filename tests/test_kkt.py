@@ -304,3 +304,37 @@ class TestGpuKkt:
         sol = s.solve(cf.fact)
         corr = mat + np.diag(np.r_[np.full(n, cf.delta_w), np.full(m, -cf.delta_c)])
         assert np.abs(corr @ sol - rhs).max() <= 1e-10 * (np.abs(corr).max() * np.abs(sol).max() + 1.0)
+
+
+@pytest.mark.gpu
+def test_kkt_without_constraints_and_large_system():
+    """m = 0 (no constraint block, delta_c never used) and a dimension past
+    the blocked factorisation's limit (grid kernel inside inertia_correct)."""
+    if not has_gpu():
+        pytest.skip("no GPU")
+    import paper_2509_22462_b200 as gb
+    rng = np.random.default_rng(12)
+    n = 40
+    q = spd_matrix(rng, n) - 2.5 * n * np.eye(n)   # indefinite: needs delta_w
+    rows, cols = np.tril_indices(n)
+    s = gb.assemble_kkt(np.zeros(n), np.full(n, NO_LB), np.zeros(n), [], rng.normal(size=n), [], [], [], [],
+                        rows, cols, q[rows, cols], 0.0)
+    cf = gb.inertia_correct(s)
+    dw, dc, inert = lo.inertia_correct(s.mat, n, 0)
+    assert cf.fact.inertia == inert == (n, 0, 0) and (cf.delta_w, cf.delta_c) == (dw, dc) and cf.delta_w > 0
+    n, m = 2000, 400
+    c = random_case(13, n, m, 6000, 3000)
+    rows, cols = np.tril_indices(n)
+    h = np.diag(rng.uniform(1, 2, n))
+    c.update(hess_rows=np.r_[c["hess_rows"], np.arange(n)], hess_cols=np.r_[c["hess_cols"], np.arange(n)],
+             hess_values=np.r_[c["hess_values"], 50.0 * np.ones(n)])
+    pat = gb.KktPattern(n, m, c["hess_rows"], c["hess_cols"], c["jac_rows"], c["jac_cols"])
+    sys_ = pat.assemble(c["x"], c["lower"], c["z"], c["lam"], c["grad_f"], c["g"], c["jac_values"], c["hess_values"],
+                        c["mu"])
+    mat, rhs = oracle_of(c)
+    assert np.array_equal(sys_.mat, mat) and np.array_equal(sys_.rhs, rhs)
+    cf = gb.inertia_correct(sys_)
+    assert cf.fact.inertia == (n, m, 0)
+    sol = sys_.solve(cf.fact)
+    corr = mat + np.diag(np.r_[np.full(n, cf.delta_w), np.full(m, -cf.delta_c)])
+    assert np.abs(corr @ sol - rhs).max() <= 1e-8 * (np.abs(corr).max() * np.abs(sol).max() + 1.0)

@@ -243,3 +243,25 @@ def test_substitution_kernels_agree(monkeypatch, solve):
         b = rng.uniform(-1, 1, n)
         x = f.solve(b)
         assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2047, 2049, 3001])
+def test_default_kernel_choice_across_thresholds(n):
+    """Dimensions either side of the blocked-kernel (2048) and one-CTA
+    substitution (3000) limits, through the default path."""
+    if not has_gpu():
+        pytest.skip("no GPU")
+    import paper_2509_22462_b200 as gb
+    rng = np.random.default_rng(n)
+    m = n // 5
+    H = rng.uniform(-1, 1, (n - m, n - m))
+    H = 0.5 * (H + H.T) + np.diag(10.0 ** rng.uniform(-2, 4, n - m))
+    J = rng.uniform(-1, 1, (m, n - m))
+    K = np.block([[H, J.T], [J, -1e-8 * np.eye(m)]])
+    f = gb.ldlt_factor(K)
+    ev = np.linalg.eigvalsh(K)
+    assert f.inertia == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
+    b = rng.uniform(-1, 1, n)
+    x = f.solve(b)
+    assert np.abs(K @ x - b).max() <= 1e-8 * (np.abs(K).max() * np.abs(x).max() + 1.0)
