@@ -201,6 +201,8 @@ class DeviceNet {
   bool concurrent_ = true;
   std::vector<cudaEvent_t> evpool_;
   cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
+  cudaStream_t copy_stream_ = nullptr;  // host-buffer calls: D2H of finished chunks
+  std::vector<cudaEvent_t> chunk_ev_;
   int64_t n_ = 0, m_ = 0, L_ = 0, n_pad_ = 0;
   std::vector<DevLayer> layers_;
   double* t0_ = nullptr;  // W_0^T [n_pad][ldt0_]

@@ -137,6 +137,7 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   concurrent_ = std::getenv("GBOPT_SERIAL") == nullptr;  // debugging / A-B switch
   CK(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
 
   n_ = net.input_dim();
   m_ = net.output_dim();
@@ -208,6 +209,8 @@ DeviceNet::~DeviceNet() {
   for (cudaEvent_t e : evpool_) cudaEventDestroy(e);
   if (ev_in_) cudaEventDestroy(ev_in_);
   if (ev_out_) cudaEventDestroy(ev_out_);
+  for (cudaEvent_t e : chunk_ev_) cudaEventDestroy(e);
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
 }
 
 void DeviceNet::free_workspace() {
@@ -1035,39 +1038,28 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
   Workspace& w = ws_;
-  Outputs o;
-  o.y = y ? w.y_out : nullptr;
-  o.j = jac ? w.j_out : nullptr;
-  o.h = hess ? w.h_out : nullptr;
-  o.g = grad ? w.g_out : nullptr;
-  o.h_packed = hess_packed;
-  prepare(nb, o);
-  CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x, sizeof(double) * n_, sizeof(double) * n_, nb,
-                       cudaMemcpyHostToDevice, stream_));
-  if (lam)
-    CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam, sizeof(double) * m_, sizeof(double) * m_, nb,
-                         cudaMemcpyHostToDevice, stream_));
-  run(stream_, nb, o);
   // Results go to pinned caller buffers directly; pageable ones through a
   // pinned staging area (a pageable D2H runs at a fraction of the PCIe rate)
   // and are written only after the evaluation has completed.
+  const size_t hsz = hess_packed ? static_cast<size_t>(n_ * (n_ + 1) / 2) : static_cast<size_t>(n_ * n_);
   struct Out {
     double* dst;
-    const double* src;
-    size_t n;
+    double* src;
+    size_t per_point;
   };
-  const Out outs[4] = {{y, w.y_out, static_cast<size_t>(nb) * m_},
-                       {jac, w.j_out, static_cast<size_t>(nb) * m_ * n_},
-                       {hess, w.h_out, static_cast<size_t>(nb) * (hess_packed ? n_ * (n_ + 1) / 2 : n_ * n_)},
-                       {grad, w.g_out, static_cast<size_t>(nb) * n_}};
-  size_t staged = 0;
+  const Out outs[4] = {{y, w.y_out, static_cast<size_t>(m_)},
+                       {jac, w.j_out, static_cast<size_t>(m_ * n_)},
+                       {hess, w.h_out, hsz},
+                       {grad, w.g_out, static_cast<size_t>(n_)}};
+  size_t staged = 0, out_bytes = 0;
   bool pinned[4] = {false, false, false, false};
   for (int i = 0; i < 4; ++i) {
     if (!outs[i].dst) continue;
     cudaPointerAttributes a;
     pinned[i] = cudaPointerGetAttributes(&a, outs[i].dst) == cudaSuccess && a.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    if (!pinned[i]) staged += outs[i].n;
+    if (!pinned[i]) staged += outs[i].per_point * nb;
+    out_bytes += sizeof(double) * outs[i].per_point * nb;
   }
   if (staged > stage_cap_) {
     if (stage_) cudaFreeHost(stage_);
@@ -1076,19 +1068,68 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
     CK(cudaHostAlloc(reinterpret_cast<void**>(&stage_), sizeof(double) * staged, cudaHostAllocDefault));
     stage_cap_ = staged;
   }
-  size_t off = 0;
-  for (int i = 0; i < 4; ++i) {
-    if (!outs[i].dst) continue;
-    double* d = pinned[i] ? outs[i].dst : stage_ + off;
-    CK(cudaMemcpyAsync(d, outs[i].src, sizeof(double) * outs[i].n, cudaMemcpyDeviceToHost, stream_));
-    if (!pinned[i]) off += outs[i].n;
+  // Batched results whose copy-out is a visible share of the call (c4: 94 KB
+  // per point against ~0.5 GFLOP of work, ~12%) leave the GPU in chunks:
+  // chunk c's D2H on copy_stream_ overlaps chunk c + 1's evaluation, so only
+  // the last chunk's copy is exposed.  At ~37 TFLOP/s against ~50 GB/s of
+  // PCIe (740 flop/B break-even) a point below ~25k flops per output byte
+  // spends > ~3% of its time in the copy; above that (c3: 36k flop/B) the
+  // smaller chunks cost more than they hide.  Chunks keep >= 32 points.
+  double flops = 0.0;  // F_jac + F_hess per point
+  for (size_t l = 0; l < layers_.size(); ++l) {
+    if (l > 0) flops += 2.0 * static_cast<double>(layers_[l].rows * layers_[l].cols * n_);
+    if (layers_[l].act != kLinear) flops += static_cast<double>(layers_[l].rows * n_ * (n_ + 1));
+  }
+  const double bytes_pp = static_cast<double>(out_bytes) / nb;
+  int chunks = 1;
+  if (nb >= 128 && out_bytes >= (size_t(64) << 20) && flops < 25000.0 * bytes_pp) chunks = 4;
+  if (const char* e = std::getenv("GBOPT_HOST_CHUNKS")) chunks = std::max(1, std::min(nb, std::atoi(e)));
+  const int per = (nb + chunks - 1) / chunks;
+  while (static_cast<int>(chunk_ev_.size()) < chunks) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    chunk_ev_.push_back(e);
+  }
+  CK(cudaEventRecord(ev_in_, stream_));
+  CK(cudaStreamWaitEvent(copy_stream_, ev_in_, 0));  // no copy of this call overtakes earlier work
+  int ci = 0;
+  for (int c0 = 0; c0 < nb; c0 += per, ++ci) {
+    const int nbc = std::min(per, nb - c0);
+    Outputs o;
+    o.y = y ? w.y_out + static_cast<size_t>(c0) * m_ : nullptr;
+    o.j = jac ? w.j_out + static_cast<size_t>(c0) * m_ * n_ : nullptr;
+    o.h = hess ? w.h_out + static_cast<size_t>(c0) * hsz : nullptr;
+    o.g = grad ? w.g_out + static_cast<size_t>(c0) * n_ : nullptr;
+    o.h_packed = hess_packed;
+    prepare(nbc, o);
+    CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, x + static_cast<size_t>(c0) * n_, sizeof(double) * n_,
+                         sizeof(double) * n_, nbc, cudaMemcpyHostToDevice, stream_));
+    if (lam)
+      CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam + static_cast<size_t>(c0) * m_, sizeof(double) * m_,
+                           sizeof(double) * m_, nbc, cudaMemcpyHostToDevice, stream_));
+    run(stream_, nbc, o);
+    cudaStream_t cs = chunks > 1 ? copy_stream_ : stream_;
+    if (chunks > 1) {
+      CK(cudaEventRecord(chunk_ev_[static_cast<size_t>(ci)], stream_));
+      CK(cudaStreamWaitEvent(copy_stream_, chunk_ev_[static_cast<size_t>(ci)], 0));
+    }
+    size_t off = 0;
+    for (int i = 0; i < 4; ++i) {
+      if (!outs[i].dst) continue;
+      const size_t pp = outs[i].per_point;
+      double* d = pinned[i] ? outs[i].dst + static_cast<size_t>(c0) * pp : stage_ + off + static_cast<size_t>(c0) * pp;
+      CK(cudaMemcpyAsync(d, outs[i].src + static_cast<size_t>(c0) * pp, sizeof(double) * pp * nbc,
+                         cudaMemcpyDeviceToHost, cs));
+      if (!pinned[i]) off += pp * nb;
+    }
   }
   CK(cudaStreamSynchronize(stream_));
-  off = 0;
+  if (chunks > 1) CK(cudaStreamSynchronize(copy_stream_));
+  size_t off = 0;
   for (int i = 0; i < 4; ++i) {
     if (!outs[i].dst || pinned[i]) continue;
-    std::memcpy(outs[i].dst, stage_ + off, sizeof(double) * outs[i].n);
-    off += outs[i].n;
+    std::memcpy(outs[i].dst, stage_ + off, sizeof(double) * outs[i].per_point * nb);
+    off += outs[i].per_point * nb;
   }
 }
 

@@ -189,3 +189,29 @@ def test_oracle_lower_packs_the_full_hessian(schedule, widths, hid, fin, seed):
     # Hessian only
     _, _, hl2 = net.oracle_lower(x, lam, want_y=False, want_j=False)
     assert np.array_equal(hl2, hl)
+
+
+@pytest.mark.parametrize("chunks", [2, 3, 7])
+def test_host_call_in_chunks(monkeypatch, chunks):
+    """Host-buffer batched calls evaluated in chunks whose device->host
+    copies overlap the next chunk (GBOPT_HOST_CHUNKS forces the split):
+    same results as one chunk (y, J bitwise; H to rounding) and as the
+    oracle, pinned and pageable outputs."""
+    import torch
+    net = gb.random_net([40, 64, 48, 6], "tanh", "linear", 19).bind_device(0)
+    ref = to_oracle(net)
+    rng = np.random.default_rng(chunks)
+    B = 7
+    X = rng.uniform(-1, 1, (B, 40))
+    Lam = rng.normal(0, 1, (B, 6))
+    monkeypatch.setenv("GBOPT_HOST_CHUNKS", "1")
+    Y0, J0, H0 = net.oracle_batched(X, Lam)
+    monkeypatch.setenv("GBOPT_HOST_CHUNKS", str(chunks))
+    Y1, J1, H1 = net.oracle_batched(X, Lam)
+    pinned = [torch.empty(shape, dtype=torch.float64).pin_memory().numpy() for shape in ((B, 6), (B, 6, 40), (B, 40, 40))]
+    Y2, J2, H2 = net.oracle_batched(X, Lam, out=tuple(pinned))
+    for (Y, J, H) in ((Y1, J1, H1), (Y2, J2, H2)):
+        for b in range(B):  # a one-point chunk takes the single-point kernels: equal to rounding
+            assert orc.rel_err(Y[b], Y0[b]) <= 1e-14 and orc.rel_err(J[b], J0[b]) <= 1e-14
+            assert orc.rel_err(H[b], H0[b]) <= 1e-14
+            assert orc.rel_err(H[b], ref.lagrangian_hessian(X[b], Lam[b])) <= TOL
