@@ -1074,7 +1074,9 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   // the last chunk's copy is exposed.  At ~37 TFLOP/s against ~50 GB/s of
   // PCIe (740 flop/B break-even) a point below ~25k flops per output byte
   // spends > ~3% of its time in the copy; above that (c3: 36k flop/B) the
-  // smaller chunks cost more than they hide.  Chunks keep >= 32 points.
+  // smaller chunks cost more than they hide.  Measured: c4 (4096 points) 4
+  // chunks 56.0k -> 59.6k e2e evals/s (8 chunks: 59.4k); c5 (16 points, 8.8k
+  // flop/B) 2 chunks 700 -> 717 (4 chunks: 699).
   double flops = 0.0;  // F_jac + F_hess per point
   for (size_t l = 0; l < layers_.size(); ++l) {
     if (l > 0) flops += 2.0 * static_cast<double>(layers_[l].rows * layers_[l].cols * n_);
@@ -1082,7 +1084,7 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   }
   const double bytes_pp = static_cast<double>(out_bytes) / nb;
   int chunks = 1;
-  if (nb >= 128 && out_bytes >= (size_t(64) << 20) && flops < 25000.0 * bytes_pp) chunks = 4;
+  if (out_bytes >= (size_t(64) << 20) && flops < 25000.0 * bytes_pp) chunks = nb >= 128 ? 4 : (nb >= 16 ? 2 : 1);
   if (const char* e = std::getenv("GBOPT_HOST_CHUNKS")) chunks = std::max(1, std::min(nb, std::atoi(e)));
   const int per = (nb + chunks - 1) / chunks;
   while (static_cast<int>(chunk_ev_.size()) < chunks) {

@@ -396,7 +396,8 @@ class NeuralNet:
         return Y, J, H
 
     def intermediate(self, name: str, layer: int, batch: int = 1) -> np.ndarray:
-        """Per-layer vector of the last evaluation (white-box tests)."""
+        """Per-layer vector of the last evaluation (white-box tests; the last
+        chunk's when a host-buffer batch ran in chunks, see GBOPT_HOST_CHUNKS)."""
         rows = self.layer(layer)[0].shape[0]
         out = np.empty((batch, rows))
         _check(_net_debug_intermediate(self._h, name.encode(), layer, batch, _dptr(out), out.size))

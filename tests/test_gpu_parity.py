@@ -266,10 +266,13 @@ def test_nonfinite_input_propagates_like_reference():
     assert np.isnan(y).all()
 
 
-def test_batched_intermediates_match_single():
+def test_batched_intermediates_match_single(monkeypatch):
     """White-box: the batched (GEMM) forward/adjoint chains give the same
     per-layer z, y, sigma', sigma'', ybar, gz, d as the single-point GEMV
-    chains (regression: stream-ordering of the W^T build / zero fills)."""
+    chains (regression: stream-ordering of the W^T build / zero fills).
+    The workspace holds the whole batch only when the host call is not
+    split into chunks."""
+    monkeypatch.setenv("GBOPT_HOST_CHUNKS", "1")
     widths = [784, 2048, 2048, 2048, 10]
     ref = gb.random_net(widths, "softplus", "linear", 3)
     rng = np.random.default_rng(0)
