@@ -18,6 +18,7 @@
 // Everything O(n^2) per pass (checks, equilibration, residuals) runs on the
 // device too; only the 2n pivot-block entries and vectors cross PCIe after
 // the matrix upload.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -48,56 +49,11 @@ void cs_check(cusolverStatus_t s, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 #define CS(x) cs_check((x), #x)
+namespace cg = cooperative_groups;
 
 __device__ inline void atomic_max_pos(double* addr, double v) {
   // v >= 0: ordering of non-negative doubles matches their bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr), __double_as_longlong(v));
-}
-
-// out[0] = max|A|, out[1] = max|A - A^T| (lower vs upper), out[2] = #non-finite
-__global__ void ldlt_check_kernel(const double* __restrict__ a, int64_t n, double* out) {
-  double amax = 0.0, asym = 0.0, bad = 0.0;
-  const int64_t nn = n * n;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nn;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = e / n, j = e % n;
-    const double v = a[e];
-    if (!isfinite(v)) {
-      bad += 1.0;
-      continue;
-    }
-    amax = fmax(amax, fabs(v));
-    if (j < i) asym = fmax(asym, fabs(v - a[j * n + i]));
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
-    bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomic_max_pos(out + 0, amax);
-    if (asym == asym) atomic_max_pos(out + 1, asym);
-    if (bad > 0) atomicAdd(out + 2, bad);
-  }
-}
-
-// cmax[j] = max_i |A[i][j]|  (one warp per column, symmetric: rows = cols)
-__global__ void ldlt_colmax_kernel(const double* __restrict__ a, int64_t n, double* __restrict__ cmax) {
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (col >= n) return;
-  const int lane = threadIdx.x & 31;
-  // row `col` of the symmetric matrix == column `col`: read it contiguously
-  double m = 0.0;
-  for (int64_t k = lane; k < n; k += 32) m = fmax(m, fabs(a[col * n + k]));
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) cmax[col] = m;
-}
-
-__global__ void ldlt_scale_kernel(double* __restrict__ a, int64_t n, const double* __restrict__ rs) {
-  const int64_t nn = n * n;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nn;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    a[e] *= rs[e / n] * rs[e % n];
 }
 
 // r = b - A x (one warp per row), also |r|_inf and |x|_inf into out[0..1]
@@ -115,6 +71,67 @@ __global__ void ldlt_residual_kernel(const double* __restrict__ a, int64_t n, co
     atomic_max_pos(out + 0, fabs(v));
     atomic_max_pos(out + 1, fabs(x[row]));
   }
+}
+
+// Checks and Ruiz equilibration in ONE cooperative launch (linalg.cpp:45-99):
+// the same quantities as ldlt_check_kernel / ldlt_colmax_kernel /
+// ldlt_scale_kernel, with the round control on the device (a per-round
+// maximum |cmax - 1| in scal[8 + round], read by every thread after the
+// grid barrier) instead of a host round trip per round.
+// scal: [0] max|A|, [1] max|A - A^T|, [2] #non-finite, [3] max cmax of the
+// final matrix, [8 + r] round r's deviation; all zeroed by the caller.
+__global__ void ldlt_prep_kernel(double* __restrict__ a, int64_t n, double* __restrict__ rs,
+                                 double* __restrict__ scale, double* __restrict__ cmax, double* scal) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = tid >> 5, nw = nt >> 5;
+  {
+    double amax = 0.0, asym = 0.0, bad = 0.0;
+    for (int64_t e = tid; e < n * n; e += nt) {
+      const int64_t i = e / n, j = e % n;
+      const double v = a[e];
+      if (!isfinite(v)) {
+        bad += 1.0;
+        continue;
+      }
+      amax = fmax(amax, fabs(v));
+      if (j < i) asym = fmax(asym, fabs(v - a[j * n + i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+      bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+      atomic_max_pos(scal + 0, amax);
+      if (asym == asym) atomic_max_pos(scal + 1, asym);
+      if (bad > 0) atomicAdd(scal + 2, bad);
+    }
+  }
+  grid.sync();
+  if (__ldcg(scal + 2) > 0 || __ldcg(scal + 1) > 1e-12 * fmax(1.0, __ldcg(scal + 0))) return;  // the host throws
+  for (int64_t i = tid; i < n; i += nt) scale[i] = 1.0;
+  for (int round = 0; round < 20; ++round) {
+    // cmax of row i == column i (symmetric): one warp per row
+    for (int64_t row = gw; row < n; row += nw) {
+      double m = 0.0;
+      for (int64_t k = lane; k < n; k += 32) m = fmax(m, fabs(a[row * n + k]));
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) {
+        cmax[row] = m;
+        rs[row] = m > 0.0 ? 1.0 / sqrt(m) : 1.0;
+        if (m > 0.0) atomic_max_pos(scal + 8 + round, fabs(m - 1.0));
+      }
+    }
+    grid.sync();
+    if (__ldcg(scal + 8 + round) <= 0.01) break;  // the same value in every thread
+    for (int64_t e = tid; e < n * n; e += nt) a[e] *= __ldcg(rs + e / n) * __ldcg(rs + e % n);
+    for (int64_t i = tid; i < n; i += nt) scale[i] *= __ldcg(rs + i);
+    grid.sync();
+  }
+  for (int64_t i = tid; i < n; i += nt) atomic_max_pos(scal + 3, __ldcg(cmax + i));  // cmax of the final matrix
 }
 
 // A(i, i) += delta_w for i < n_var; A(i, i) -= delta_c for i >= n_var
@@ -186,6 +203,7 @@ int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t
 }  // namespace
 
 constexpr int64_t kNativeMaxN = 20000;
+constexpr int kScal = 32;  // device scalars after the four n-vectors of d_vec_ (ldlt_prep_kernel)
 constexpr int64_t kCtaSolveMaxN = 3000;  // one-CTA substitution below (n 804: 0.20 vs 0.44 ms; 4500: 3.08 vs 2.45)
 
 // GBOPT_LDLT_TIMING=1: host wall time of the factorisation phases on stderr
@@ -249,7 +267,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
   f->stream_ = st;
   const size_t bytes = sizeof(double) * static_cast<size_t>(n) * n;
   f->palloc(&f->d_fact_, bytes);
-  f->palloc(&f->d_vec_, sizeof(double) * (4 * n + 8));  // rs | scale | cmax | x ... | scalars
+  f->palloc(&f->d_vec_, sizeof(double) * (4 * n + kScal));  // rs | scale | cmax | x ... | scalars
   f->palloc(&f->d_rhs_, sizeof(double) * n);
   if (on_device) {
     // try_mat = A + delta_w I (head) - delta_c I (tail), ipm.cpp:529-536:
@@ -269,42 +287,29 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
   double* scal = f->d_vec_ + 4 * n;  // 8 scalars
 
   pt.mark("setup+upload", st);
-  // checks (linalg.cpp:45-71)
-  CK(cudaMemsetAsync(scal, 0, sizeof(double) * 3, st));
-  ldlt_check_kernel<<<blocks_for(n * n, 256), 256, 0, st>>>(f->d_fact_, n, scal);
-  CK(cudaGetLastError());
-  double chk[3];
+  // checks (linalg.cpp:45-71) and Ruiz equilibration (linalg.cpp:72-99):
+  // one cooperative launch, one host round trip
+  CK(cudaMemsetAsync(scal, 0, sizeof(double) * kScal, st));
+  {
+    int sms_p = 0, per_p = 0;
+    CK(cudaDeviceGetAttribute(&sms_p, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_p, ldlt_prep_kernel, 256, 0));
+    const int g = std::max(1, std::min(sms_p * std::max(per_p, 1), blocks_for(n * n, 256)));
+    double* ap = f->d_fact_;
+    int64_t nn = n;
+    void* pargs[] = {&ap, &nn, &rs, &scale, &cmax, &scal};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(ldlt_prep_kernel), dim3(g), dim3(256), pargs, 0, st));
+  }
+  double chk[kScal];
+  f->scale_.assign(static_cast<size_t>(n), 1.0);
   CK(cudaMemcpyAsync(chk, scal, sizeof(chk), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(f->scale_.data(), scale, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (chk[2] > 0) throw NumericError("ldlt_factor: matrix contains NaN or Inf");
   if (chk[1] > 1e-12 * std::max(1.0, chk[0]))
     throw StructuralError("ldlt_factor: matrix is not symmetric (max deviation " + std::to_string(chk[1]) + ")");
-
   pt.mark("checks", st);
-  // Ruiz equilibration (linalg.cpp:72-99) on the device; the round control
-  // (max |cmax - 1|) is a host reduction of n values per round.
-  std::vector<double> h_cmax(static_cast<size_t>(n)), h_rs(static_cast<size_t>(n));
-  f->scale_.assign(static_cast<size_t>(n), 1.0);
-  for (int round = 0; round < 20; ++round) {
-    ldlt_colmax_kernel<<<blocks_for(n, 8), 256, 0, st>>>(f->d_fact_, n, cmax);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h_cmax.data(), cmax, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    double dev = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      h_rs[i] = h_cmax[i] > 0.0 ? 1.0 / std::sqrt(h_cmax[i]) : 1.0;
-      if (h_cmax[i] > 0.0) dev = std::max(dev, std::fabs(h_cmax[i] - 1.0));
-    }
-    if (dev <= 0.01) break;
-    CK(cudaMemcpyAsync(rs, h_rs.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    ldlt_scale_kernel<<<blocks_for(n * n, 256), 256, 0, st>>>(f->d_fact_, n, rs);
-    CK(cudaGetLastError());
-    for (int64_t i = 0; i < n; ++i) f->scale_[i] *= h_rs[i];
-  }
-  double bmax = 0.0;
-  for (int64_t i = 0; i < n; ++i) bmax = std::max(bmax, h_cmax[i]);  // cmax of the final matrix
-  f->zero_thresh_ = 1e-11 * bmax;
-  CK(cudaMemcpyAsync(scale, f->scale_.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  f->zero_thresh_ = 1e-11 * chk[3];
   pt.mark("ruiz", st);
   if (keep_input) {
     f->palloc(&f->d_input_, bytes);
