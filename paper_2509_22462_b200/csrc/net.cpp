@@ -4,7 +4,9 @@
 #include "net.hpp"
 
 #include "device_net.hpp"
+#include "parallel_host.hpp"
 
+#include <atomic>
 #include <cmath>
 #include <utility>
 
@@ -43,8 +45,15 @@ Net::Net(std::vector<HostLayer> layers) : layers_(std::move(layers)) {
     if (l > 0 && lay.cols != layers_[l - 1].rows)
       throw StructuralError(tag + " input width does not chain");
     if (lay.act < 0 || lay.act > kMaxActCode) throw StructuralError(tag + " bad activation kind");
-    for (double v : lay.w)
-      if (!std::isfinite(v)) throw NumericError(tag + " has non-finite entries");
+    std::atomic<bool> finite{true};
+    parallel_slices(static_cast<int64_t>(lay.w.size()), int64_t(1) << 20, [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i)
+        if (!std::isfinite(lay.w[static_cast<size_t>(i)])) {
+          finite = false;
+          return;
+        }
+    });
+    if (!finite) throw NumericError(tag + " has non-finite entries");
     for (double v : lay.b)
       if (!std::isfinite(v)) throw NumericError(tag + " has non-finite entries");
     if (lay.act == kSoftmax && l + 1 != layers_.size())

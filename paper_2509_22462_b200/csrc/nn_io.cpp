@@ -4,13 +4,16 @@
 // layer u32 rows, u32 cols, u8 activation, rows*cols f64 weights row-major,
 // rows f64 biases; no trailing bytes.  Activation code 4 (softplus) is this
 // build's extension (the reference accepts 0..3, nn_io.cpp:77,184).
+#include <atomic>
 #include <bit>
 #include <cerrno>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fcntl.h>
 #include <fstream>
+#include <unistd.h>
 #include <map>
 #include <memory>
 #include <sstream>
@@ -18,6 +21,7 @@
 #include <vector>
 
 #include "net.hpp"
+#include "parallel_host.hpp"
 
 #include "device_net.hpp"
 
@@ -327,6 +331,13 @@ std::unique_ptr<Net> load_weights(const std::string& path) {
   if (ends_with_json(path)) return load_weights_json(path);
   std::ifstream in(path, std::ios::binary);
   if (!in) throw IoError("load_weights: cannot open " + path);
+  struct Fd {
+    int fd;
+    ~Fd() {
+      if (fd >= 0) ::close(fd);
+    }
+  } fd_guard{::open(path.c_str(), O_RDONLY)};
+  const int fd = fd_guard.fd;
   char magic[4];
   if (!in.read(magic, 4) || std::memcmp(magic, kMagic, 4) != 0)
     throw FormatError("load_weights: " + path + " lacks the GBNN magic");
@@ -355,11 +366,30 @@ std::unique_ptr<Net> load_weights(const std::string& path) {
     lay.rows = rows;
     lay.cols = cols;
     lay.act = act;
-    // Row-major on disk and in host memory: one read per layer.
+    // Row-major on disk and in host memory: large payloads are read with
+    // parallel pread()s straight into the layer (no stream-buffer copy),
+    // small ones through the stream.
     lay.w.resize(static_cast<size_t>(rows) * cols);
-    if (!in.read(reinterpret_cast<char*>(lay.w.data()),
-                 static_cast<std::streamsize>(sizeof(double) * lay.w.size())))
+    const int64_t wbytes = static_cast<int64_t>(sizeof(double) * lay.w.size());
+    if (fd >= 0 && wbytes >= (int64_t(16) << 20)) {
+      const int64_t off0 = static_cast<int64_t>(in.tellg());
+      std::atomic<bool> ok{off0 >= 0};
+      char* dst = reinterpret_cast<char*>(lay.w.data());
+      parallel_slices(wbytes, int64_t(4) << 20, [&](int64_t a, int64_t b) {
+        while (a < b && ok) {
+          const ssize_t got = ::pread(fd, dst + a, static_cast<size_t>(b - a), static_cast<off_t>(off0 + a));
+          if (got <= 0) {
+            ok = false;
+            return;
+          }
+          a += got;
+        }
+      });
+      if (!ok) throw TruncatedError("load_weights: weight payload truncated in " + path);
+      in.seekg(off0 + wbytes);
+    } else if (!in.read(reinterpret_cast<char*>(lay.w.data()), static_cast<std::streamsize>(wbytes))) {
       throw TruncatedError("load_weights: weight payload truncated in " + path);
+    }
     lay.b.resize(rows);
     if (!in.read(reinterpret_cast<char*>(lay.b.data()), static_cast<std::streamsize>(sizeof(double) * rows)))
       throw TruncatedError("load_weights: bias payload truncated in " + path);

@@ -273,3 +273,25 @@ def test_compute_without_device_fails_loudly():
     with pytest.raises(gb.DeviceError):
         net.bind_device(0)
     assert net.device == -1
+
+
+def test_large_gbnn_round_trip_and_truncation(tmp_path):
+    """Payloads >= 16 MB take the parallel pread path (nn_io.cpp): identical
+    weights after a round trip, TruncatedError on a cut file."""
+    import paper_2509_22462_b200 as gb
+    net = gb.random_net([300, 2100, 8], "tanh", "linear", 5)  # 2100 x 300 and 8 x 2100
+    big = gb.random_net([2100, 2100, 3], "sigmoid", "linear", 6)  # 35 MB first layer
+    for k, n in (("a", net), ("b", big)):
+        path = str(tmp_path / f"{k}.gbnn")
+        gb.save_weights(n, path)
+        back = gb.load_weights(path)
+        for l in range(n.layer_count):
+            w0, b0, a0 = n.layer(l)
+            w1, b1, a1 = back.layer(l)
+            assert np.array_equal(w0, w1) and np.array_equal(b0, b1) and a0 == a1
+    path = str(tmp_path / "b.gbnn")
+    data = open(path, "rb").read()
+    cut = str(tmp_path / "cut.gbnn")
+    open(cut, "wb").write(data[: len(data) // 2])
+    with pytest.raises(gb.TruncatedError):
+        gb.load_weights(cut)
