@@ -72,6 +72,13 @@ struct DenseMat {
   double operator()(int64_t i, int64_t j) const { return data[static_cast<size_t>(i * cols + j)]; }
 };
 
+// Per-layer values of one forward pass (reference nn.hpp:31-36):
+// z[l] = W_l y[l-1] + b_l (y[-1] = x), y[l] = sigma_l(z[l]).
+struct ForwardTrace {
+  std::vector<std::vector<double>> z;
+  std::vector<std::vector<double>> y;
+};
+
 enum class ActivationKind : int32_t { Linear = 0, Tanh = 1, Sigmoid = 2, Softmax = 3, Softplus = 4 };
 
 struct Layer {
@@ -188,6 +195,30 @@ class NeuralNet {
     hess_lower->assign(static_cast<size_t>(n * (n + 1) / 2), 0.0);
     check(gbopt_net_oracle_lower(h_.get(), 1, x.data(), x.size(), lambda.data(), lambda.size(), y ? y->data() : nullptr,
                                  jac ? jac->data.data() : nullptr, hess_lower->data(), hess_lower->size()));
+  }
+
+  // nn.hpp:31-36, nn.cpp:127-146
+  ForwardTrace forward_trace(const RealVec& x) const {
+    check_len(x, input_dim(), "forward_trace");
+    std::vector<int64_t> rows;
+    int64_t total = 0;
+    for (int64_t l = 0; l < layer_count(); ++l) {
+      int64_t r = 0, c = 0;
+      int32_t act = 0;
+      check(gbopt_net_layer_info(h_.get(), l, &r, &c, &act));
+      rows.push_back(r);
+      total += r;
+    }
+    RealVec z(static_cast<size_t>(total)), y(static_cast<size_t>(total));
+    check(gbopt_net_forward_trace(h_.get(), x.data(), x.size(), z.data(), y.data(), z.size()));
+    ForwardTrace t;
+    int64_t off = 0;
+    for (int64_t r : rows) {
+      t.z.emplace_back(z.begin() + off, z.begin() + off + r);
+      t.y.emplace_back(y.begin() + off, y.begin() + off + r);
+      off += r;
+    }
+    return t;
   }
 
   const gbopt_net* handle() const { return h_.get(); }

@@ -162,6 +162,15 @@ int gbopt_net_device(const gbopt_net* net);
 gbopt_status gbopt_net_forward(const gbopt_net* net, const double* x,
                                size_t n, double* y, size_t m);
 
+/* Per-layer values of one forward pass (reference ForwardTrace,
+ * nn.hpp:31-36, NeuralNet::forward_trace, nn.cpp:127-146):
+ * z_l = W_l y_{l-1} + b_l and y_l = sigma_l(z_l), layers concatenated
+ * (z = [z_0 | z_1 | ...], same for y); len == sum of the layers' output
+ * widths for both buffers. */
+gbopt_status gbopt_net_forward_trace(const gbopt_net* net, const double* x,
+                                     size_t n, double* z, double* y,
+                                     size_t len);
+
 /* J = dy/dx, m x n row-major, jac_len == m*n.  (nn.cpp:148-170) */
 gbopt_status gbopt_net_jacobian(const gbopt_net* net, const double* x,
                                 size_t n, double* jac, size_t jac_len);

@@ -292,6 +292,31 @@ gbopt_status gbopt_net_forward(const gbopt_net* net, const double* x, size_t n, 
   });
 }
 
+gbopt_status gbopt_net_forward_trace(const gbopt_net* net, const double* x, size_t n, double* z, double* y,
+                                     size_t len) {
+  if (net == nullptr || x == nullptr || z == nullptr || y == nullptr)
+    return fail_argument("gbopt_net_forward_trace: pointer arguments must be non-null");
+  const gbb::Net& nn = *net->net;
+  int64_t total = 0;
+  for (int64_t l = 0; l < nn.layer_count(); ++l) total += nn.layer(l).rows;
+  if (static_cast<int64_t>(n) != nn.input_dim() || static_cast<int64_t>(len) != total)
+    return fail_argument("gbopt_net_forward_trace: buffer lengths do not match the network dimensions");
+  return guarded([&] {
+    gbb::DeviceNet& d = net->net->device();
+    const int64_t L = nn.layer_count();
+    const int64_t last = nn.layer(L - 1).rows;
+    // one forward pass; the final y (softmax applied) is the output, the
+    // rest are the forward chain's per-layer buffers
+    d.evaluate_host(1, x, nullptr, y + (total - last), nullptr, nullptr, nullptr);
+    int64_t off = 0;
+    for (int64_t l = 0; l < L; ++l) {
+      d.copy_intermediate("z", static_cast<int>(l), 1, z + off);
+      if (l + 1 < L) d.copy_intermediate("y", static_cast<int>(l), 1, y + off);
+      off += nn.layer(l).rows;
+    }
+  });
+}
+
 gbopt_status gbopt_net_jacobian(const gbopt_net* net, const double* x, size_t n, double* jac, size_t jac_len) {
   if (net == nullptr || x == nullptr || jac == nullptr)
     return fail_argument("gbopt_net_jacobian: pointer arguments must be non-null");

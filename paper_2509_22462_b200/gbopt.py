@@ -74,6 +74,7 @@ _net_oracle = _fn("gbopt_net_oracle", _status, _vp, _dp, _sz, _dp, _sz, _dp, _dp
 _net_oracle_batched = _fn("gbopt_net_oracle_batched", _status, _vp, _sz, _dp, _sz, _dp, _sz, _dp, _dp, _dp)
 _net_oracle_batched_device = _fn("gbopt_net_oracle_batched_device", _status, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp,
                                  _vp, _vp)
+_net_forward_trace = _fn("gbopt_net_forward_trace", _status, _vp, _dp, _sz, _dp, _dp, _sz)
 _net_oracle_lower = _fn("gbopt_net_oracle_lower", _status, _vp, _sz, _dp, _sz, _dp, _sz, _dp, _dp, _dp, _sz)
 _net_last_launch_count = _fn("gbopt_net_last_launch_count", _i64, _vp)
 _net_set_schedule = _fn("gbopt_net_set_schedule", _status, _vp, ctypes.c_int)
@@ -358,6 +359,17 @@ class NeuralNet:
         _check(_net_oracle(self._h, _dptr(x), x.size, _dptr(lam), m if lam is None else lam.size,
                            _dptr(y), _dptr(j), _dptr(h)))
         return y, j, h
+
+    def forward_trace(self, x):
+        """Per-layer (z_l, y_l) of one forward pass (reference
+        NeuralNet::forward_trace, nn.cpp:127-146): two lists of vectors."""
+        x = _vec(x)
+        rows = [self.layer(l)[0].shape[0] for l in range(self.layer_count)]
+        z = np.empty(sum(rows))
+        y = np.empty(sum(rows))
+        _check(_net_forward_trace(self._h, _dptr(x), x.size, _dptr(z), _dptr(y), z.size))
+        cuts = np.cumsum(rows)[:-1]
+        return list(np.split(z, cuts)), list(np.split(y, cuts))
 
     def oracle_lower(self, x, lam, want_y=True, want_j=True):
         """(y, J, Hl) at one point with the Hessian as its packed lower triangle in

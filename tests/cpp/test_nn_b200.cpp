@@ -3,6 +3,7 @@
 // cases of proj/tests/test_formulations.cpp:215-274.
 //   ./test_nn_b200        host-side checks (no GPU needed)
 //   ./test_nn_b200 gpu    + device checks (oracle, reduced-space callbacks)
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -67,6 +68,16 @@ int main(int argc, char** argv) {
   CHECK(std::fabs(y[0] + y[1] + y[2] - 1.0) <= 1e-12);  // softmax simplex (test_capi.cpp:42-43)
   RealVec y2 = back.forward(x);
   CHECK(y == y2);
+  {  // forward_trace (nn.cpp:127-146): the last y is the forward output, z_L its pre-softmax values
+    ForwardTrace tr = net.forward_trace(x);
+    CHECK(tr.z.size() == 2 && tr.y.size() == 2 && tr.z[0].size() == 6 && tr.y[1].size() == 3);
+    CHECK(tr.y[1] == y);
+    double zs = 0.0, mx = tr.z[1][0];
+    for (double v : tr.z[1]) mx = std::max(mx, v);
+    for (double v : tr.z[1]) zs += std::exp(v - mx);
+    CHECK(std::fabs(std::exp(tr.z[1][0] - mx) / zs - y[0]) <= 1e-14);
+    CHECK(throws<StructuralError>([&] { net.forward_trace(RealVec(3, 0.0)); }));  // nn.cpp:105-111
+  }
   // J vs central differences (test_nn.cpp:96-108 style)
   NeuralNet t = random_net({5, 7, 4}, "tanh", "tanh", 1234);
   const RealVec xt = {0.3, -0.2, 0.5, 1.1, -0.7};

@@ -290,3 +290,23 @@ def test_batched_intermediates_match_single(monkeypatch):
                     assert np.abs(got).max() == 0, (name, l)
                 else:
                     assert orc.rel_err(got, want) <= 1e-13, (name, l, b)
+
+
+@pytest.mark.parametrize("widths,hid,fin", [([5, 7, 4], "tanh", "softmax"), ([784, 512, 512, 10], "tanh", "linear"),
+                                             ([20, 64, 48, 3], "softplus", "sigmoid"), ([3, 2], "sigmoid", "tanh")])
+def test_forward_trace_matches_oracle(widths, hid, fin):
+    """forward_trace (nn.cpp:127-146): per-layer z and y of the device
+    forward chain against the oracle restatement; the last y is the forward
+    output (softmax applied)."""
+    net = gb.random_net(widths, hid, fin, 12)
+    ref = orc.NeuralNet([orc.Layer(*net.layer(l)) for l in range(net.layer_count)])
+    x = np.random.default_rng(1).uniform(-1, 1, widths[0])
+    zs, ys = net.forward_trace(x)
+    rz, ry = ref.forward_trace(x)
+    assert len(zs) == len(rz) == net.layer_count
+    for l in range(net.layer_count):
+        assert orc.rel_err(zs[l], rz[l]) <= 1e-13, ("z", l)
+        assert orc.rel_err(ys[l], ry[l]) <= 1e-13, ("y", l)
+    assert np.array_equal(ys[-1], net.forward(x))
+    with pytest.raises(gb.ArgumentError):
+        net.forward_trace(x[:-1])
