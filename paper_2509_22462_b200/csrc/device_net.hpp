@@ -132,6 +132,10 @@ class DeviceNet {
   // ("z", "y", "s1", "s2", "ybar", "gz", "d") for `nb` points into out
   // (nb x rows(l), row-major).  Synchronous; for white-box tests.
   void copy_intermediate(const char* name, int layer, int nb, double* out);
+  struct AdjLayout {
+    int kw = 2, gx = 1, crows = 128, chunks = 1;
+  };
+  AdjLayout adj_layout(const DevLayer& d, bool multi) const;
   // Eager run with CUDA events around every launch (on the launching stream).
   void profile(int nb, const double* dx, const double* dlam, std::vector<ProfResult>* out, bool timeline = false);
   // Device buffers, ordered on `user` stream, asynchronous.

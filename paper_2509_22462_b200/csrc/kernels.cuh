@@ -786,39 +786,57 @@ __global__ void adj_seed_kernel(const double* __restrict__ lam, int64_t ld_lam, 
 constexpr int kAdjThreads = 256;
 constexpr int kAdjRows = 128;
 
-template <int NB>
+// KW adjacent k per thread (2: one 16-B load per row; 4: two), so a row's
+// NB shared-memory gz values are reused over KW columns -- the multi-vector
+// sweeps (reverse-mode J: NB = 12 / 16) are otherwise bound by those loads.
+template <int NB, int KW = 2>
 __global__ void __launch_bounds__(kAdjThreads)
     adj_cols_kernel(const double* __restrict__ w, int64_t ldw, int rows, int k_dim, const double* __restrict__ gz,
-                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part) {
+                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows) {
+  static_assert(KW == 2 || KW == 4, "KW");
   __shared__ double gs[NB][kAdjRows];
-  const int k = 2 * (blockIdx.x * kAdjThreads + threadIdx.x);
-  const int r0 = blockIdx.y * kAdjRows;
-  const int nr = min(kAdjRows, rows - r0);
+  const int k = KW * (blockIdx.x * kAdjThreads + threadIdx.x);
+  const int r0 = blockIdx.y * crows;  // crows <= kAdjRows rows per chunk
+  const int nr = min(crows, rows - r0);
   for (int e = threadIdx.x; e < NB * kAdjRows; e += kAdjThreads) {
     const int b = e / kAdjRows, i = e % kAdjRows;
     gs[b][i] = (p0 + b < nb && i < nr) ? gz[static_cast<int64_t>(p0 + b) * ld_gz + r0 + i] : 0.0;
   }
   __syncthreads();
   if (k >= k_dim) return;
-  double a0[NB], a1[NB];
+  double a[NB][KW];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0;
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int c = 0; c < KW; ++c) a[b][c] = 0.0;
   const double* wp = w + static_cast<int64_t>(r0) * ldw + k;
-#pragma unroll 16
+#pragma unroll (KW == 2 ? 16 : 8)
   for (int i = 0; i < nr; ++i) {
-    const double2 wv = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw));
+    double wv[KW];
+    const double2 w01 = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw));
+    wv[0] = w01.x;
+    wv[1] = w01.y;
+    if constexpr (KW == 4) {
+      // k + 2 < ldw always (ldw is a multiple of 16 and k a multiple of 4);
+      // columns past k_dim are the zero padding
+      const double2 w23 = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw + 2));
+      wv[2] = w23.x;
+      wv[3] = w23.y;
+    }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      a0[b] = fma(wv.x, gs[b][i], a0[b]);
-      a1[b] = fma(wv.y, gs[b][i], a1[b]);
+      const double g = gs[b][i];
+#pragma unroll
+      for (int c = 0; c < KW; ++c) a[b][c] = fma(wv[c], g, a[b][c]);
     }
   }
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (p0 + b >= nb) break;
     double* o = partial + (static_cast<int64_t>(blockIdx.y) * nb + p0 + b) * ld_part + k;
-    o[0] = a0[b];
-    if (k + 1 < k_dim) o[1] = a1[b];
+#pragma unroll
+    for (int c = 0; c < KW; ++c)
+      if (k + c < k_dim) o[c] = a[b][c];
   }
 }
 

@@ -244,6 +244,20 @@ int DeviceNet::syrk_split(int points, int k_blocks) const {
   return std::max(1, std::min(sm_count_ / tiles, k_blocks / 8));
 }
 
+// Adjoint sweep layout of a layer: columns per thread (4 for multi-vector
+// sweeps of wide layers -- the shared-memory gz values reused over more
+// columns -- else 2) and rows per chunk (kAdjRows, halved down to 16 while
+// the grid would not cover two waves).
+DeviceNet::AdjLayout DeviceNet::adj_layout(const DevLayer& d, bool multi) const {
+  AdjLayout a;
+  a.kw = multi && ceil_div(d.cols, 4 * dev::kAdjThreads) * ceil_div(d.rows, dev::kAdjRows) >= 2 * sm_count_ ? 4 : 2;
+  a.gx = static_cast<int>(ceil_div(d.cols, a.kw * dev::kAdjThreads));
+  a.crows = dev::kAdjRows;
+  while (a.crows > 16 && a.gx * ceil_div(d.rows, a.crows) < 2 * sm_count_) a.crows /= 2;
+  a.chunks = static_cast<int>(ceil_div(d.rows, a.crows));
+  return a;
+}
+
 void DeviceNet::ensure_workspace(int batch) {
   if (batch <= ws_cap_) return;
   free_workspace();
@@ -279,7 +293,9 @@ void DeviceNet::ensure_workspace(int batch) {
   // adjoint partials: [chunks][cap][ldmax]
   int64_t rmax = 1;
   for (auto& d : layers_) rmax = std::max(rmax, d.rows);
-  w.adj_chunks_max = ceil_div(rmax, dev::kAdjRows);
+  w.adj_chunks_max = 1;
+  for (auto& d : layers_)
+    for (bool multi : {false, true}) w.adj_chunks_max = std::max(w.adj_chunks_max, adj_layout(d, multi).chunks);
   w.ld_part = ldt_ > w.ld_in ? ldt_ : w.ld_in;
   w.adj_part = ws_alloc(static_cast<size_t>(w.adj_chunks_max) * vcap * w.ld_part);
   // tangents (only needed with >= 2 layers)
@@ -666,26 +682,30 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         batch_gemm(sb, nv, w.tm_gz[static_cast<size_t>(l)], d, true, &e, e.ybar);
         continue;
       }
-      const int chunks = ceil_div(d.rows, dev::kAdjRows);
-      dim3 grid(ceil_div(d.cols, 2 * dev::kAdjThreads), chunks);
+      const AdjLayout al = adj_layout(d, nv >= 5);
+      const int kw = al.kw, gx = al.gx, crows = al.crows, chunks = al.chunks;
+      dim3 grid(gx, chunks);
       for (int p0 = 0; p0 < nv;) {
         const int left = nv - p0;
-        // one weight sweep per up to 16 vectors (reverse-mode J: m <= 16 seeds per point)
-        const int pass = left >= 9 ? 16 : (left >= 5 ? 8 : (left >= 2 ? 4 : 1));
+        // one weight sweep per up to 16 vectors (reverse-mode J: m <= 16
+        // seeds per point)
+        const int pass = left >= 13 ? 16 : (left >= 9 ? 12 : (left >= 5 ? 8 : (left >= 2 ? 4 : 1)));
         prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * std::min(pass, left), 8.0 * d.rows * d.cols);
+#define GBB_ADJ(NBV, KWV)                                                                                          \
+  dev::adj_cols_kernel<NBV, KWV><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l], nv, \
+                                                                    p0, w.adj_part, w.ld_part, crows)
         if (pass == 16) {
-          dev::adj_cols_kernel<16><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                      nv, p0, w.adj_part, w.ld_part);
+          if (kw == 4) GBB_ADJ(16, 4); else GBB_ADJ(16, 2);
+        } else if (pass == 12) {
+          if (kw == 4) GBB_ADJ(12, 4); else GBB_ADJ(12, 2);
         } else if (pass == 8) {
-          dev::adj_cols_kernel<8><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                     nv, p0, w.adj_part, w.ld_part);
+          if (kw == 4) GBB_ADJ(8, 4); else GBB_ADJ(8, 2);
         } else if (pass == 4) {
-          dev::adj_cols_kernel<4><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                     nv, p0, w.adj_part, w.ld_part);
+          GBB_ADJ(4, 2);
         } else {
-          dev::adj_cols_kernel<1><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l],
-                                                                     nv, p0, w.adj_part, w.ld_part);
+          GBB_ADJ(1, 2);
         }
+#undef GBB_ADJ
         p0 += pass;
         after_launch(sb);
       }
