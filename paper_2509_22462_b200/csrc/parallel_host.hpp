@@ -11,7 +11,8 @@
 namespace gbb {
 
 // Calls fn(begin, end) on up to `max_threads` contiguous slices of
-// [0, n); slices below `grain` elements are not split further.
+// [0, n); slices below `grain` elements are not split further.  fn must not
+// throw (report failures through captured state, as the callers do).
 template <class Fn>
 void parallel_slices(int64_t n, int64_t grain, Fn&& fn, int max_threads = 8) {
   const int64_t hw = std::max<int64_t>(1, std::thread::hardware_concurrency());
