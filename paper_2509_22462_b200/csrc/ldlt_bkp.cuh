@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxRowsPerThread = 4;  // n <= 2048
+constexpr int kMaxRowsPerThread = 4;  // n <= 2048 (logical indices fit the 12-bit key field)
 constexpr int kMaxNb = 32;
 constexpr int kUpdRows = 16;  // trailing rows per CTA pass
 constexpr double kAlpha = 0.64038820320220756872;  // (1 + sqrt(17)) / 8
@@ -126,8 +126,12 @@ __device__ double panel_column(const Params& p, const Panel& s, int n, int q, in
   }
   __syncthreads();
   if (qn >= 0) load_row(p, n, qn, next);
-  double m = -1.0;
-  int mi = -1;
+  // off-diagonal argmax as ONE 64-bit key per candidate: |v| with its low 12
+  // mantissa bits replaced by (4095 - logical index), so an integer max picks
+  // the largest |v| (to 2^-40 relative) and, among ties, the smallest index;
+  // key 0 = no candidate.  (A (double, index) pair reduction costs ~3x more
+  // in dependent shuffle/compare rounds: tools/panel_gemv_probe.cu.)
+  unsigned long long key = 0;
 #pragma unroll
   for (int t = 0; t < kMaxRowsPerThread; ++t) {
     const int P = threadIdx.x + t * kThreads;
@@ -141,11 +145,31 @@ __device__ double panel_column(const Params& p, const Panel& s, int n, int q, in
     if (c < jj) s0 = fma(s.W[c * n + P], s.zs[c], s0);
     const double v = arow[t] - (s0 + s1);
     out[P] = v;
-    if (P != q) max_pair(m, mi, fabs(v), s.inv[P]);
+    if (P != q) {
+      const unsigned long long k2 = (static_cast<unsigned long long>(__double_as_longlong(fabs(v))) & ~0xFFFull) |
+                                    static_cast<unsigned long long>(0xFFF - s.inv[P]);
+      key = k2 > key ? k2 : key;
+    }
   }
-  cta_max(m, mi, rv, ri);
-  idx = mi;
-  return m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
+    key = k2 > key ? k2 : key;
+  }
+  unsigned long long* kw = reinterpret_cast<unsigned long long*>(rv);  // kWarps slots
+  if (lane == 0) kw[warp] = key;
+  __syncthreads();
+  unsigned long long best = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) best = kw[w] > best ? kw[w] : best;
+  __syncthreads();  // kw reusable
+  if (best == 0) {
+    idx = -1;
+    return -1.0;
+  }
+  idx = 0xFFF - static_cast<int>(best & 0xFFF);
+  return fabs(out[s.loc[idx]]);  // the exact value of the winner
 }
 
 __global__ void __launch_bounds__(kThreads, 1) bkp_factor_kernel(Params p) {
