@@ -332,7 +332,12 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     f->native_ = true;
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    const size_t smem = sizeof(double) * static_cast<size_t>(n);
+    // blocked grid kernel: panel width (GBOPT_LDLT_GRID_NB; 0 = unblocked
+    // left-looking, every column update spanning all previous columns)
+    int grid_nb = 64;
+    if (const char* e = std::getenv("GBOPT_LDLT_GRID_NB")) grid_nb = std::max(0, std::min(std::atoi(e), bk::kMaxGridNb));
+    const size_t smem =
+        sizeof(double) * static_cast<size_t>(std::max<int64_t>(n, bk::trailing_smem_doubles(grid_nb)));
     CK(cudaFuncSetAttribute(bk::bk_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bk::bk_factor_kernel, bk::kThreads, smem));
     if (per_sm < 1) throw DeviceError("ldlt_factor: the Bunch-Kaufman kernel does not fit on an SM");
@@ -370,6 +375,8 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     F.perm = f->d_bki_ + n;
     F.n = static_cast<int>(n);
     F.ldl = static_cast<int>(f->ldl_);
+    F.nb = grid_nb;
+    F.trace = nullptr;
     CK(cudaMemsetAsync(F.e, 0, sizeof(double) * n, st));
     // Kernel choice (GBOPT_LDLT_KERNEL = panel | cluster | grid forces one):
     //   panel   (ldlt_bkp.cuh): blocked; CTA 0 factors nb-column panels in
@@ -563,6 +570,8 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       CK(cudaEventCreate(&t0));
       CK(cudaEventCreate(&t1));
       CK(cudaEventRecord(t0, st));
+      CK(cudaMalloc(&F.trace, sizeof(long long) * 2));
+      CK(cudaMemsetAsync(F.trace, 0, sizeof(long long) * 2, st));
     }
     if (!use_cluster && !use_panel)
       CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_factor_kernel), dim3(grid), dim3(bk::kThreads),
@@ -572,8 +581,12 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       CK(cudaEventSynchronize(t1));
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, t0, t1));
-      std::fprintf(stderr, "ldlt: n %lld grid %d per_sm %d bk_factor_kernel %.3f ms\n", static_cast<long long>(n), grid,
-                   per_sm, ms);
+      long long tr[2];
+      CK(cudaMemcpy(tr, F.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+      CK(cudaFree(F.trace));
+      std::fprintf(stderr, "ldlt: n %lld grid %d per_sm %d nb %d bk_factor_kernel %.3f ms; CTA-0 clocks: trailing "
+                   "updates %lld of %lld\n",
+                   static_cast<long long>(n), grid, per_sm, grid_nb, ms, tr[0], tr[1]);
       cudaEventDestroy(t0);
       cudaEventDestroy(t1);
     }

@@ -58,6 +58,9 @@ struct Factor {
   double* part2;  // [2 * grid] the same for column r (separate: CTAs may still read part)
   int n;
   int ldl;
+  int nb;  // > 0: blocked -- column updates span only the current panel's
+           // columns, and the trailing A takes a rank-nb update per panel
+  long long* trace;  // null, or [2]: CTA 0's clocks in trailing updates (incl. their barrier), whole kernel
 };
 
 // (value, index) maximum with ties to the smaller index
@@ -98,24 +101,26 @@ __device__ double grid_max(const double* part, int& idx, double* sv, int* si) {
   return cta_max(v, idx, sv, si);
 }
 
-// v[0:k] = W(row, 0:k) = (D L(row, 0:k)^T)^T into shared memory (16-byte loads)
-__device__ void d_times_lrow(const Factor& F, int row, int k, double* v) {
+// v[j0:k] = W(row, j0:k) = (D L(row, j0:k)^T)^T into shared memory (16-byte
+// loads; j0 even, v[j0 .. k0) zeroed by the caller's choice of k0)
+__device__ void d_times_lrow(const Factor& F, int row, int k0, int k, double* v) {
   const double* wr = F.wd + static_cast<int64_t>(row) * F.ldl;
-  for (int j = 2 * threadIdx.x; j < k; j += 2 * kThreads) {
+  const int j0 = k0 & ~1;
+  for (int j = j0 + 2 * threadIdx.x; j < k; j += 2 * kThreads) {
     if (j + 1 < k) {
       const double2 t = __ldcg(reinterpret_cast<const double2*>(wr + j));
-      v[j] = t.x;
+      v[j] = j < k0 ? 0.0 : t.x;  // only j0 = k0 - 1 can be outside the panel
       v[j + 1] = t.y;
     } else {
-      v[j] = __ldcg(wr + j);
+      v[j] = j < k0 ? 0.0 : __ldcg(wr + j);
     }
   }
 }
 
 // out[i] = A[i][col] - L(i, 0:k) . v for i >= k (one warp per row), and the
 // CTA's maximum of |out[i]| over i >= k, i != skip
-__device__ double column_update(const Factor& F, int col, int k, const double* v, double* out, int skip, int& idx,
-                                double* sv, int* si) {
+__device__ double column_update(const Factor& F, int col, int k0, int k, const double* v, double* out, int skip,
+                                int& idx, double* sv, int* si) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   double m = -1.0;
@@ -125,7 +130,7 @@ __device__ double column_update(const Factor& F, int col, int k, const double* v
     // 16-byte loads, four in flight per lane (the rows are latency-bound
     // otherwise: one dependent load per 32 lanes per iteration)
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int j = 2 * lane;
+    int j = (k0 & ~1) + 2 * lane;  // the panel's columns (v is 0 before k0)
     for (; j + 192 + 1 < k; j += 256) {
       const double2 a0 = __ldcg(reinterpret_cast<const double2*>(li + j));
       const double2 a1 = __ldcg(reinterpret_cast<const double2*>(li + j + 64));
@@ -164,8 +169,8 @@ __device__ double column_update(const Factor& F, int col, int k, const double* v
 // step, w'_i = A(i,k+1) - L(i,0:k) W(k+1,0:k)^T - L(i,k) W(k+1,k), with the
 // new column applied as a rank-1 term from registers -- one grid barrier
 // per such pivot instead of two.  v[0:k] = W(k+1, 0:k) must be staged.
-__device__ double lookahead_update(const Factor& F, int k, double dk, const double* w, const double* v, double vk,
-                                   double* wn, int& idx, double* sv, int* si) {
+__device__ double lookahead_update(const Factor& F, int k0, int k, double dk, const double* w, const double* v,
+                                   double vk, double* wn, int& idx, double* sv, int* si) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   double m = -1.0;
@@ -173,7 +178,7 @@ __device__ double lookahead_update(const Factor& F, int k, double dk, const doub
   for (int i = k + 1 + gw; i < F.n; i += nw) {
     const double* li = F.l + static_cast<int64_t>(i) * F.ldl;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int j = 2 * lane;
+    int j = (k0 & ~1) + 2 * lane;  // the panel's columns (v is 0 before k0)
     for (; j + 192 + 1 < k; j += 256) {
       const double2 a0 = __ldcg(reinterpret_cast<const double2*>(li + j));
       const double2 a1 = __ldcg(reinterpret_cast<const double2*>(li + j + 64));
@@ -213,6 +218,115 @@ __device__ double lookahead_update(const Factor& F, int k, double dk, const doub
   return cta_max(m, idx, sv, si);
 }
 
+// Blocked mode: the trailing update runs on the FP64 tensor pipe
+// (mma.sync m8n8k4 DMMA) over 64 x 64 tiles; a tile's L rows and W rows
+// (panel columns, zero-padded to a multiple of 4) are staged row-major with
+// a pitch of 4 mod 16 doubles, which makes both the coalesced staging stores
+// and the fragment loads (8 rows x 4 columns per warp) bank-conflict-free.
+constexpr int kTile = 64;
+constexpr int kMaxGridNb = 128;  // panel width cap (a panel may end one column late, at a 2x2 pivot)
+
+// staged columns: [k0 & ~1, k1) rounded up to 4 (a panel is at most nb + 1 wide)
+__host__ __device__ constexpr int tile_pitch(int nb) { return (((nb + 2 + 3) / 4 * 4 - 4 + 15) / 16) * 16 + 4; }
+__host__ __device__ constexpr int trailing_smem_doubles(int nb) { return nb > 0 ? 2 * kTile * tile_pitch(nb) : 0; }
+
+// 16-byte global -> shared copy through L2 only (the panel's columns were
+// written by other CTAs: no L1), bypassing registers; the bytes past
+// src_bytes are zero-filled
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// D(8x8) += A(8x4, row) B(4x8, col) on the FP64 tensor pipe
+__device__ __forceinline__ void dmma884_bk(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// A(i, j) -= sum_{c in [k0, k1)} L(i, c) W(j, c) for i, j in [k1, n): the
+// panel's rank-(k1 - k0) update of the trailing square, so that the next
+// panel's column updates span only its own columns.  64 x 64 tiles strided
+// over the grid; 8 warps as 2 x 4, a warp owning 32 rows x 16 columns
+// (4 x 2 DMMA tiles); the k order is fixed (deterministic).
+__device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
+  const int n = F.n, w = k1 - k0, m = n - k1;
+  if (m <= 0 || w <= 0) return;
+  const int jb = k0 & ~1;                          // 16-byte aligned first staged column
+  const int w4 = (k1 - jb + 3) & ~3, pitch = tile_pitch(F.nb);
+  const int tiles = (m + kTile - 1) / kTile;
+  double* const ls = sm;                  // [64][pitch]: ls[r][c] = L(i0 + r, jb + c) (0 for columns < k0)
+  double* const ws = sm + kTile * pitch;  // [64][pitch]: ws[r][c] = W(j0 + r, jb + c)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wr0 = (warp >> 2) * 32, wc0 = (warp & 3) * 16;  // the warp's sub-tile
+  const int fr = lane >> 2, fk = lane & 3;                    // fragment row / k of this lane
+  for (int t = blockIdx.x; t < tiles * tiles; t += gridDim.x) {
+    const int i0 = k1 + (t / tiles) * kTile, j0 = k1 + (t % tiles) * kTile;
+    __syncthreads();  // the previous tile's reads (or v) are done
+    // asynchronous 8-byte copies (zero-filled outside the matrix / panel):
+    // every load of the tile in flight at once
+    for (int e = threadIdx.x; e < kTile * (w4 / 2); e += kThreads) {
+      const int r = e / (w4 / 2), c = 2 * (e - r * (w4 / 2));
+      const int i = i0 + r, j = j0 + r;
+      const int valid = 8 * max(0, min(2, k1 - (jb + c)));
+      const int cs = valid ? c : 0;
+      cp_async16(ls + r * pitch + c, F.l + static_cast<int64_t>(i < n ? i : k1) * F.ldl + jb + cs, i < n ? valid : 0);
+      cp_async16(ws + r * pitch + c, F.wd + static_cast<int64_t>(j < n ? j : k1) * F.ldl + jb + cs, j < n ? valid : 0);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (jb < k0) {  // odd panel start: column k0 - 1 belongs to the previous panel
+      __syncthreads();
+      if (threadIdx.x < kTile) ls[threadIdx.x * pitch] = 0.0;
+    }
+    __syncthreads();
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const double* la = ls + (wr0 + fr) * pitch + fk;
+    const double* wb = ws + (wc0 + fr) * pitch + fk;
+#pragma unroll 2
+    for (int kk = 0; kk < w4; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = la[a * 8 * pitch + kk];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) bf[b] = wb[b * 8 * pitch + kk];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma884_bk(acc[a][b], af[a], bf[b]);
+    }
+    // all 16 loads of A first, then the stores (a load -> store chain per
+    // element would serialise on the memory latency)
+    double old[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = i0 + wr0 + a * 8 + fr;
+      const double* ar = F.a + static_cast<int64_t>(i) * n;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int j = j0 + wc0 + b * 8 + 2 * fk;
+        old[a][b][0] = (i < n && j < n) ? __ldcg(ar + j) : 0.0;
+        old[a][b][1] = (i < n && j + 1 < n) ? __ldcg(ar + j + 1) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = i0 + wr0 + a * 8 + fr;
+      double* ar = F.a + static_cast<int64_t>(i) * n;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int j = j0 + wc0 + b * 8 + 2 * fk;
+        if (i < n && j < n) ar[j] = old[a][b][0] - acc[a][b][0];
+        if (i < n && j + 1 < n) ar[j + 1] = old[a][b][1] - acc[a][b][1];
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
   extern __shared__ double smem[];
   double* v = smem;               // [n]
@@ -224,15 +338,18 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
 
   int cur = 0;        // which of (w, part) / (w2, part3) holds the current column
   bool pre = false;   // column k already computed (and its maxima published) by a look-ahead
+  int k0 = 0;         // first column of the current panel (blocked mode; 0 throughout otherwise)
+  const long long c_start = clock64();
+  long long c_upd = 0;
   for (int k = 0; k < n;) {
     double* const wk = cur ? F.w2 : F.w;
     double* const pk = cur ? F.part3 : F.part;
     if (!pre) {
       // ---- updated column k and its maximum below the diagonal ----
-      d_times_lrow(F, k, k, v);
+      d_times_lrow(F, k, k0, k, v);
       __syncthreads();
       int idx;
-      double m = column_update(F, k, k, v, wk, k, idx, sv, si);
+      double m = column_update(F, k, k0, k, v, wk, k, idx, sv, si);
       if (threadIdx.x == 0) {
         pk[2 * blockIdx.x] = m;
         pk[2 * blockIdx.x + 1] = idx;
@@ -246,10 +363,10 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
     if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
       // ---- updated column r and its off-diagonal maximum ----
       __syncthreads();  // v is reused
-      d_times_lrow(F, r, k, v);
+      d_times_lrow(F, r, k0, k, v);
       __syncthreads();
       int idx2;
-      double m2 = column_update(F, r, k, v, F.wr, r, idx2, sv, si);
+      double m2 = column_update(F, r, k0, k, v, F.wr, r, idx2, sv, si);
       __syncthreads();
       if (threadIdx.x == 0) {
         F.part2[2 * blockIdx.x] = m2;
@@ -265,17 +382,18 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
       else
         kind = 2;
     }
-    if (kind == 0 && k + 1 < n) {
+    // (no look-ahead into the next panel: its columns need the trailing update first)
+    if (kind == 0 && k + 1 < n && (F.nb <= 0 || k + 1 - k0 < F.nb)) {
       // ---- look-ahead: column k of L / W and column k+1, one barrier ----
       const double dk = __ldcg(wk + k);
       __syncthreads();  // v is reused
-      d_times_lrow(F, k + 1, k, v);
+      d_times_lrow(F, k + 1, k0, k, v);
       __syncthreads();
       const double vk = dk != 0.0 ? __ldcg(wk + k + 1) : 0.0;  // W(k+1, k)
       double* const wn = cur ? F.w : F.w2;
       double* const pn = cur ? F.part : F.part3;
       int idx;
-      const double m = lookahead_update(F, k, dk, wk, v, vk, wn, idx, sv, si);
+      const double m = lookahead_update(F, k0, k, dk, wk, v, vk, wn, idx, sv, si);
       if (threadIdx.x == 0) {
         pn[2 * blockIdx.x] = m;
         pn[2 * blockIdx.x + 1] = idx;
@@ -386,6 +504,18 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
     }
     grid.sync();
     k += kind == 2 ? 2 : 1;
+    if (F.nb > 0 && k - k0 >= F.nb && k < n) {
+      // ---- panel end: rank-(k - k0) update of the trailing square ----
+      const long long c0 = clock64();
+      trailing_update(F, k0, k, smem);
+      grid.sync();
+      c_upd += clock64() - c0;
+      k0 = k;
+    }
+  }
+  if (F.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    F.trace[0] = c_upd;
+    F.trace[1] = clock64() - c_start;
   }
 }
 
