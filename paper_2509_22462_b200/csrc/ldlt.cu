@@ -337,14 +337,15 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     int grid_nb = 64;
     if (const char* e = std::getenv("GBOPT_LDLT_GRID_NB")) grid_nb = std::max(0, std::min(std::atoi(e), bk::kMaxGridNb));
     const size_t smem =
-        sizeof(double) * static_cast<size_t>(std::max<int64_t>(n, bk::trailing_smem_doubles(grid_nb)));
+        sizeof(double) * static_cast<size_t>(std::max<int64_t>({n, bk::trailing_smem_doubles(grid_nb), 32 * 33}));
     CK(cudaFuncSetAttribute(bk::bk_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bk::bk_factor_kernel, bk::kThreads, smem));
     if (per_sm < 1) throw DeviceError("ldlt_factor: the Bunch-Kaufman kernel does not fit on an SM");
     // a grid barrier costs ~1.2 us whatever the grid size (tools/gridsync_probe.cu),
     // so use every co-resident CTA up to about one row per warp
-    const int grid = static_cast<int>(
+    int grid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, (n + bk::kWarps - 1) / bk::kWarps)));
+    if (const char* e = std::getenv("GBOPT_LDLT_GRID_CTAS")) grid = std::max(1, std::min(grid, std::atoi(e)));
     f->ldl_ = (n + 1) / 2 * 2;  // 16-byte rows
     const size_t lbytes = sizeof(double) * static_cast<size_t>(n) * f->ldl_;
     f->palloc(&f->d_l_, 2 * lbytes);  // L | W = L D
@@ -570,8 +571,8 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       CK(cudaEventCreate(&t0));
       CK(cudaEventCreate(&t1));
       CK(cudaEventRecord(t0, st));
-      CK(cudaMalloc(&F.trace, sizeof(long long) * 2));
-      CK(cudaMemsetAsync(F.trace, 0, sizeof(long long) * 2, st));
+      CK(cudaMalloc(&F.trace, sizeof(long long) * 16));
+      CK(cudaMemsetAsync(F.trace, 0, sizeof(long long) * 16, st));
     }
     if (!use_cluster && !use_panel)
       CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bk::bk_factor_kernel), dim3(grid), dim3(bk::kThreads),
@@ -581,12 +582,14 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       CK(cudaEventSynchronize(t1));
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, t0, t1));
-      long long tr[2];
-      CK(cudaMemcpy(tr, F.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+      long long tr[16] = {};
+      if (!use_cluster && !use_panel) CK(cudaMemcpy(tr, F.trace, sizeof(tr), cudaMemcpyDeviceToHost));
       CK(cudaFree(F.trace));
       std::fprintf(stderr, "ldlt: n %lld grid %d per_sm %d nb %d bk_factor_kernel %.3f ms; CTA-0 clocks: trailing "
-                   "updates %lld of %lld\n",
-                   static_cast<long long>(n), grid, per_sm, grid_nb, ms, tr[0], tr[1]);
+                   "updates %lld of %lld; phases (clocks / count): column k %lld/%lld, decide %lld/%lld, column r "
+                   "%lld/%lld, look-ahead %lld/%lld, interchange+L %lld/%lld\n",
+                   static_cast<long long>(n), grid, per_sm, grid_nb, ms, tr[0], tr[1], tr[2], tr[7], tr[3], tr[8],
+                   tr[4], tr[9], tr[5], tr[10], tr[6], tr[11]);
       cudaEventDestroy(t0);
       cudaEventDestroy(t1);
     }

@@ -60,7 +60,8 @@ struct Factor {
   int ldl;
   int nb;  // > 0: blocked -- column updates span only the current panel's
            // columns, and the trailing A takes a rank-nb update per panel
-  long long* trace;  // null, or [2]: CTA 0's clocks in trailing updates (incl. their barrier), whole kernel
+  long long* trace;  // null, or [16]: CTA 0's clocks -- trailing updates (incl. their barrier), whole kernel,
+                     // phases (column k, decision, column r, look-ahead, interchange + new column), phase counts
 };
 
 // (value, index) maximum with ties to the smaller index
@@ -156,7 +157,7 @@ __device__ double column_update(const Factor& F, int col, int k0, int k, const d
     double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const double wi = __ldcg(F.a + static_cast<int64_t>(i) * F.n + col) - s;
+    const double wi = __ldcg(F.a + static_cast<int64_t>(col) * F.n + i) - s;  // A symmetric: row col, coalesced
     if (lane == 0) out[i] = wi;
     if (i != skip) max_pair(m, idx, fabs(wi), i);
   }
@@ -207,7 +208,7 @@ __device__ double lookahead_update(const Factor& F, int k0, int k, double dk, co
     const double x = __ldcg(w + i);
     const double lik = dk != 0.0 ? x / dk : 0.0;
     s = fma(lik, vk, s);  // the new column k (fixed order: after the reduction)
-    const double wi = __ldcg(F.a + static_cast<int64_t>(i) * F.n + k + 1) - s;
+    const double wi = __ldcg(F.a + static_cast<int64_t>(k + 1) * F.n + i) - s;
     if (lane == 0) {
       F.l[static_cast<int64_t>(i) * F.ldl + k] = lik;
       F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
@@ -261,8 +262,13 @@ __device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wr0 = (warp >> 2) * 32, wc0 = (warp & 3) * 16;  // the warp's sub-tile
   const int fr = lane >> 2, fk = lane & 3;                    // fragment row / k of this lane
-  for (int t = blockIdx.x; t < tiles * tiles; t += gridDim.x) {
-    const int i0 = k1 + (t / tiles) * kTile, j0 = k1 + (t % tiles) * kTile;
+  for (int t = blockIdx.x; t < tiles * (tiles + 1) / 2; t += gridDim.x) {
+    // lower tiles (ti >= tj) only; the update is mirrored, so A stays exactly symmetric
+    int ti = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while (ti * (ti + 1) / 2 > t) --ti;
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    const int tj = t - ti * (ti + 1) / 2;
+    const int i0 = k1 + ti * kTile, j0 = k1 + tj * kTile;
     __syncthreads();  // the previous tile's reads (or v) are done
     // asynchronous 8-byte copies (zero-filled outside the matrix / panel):
     // every load of the tile in flight at once
@@ -319,9 +325,15 @@ __device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
       double* ar = F.a + static_cast<int64_t>(i) * n;
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
-        const int j = j0 + wc0 + b * 8 + 2 * fk;
-        if (i < n && j < n) ar[j] = old[a][b][0] - acc[a][b][0];
-        if (i < n && j + 1 < n) ar[j + 1] = old[a][b][1] - acc[a][b][1];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = j0 + wc0 + b * 8 + 2 * fk + h;
+          if (i < n && j < n && j <= i) {  // (i, j) in the lower triangle: store it and its mirror
+            const double x = old[a][b][h] - acc[a][b][h];
+            ar[j] = x;
+            F.a[static_cast<int64_t>(j) * n + i] = x;
+          }
+        }
       }
     }
   }
@@ -336,11 +348,45 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
   const int n = F.n;
   const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
 
+  // A := the symmetric matrix of its lower triangle (LAPACK's 'L' view; the
+  // input is symmetric to 1e-12): 32 x 32 tiles below the diagonal are
+  // transposed through shared memory onto their mirror.  From here on every
+  // step keeps A exactly symmetric, so column reads become row reads.
+  {
+    double(*tile)[33] = reinterpret_cast<double(*)[33]>(smem);
+    const int tb = (n + 31) / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t = blockIdx.x; t < tb * (tb + 1) / 2; t += gridDim.x) {
+      int ti = static_cast<int>((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+      while (ti * (ti + 1) / 2 > t) --ti;
+      while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+      const int tj = t - ti * (ti + 1) / 2;
+      __syncthreads();
+      for (int r = warp; r < 32; r += kWarps) {
+        const int i = ti * 32 + r, j = tj * 32 + lane;
+        tile[r][lane] = (i < n && j < n) ? __ldcg(F.a + static_cast<int64_t>(i) * n + j) : 0.0;
+      }
+      __syncthreads();
+      for (int r = warp; r < 32; r += kWarps) {
+        const int j = tj * 32 + r, i = ti * 32 + lane;  // element (i, j) -> (j, i)
+        if (i < n && j < n && i > j) F.a[static_cast<int64_t>(j) * n + i] = tile[lane][r];
+      }
+    }
+    grid.sync();
+  }
+
   int cur = 0;        // which of (w, part) / (w2, part3) holds the current column
   bool pre = false;   // column k already computed (and its maxima published) by a look-ahead
   int k0 = 0;         // first column of the current panel (blocked mode; 0 throughout otherwise)
   const long long c_start = clock64();
-  long long c_upd = 0;
+  long long c_upd = 0, ph[5] = {0, 0, 0, 0, 0}, cnt[5] = {0, 0, 0, 0, 0};
+  long long c_mark = c_start;
+  auto mark = [&](int q) {
+    const long long t = clock64();
+    ph[q] += t - c_mark;
+    ++cnt[q];
+    c_mark = t;
+  };
   for (int k = 0; k < n;) {
     double* const wk = cur ? F.w2 : F.w;
     double* const pk = cur ? F.part3 : F.part;
@@ -355,14 +401,25 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
         pk[2 * blockIdx.x + 1] = idx;
       }
       grid.sync();
+      mark(0);
     }
+    // Speculative loads for the common outcome (a 1x1 pivot at k followed by
+    // the look-ahead): W(k+1, panel) into v and w_k, w_{k+1}, in flight
+    // together with the maxima (cta_max's barriers publish v)
+    const bool may_look = k + 1 < n && (F.nb <= 0 || k + 1 - k0 < F.nb);
+    if (may_look) d_times_lrow(F, k + 1, k0, k, v);
+    const double wkk = __ldcg(wk + k);
+    const double wk1 = may_look ? __ldcg(wk + k + 1) : 0.0;
+    bool v_next = may_look;  // v holds W(k+1, panel)
     int r;
     const double lambda = fmax(grid_max(pk, r, sv, si), 0.0);
-    const double absakk = fabs(__ldcg(wk + k));
+    const double absakk = fabs(wkk);
     int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
+    mark(1);
     if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
       // ---- updated column r and its off-diagonal maximum ----
       __syncthreads();  // v is reused
+      v_next = false;
       d_times_lrow(F, r, k0, k, v);
       __syncthreads();
       int idx2;
@@ -381,15 +438,18 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
         kind = 1;
       else
         kind = 2;
+      mark(2);
     }
     // (no look-ahead into the next panel: its columns need the trailing update first)
-    if (kind == 0 && k + 1 < n && (F.nb <= 0 || k + 1 - k0 < F.nb)) {
+    if (kind == 0 && may_look) {
       // ---- look-ahead: column k of L / W and column k+1, one barrier ----
-      const double dk = __ldcg(wk + k);
-      __syncthreads();  // v is reused
-      d_times_lrow(F, k + 1, k0, k, v);
-      __syncthreads();
-      const double vk = dk != 0.0 ? __ldcg(wk + k + 1) : 0.0;  // W(k+1, k)
+      const double dk = wkk;
+      if (!v_next) {
+        __syncthreads();  // v is reused
+        d_times_lrow(F, k + 1, k0, k, v);
+        __syncthreads();
+      }
+      const double vk = dk != 0.0 ? wk1 : 0.0;  // W(k+1, k)
       double* const wn = cur ? F.w : F.w2;
       double* const pn = cur ? F.part : F.part3;
       int idx;
@@ -406,6 +466,7 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
         F.wd[static_cast<int64_t>(k) * F.ldl + k] = dk;
       }
       grid.sync();
+      mark(3);
       cur ^= 1;
       pre = true;
       k += 1;
@@ -420,28 +481,29 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
         if (j == p || j == r) continue;
         double* ap = F.a + static_cast<int64_t>(p) * n;
         double* ar = F.a + static_cast<int64_t>(r) * n;
-        double t = ap[j];
-        ap[j] = ar[j];
-        ar[j] = t;
-        t = F.a[static_cast<int64_t>(j) * n + p];
-        F.a[static_cast<int64_t>(j) * n + p] = F.a[static_cast<int64_t>(j) * n + r];
-        F.a[static_cast<int64_t>(j) * n + r] = t;
+        // (L2 loads: other CTAs' trailing updates wrote A, L1 may be stale)
+        const double x = __ldcg(ap + j), y = __ldcg(ar + j);
+        ap[j] = y;
+        ar[j] = x;
+        double* aj = F.a + static_cast<int64_t>(j) * n;
+        const double u = __ldcg(aj + p), q = __ldcg(aj + r);
+        aj[p] = q;
+        aj[r] = u;
       }
       for (int j = tid; j < k; j += nt) {
         double* lp = F.l + static_cast<int64_t>(p) * F.ldl;
         double* lr = F.l + static_cast<int64_t>(r) * F.ldl;
-        double t = lp[j];
-        lp[j] = lr[j];
-        lr[j] = t;
         double* wp = F.wd + static_cast<int64_t>(p) * F.ldl;
         double* wq = F.wd + static_cast<int64_t>(r) * F.ldl;
-        t = wp[j];
-        wp[j] = wq[j];
-        wq[j] = t;
+        const double l0 = __ldcg(lp + j), l1 = __ldcg(lr + j), w0 = __ldcg(wp + j), w1 = __ldcg(wq + j);
+        lp[j] = l1;
+        lr[j] = l0;
+        wp[j] = w1;
+        wq[j] = w0;
       }
       if (tid == 0) {
-        const double t = F.a[static_cast<int64_t>(p) * n + p];
-        F.a[static_cast<int64_t>(p) * n + p] = F.a[static_cast<int64_t>(r) * n + r];
+        const double t = __ldcg(F.a + static_cast<int64_t>(p) * n + p);
+        F.a[static_cast<int64_t>(p) * n + p] = __ldcg(F.a + static_cast<int64_t>(r) * n + r);
         F.a[static_cast<int64_t>(r) * n + r] = t;
         const int pt = F.perm[p];
         F.perm[p] = F.perm[r];
@@ -503,6 +565,7 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
       }
     }
     grid.sync();
+    mark(4);
     k += kind == 2 ? 2 : 1;
     if (F.nb > 0 && k - k0 >= F.nb && k < n) {
       // ---- panel end: rank-(k - k0) update of the trailing square ----
@@ -510,12 +573,17 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
       trailing_update(F, k0, k, smem);
       grid.sync();
       c_upd += clock64() - c0;
+      c_mark = clock64();
       k0 = k;
     }
   }
   if (F.trace && blockIdx.x == 0 && threadIdx.x == 0) {
     F.trace[0] = c_upd;
     F.trace[1] = clock64() - c_start;
+    for (int q = 0; q < 5; ++q) {
+      F.trace[2 + q] = ph[q];
+      F.trace[7 + q] = cnt[q];
+    }
   }
 }
 
