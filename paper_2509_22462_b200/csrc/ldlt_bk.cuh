@@ -97,7 +97,13 @@ __device__ double cta_max(double v, int& idx, double* sv, int* si) {
 __device__ double grid_max(const double* part, int& idx, double* sv, int* si) {
   double v = -1.0;
   idx = -1;
-  for (int c = threadIdx.x; c < static_cast<int>(gridDim.x); c += kThreads)
+  // up to 2 partials per thread (grid <= 2 kThreads), both loads in flight before the compares
+  const int c0 = threadIdx.x, c1 = threadIdx.x + kThreads, g = static_cast<int>(gridDim.x);
+  const double v0 = c0 < g ? __ldcg(part + 2 * c0) : -1.0, i0 = c0 < g ? __ldcg(part + 2 * c0 + 1) : -1.0;
+  const double v1 = c1 < g ? __ldcg(part + 2 * c1) : -1.0, i1 = c1 < g ? __ldcg(part + 2 * c1 + 1) : -1.0;
+  if (c0 < g) max_pair(v, idx, v0, static_cast<int>(i0));
+  if (c1 < g) max_pair(v, idx, v1, static_cast<int>(i1));
+  for (int c = threadIdx.x + 2 * kThreads; c < g; c += kThreads)
     max_pair(v, idx, __ldcg(part + 2 * c), static_cast<int>(__ldcg(part + 2 * c + 1)));
   return cta_max(v, idx, sv, si);
 }
@@ -118,6 +124,46 @@ __device__ void d_times_lrow(const Factor& F, int row, int k0, int k, double* v)
   }
 }
 
+// Narrow panels (k - (k0 & ~1) <= 128, the blocked mode): kRowBatch rows per
+// warp pass with every load in flight before the first FMA -- a warp owns
+// several rows at large n, and one row per round trip made the column
+// phases latency-bound.  Lane l covers columns jb + 2l and jb + 2l + 64.
+constexpr int kRowBatch = 4;
+__device__ __forceinline__ void panel_dots(const Factor& F, int k0, int k, const double* v, int ibase, int stride,
+                                           double (&sum)[kRowBatch]) {
+  const int lane = threadIdx.x & 31, jb = k0 & ~1;
+  double2 a[kRowBatch][2];
+#pragma unroll
+  for (int r = 0; r < kRowBatch; ++r) {
+    const int i = ibase + r * stride;
+    const double* li = F.l + static_cast<int64_t>(i < F.n ? i : 0) * F.ldl;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = jb + 2 * lane + 64 * h;
+      if (i < F.n && j + 1 < k)
+        a[r][h] = __ldcg(reinterpret_cast<const double2*>(li + j));
+      else
+        a[r][h] = make_double2(i < F.n && j < k ? __ldcg(li + j) : 0.0, 0.0);
+    }
+  }
+  double2 vv[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = jb + 2 * lane + 64 * h;
+    vv[h] = make_double2(j < k ? v[j] : 0.0, j + 1 < k ? v[j + 1] : 0.0);
+  }
+#pragma unroll
+  for (int r = 0; r < kRowBatch; ++r) {
+    double t = fma(a[r][0].x, vv[0].x, fma(a[r][0].y, vv[0].y, 0.0));
+    t = fma(a[r][1].x, vv[1].x, fma(a[r][1].y, vv[1].y, t));
+    sum[r] = t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < kRowBatch; ++r) sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], o);
+}
+
 // out[i] = A[i][col] - L(i, 0:k) . v for i >= k (one warp per row), and the
 // CTA's maximum of |out[i]| over i >= k, i != skip
 __device__ double column_update(const Factor& F, int col, int k0, int k, const double* v, double* out, int skip,
@@ -126,6 +172,26 @@ __device__ double column_update(const Factor& F, int col, int k0, int k, const d
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   double m = -1.0;
   idx = -1;
+  if (k - (k0 & ~1) <= 128) {
+    for (int ib = k + gw; ib < F.n; ib += kRowBatch * nw) {
+      double av[kRowBatch], sum[kRowBatch];
+#pragma unroll
+      for (int r = 0; r < kRowBatch; ++r) {
+        const int i = ib + r * nw;
+        av[r] = i < F.n ? __ldcg(F.a + static_cast<int64_t>(col) * F.n + i) : 0.0;
+      }
+      panel_dots(F, k0, k, v, ib, nw, sum);
+#pragma unroll
+      for (int r = 0; r < kRowBatch; ++r) {
+        const int i = ib + r * nw;
+        if (i >= F.n) break;
+        const double wi = av[r] - sum[r];
+        if (lane == 0) out[i] = wi;
+        if (i != skip) max_pair(m, idx, fabs(wi), i);
+      }
+    }
+    return cta_max(m, idx, sv, si);
+  }
   for (int i = k + gw; i < F.n; i += nw) {
     const double* li = F.l + static_cast<int64_t>(i) * F.ldl;
     // 16-byte loads, four in flight per lane (the rows are latency-bound
@@ -176,6 +242,34 @@ __device__ double lookahead_update(const Factor& F, int k0, int k, double dk, co
   const int gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
   double m = -1.0;
   idx = -1;
+  if (k - (k0 & ~1) <= 128) {
+    for (int ib = k + 1 + gw; ib < F.n; ib += kRowBatch * nw) {
+      double av[kRowBatch], xv[kRowBatch], sum[kRowBatch];
+#pragma unroll
+      for (int r = 0; r < kRowBatch; ++r) {
+        const int i = ib + r * nw;
+        av[r] = i < F.n ? __ldcg(F.a + static_cast<int64_t>(k + 1) * F.n + i) : 0.0;
+        xv[r] = i < F.n ? __ldcg(w + i) : 0.0;
+      }
+      panel_dots(F, k0, k, v, ib, nw, sum);
+#pragma unroll
+      for (int r = 0; r < kRowBatch; ++r) {
+        const int i = ib + r * nw;
+        if (i >= F.n) break;
+        const double x = xv[r];
+        const double lik = dk != 0.0 ? x / dk : 0.0;
+        const double s = fma(lik, vk, sum[r]);  // the new column k (fixed order: after the reduction)
+        const double wi = av[r] - s;
+        if (lane == 0) {
+          F.l[static_cast<int64_t>(i) * F.ldl + k] = lik;
+          F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
+          wn[i] = wi;
+        }
+        if (i != k + 1) max_pair(m, idx, fabs(wi), i);
+      }
+    }
+    return cta_max(m, idx, sv, si);
+  }
   for (int i = k + 1 + gw; i < F.n; i += nw) {
     const double* li = F.l + static_cast<int64_t>(i) * F.ldl;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -305,33 +399,37 @@ __device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) dmma884_bk(acc[a][b], af[a], bf[b]);
     }
-    // all 16 loads of A first, then the stores (a load -> store chain per
-    // element would serialise on the memory latency)
-    double old[4][2][2];
+    // per half of the fragment rows: all 8 loads of A first, then the stores
+    // (a load -> store chain per element would serialise on the memory latency)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int i = i0 + wr0 + a * 8 + fr;
-      const double* ar = F.a + static_cast<int64_t>(i) * n;
+    for (int half = 0; half < 2; ++half) {
+      double old[2][2][2];
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const int j = j0 + wc0 + b * 8 + 2 * fk;
-        old[a][b][0] = (i < n && j < n) ? __ldcg(ar + j) : 0.0;
-        old[a][b][1] = (i < n && j + 1 < n) ? __ldcg(ar + j + 1) : 0.0;
+      for (int a2 = 0; a2 < 2; ++a2) {
+        const int i = i0 + wr0 + (2 * half + a2) * 8 + fr;
+        const double* ar = F.a + static_cast<int64_t>(i) * n;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int j = j0 + wc0 + b * 8 + 2 * fk;
+          old[a2][b][0] = (i < n && j < n) ? __ldcg(ar + j) : 0.0;
+          old[a2][b][1] = (i < n && j + 1 < n) ? __ldcg(ar + j + 1) : 0.0;
+        }
       }
-    }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int i = i0 + wr0 + a * 8 + fr;
-      double* ar = F.a + static_cast<int64_t>(i) * n;
+      for (int a2 = 0; a2 < 2; ++a2) {
+        const int a = 2 * half + a2;
+        const int i = i0 + wr0 + a * 8 + fr;
+        double* ar = F.a + static_cast<int64_t>(i) * n;
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 2; ++b) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = j0 + wc0 + b * 8 + 2 * fk + h;
-          if (i < n && j < n && j <= i) {  // (i, j) in the lower triangle: store it and its mirror
-            const double x = old[a][b][h] - acc[a][b][h];
-            ar[j] = x;
-            F.a[static_cast<int64_t>(j) * n + i] = x;
+          for (int h = 0; h < 2; ++h) {
+            const int j = j0 + wc0 + b * 8 + 2 * fk + h;
+            if (i < n && j < n && j <= i) {  // (i, j) in the lower triangle: store it and its mirror
+              const double x = old[a2][b][h] - acc[a][b][h];
+              ar[j] = x;
+              F.a[static_cast<int64_t>(j) * n + i] = x;
+            }
           }
         }
       }
@@ -339,7 +437,7 @@ __device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
+__global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
   extern __shared__ double smem[];
   double* v = smem;               // [n]
   __shared__ double sv[kWarps];
@@ -379,12 +477,17 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
   bool pre = false;   // column k already computed (and its maxima published) by a look-ahead
   int k0 = 0;         // first column of the current panel (blocked mode; 0 throughout otherwise)
   const long long c_start = clock64();
-  long long c_upd = 0, ph[5] = {0, 0, 0, 0, 0}, cnt[5] = {0, 0, 0, 0, 0};
+  // phase clocks / counts in shared memory (CTA 0, thread 0): no registers held across the kernel
+  __shared__ long long s_ph[11];  // [0..4] clocks, [5..9] counts, [10] trailing updates
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 11; ++q) s_ph[q] = 0;
   long long c_mark = c_start;
+  const bool tracing = F.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   auto mark = [&](int q) {
+    if (!tracing) return;
     const long long t = clock64();
-    ph[q] += t - c_mark;
-    ++cnt[q];
+    s_ph[q] += t - c_mark;
+    s_ph[5 + q] += 1;
     c_mark = t;
   };
   for (int k = 0; k < n;) {
@@ -572,17 +675,19 @@ __global__ void __launch_bounds__(kThreads) bk_factor_kernel(Factor F) {
       const long long c0 = clock64();
       trailing_update(F, k0, k, smem);
       grid.sync();
-      c_upd += clock64() - c0;
-      c_mark = clock64();
+      if (tracing) {
+        s_ph[10] += clock64() - c0;
+        c_mark = clock64();
+      }
       k0 = k;
     }
   }
   if (F.trace && blockIdx.x == 0 && threadIdx.x == 0) {
-    F.trace[0] = c_upd;
+    F.trace[0] = s_ph[10];
     F.trace[1] = clock64() - c_start;
     for (int q = 0; q < 5; ++q) {
-      F.trace[2 + q] = ph[q];
-      F.trace[7 + q] = cnt[q];
+      F.trace[2 + q] = s_ph[q];
+      F.trace[7 + q] = s_ph[5 + q];
     }
   }
 }
