@@ -341,10 +341,14 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     CK(cudaFuncSetAttribute(bk::bk_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bk::bk_factor_kernel, bk::kThreads, smem));
     if (per_sm < 1) throw DeviceError("ldlt_factor: the Bunch-Kaufman kernel does not fit on an SM");
-    // a grid barrier costs ~1.2 us whatever the grid size (tools/gridsync_probe.cu),
-    // so use every co-resident CTA up to about one row per warp
-    int grid = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, (n + bk::kWarps - 1) / bk::kWarps)));
+    // whole waves only (a partial second wave leaves SMs with twice the work):
+    // one CTA per SM while that is at most 3 rows per warp, else every
+    // co-resident CTA; at most one row per warp.  Barriers and the maxima
+    // reduction grow with the CTA count (n = 2531: 148 CTAs 19.2 ms, 159 20.7;
+    // 2812: 148 21.5, 176 23.3, 296 23.7; 5062: 159 50.3, 296 47.5; 10125:
+    // 148 134, 296 123)
+    const int64_t wave1 = n <= static_cast<int64_t>(sms) * bk::kWarps * 3 ? sms : static_cast<int64_t>(sms) * per_sm;
+    int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(wave1, (n + bk::kWarps - 1) / bk::kWarps)));
     if (const char* e = std::getenv("GBOPT_LDLT_GRID_CTAS")) grid = std::max(1, std::min(grid, std::atoi(e)));
     f->ldl_ = (n + 1) / 2 * 2;  // 16-byte rows
     const size_t lbytes = sizeof(double) * static_cast<size_t>(n) * f->ldl_;
