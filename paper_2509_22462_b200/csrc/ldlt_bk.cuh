@@ -323,7 +323,10 @@ constexpr int kMaxGridNb = 128;  // panel width cap (a panel may end one column 
 
 // staged columns: [k0 & ~1, k1) rounded up to 4 (a panel is at most nb + 1 wide)
 __host__ __device__ constexpr int tile_pitch(int nb) { return (((nb + 2 + 3) / 4 * 4 - 4 + 15) / 16) * 16 + 4; }
-__host__ __device__ constexpr int trailing_smem_doubles(int nb) { return nb > 0 ? 2 * kTile * tile_pitch(nb) : 0; }
+// staged L / W tiles, reused for the 64 x 65 product tile of the epilogue
+__host__ __device__ constexpr int trailing_smem_doubles(int nb) {
+  return nb <= 0 ? 0 : (2 * kTile * tile_pitch(nb) > kTile * (kTile + 1) ? 2 * kTile * tile_pitch(nb) : kTile * (kTile + 1));
+}
 
 // 16-byte global -> shared copy through L2 only (the panel's columns were
 // written by other CTAs: no L1), bypassing registers; the bytes past
@@ -399,40 +402,41 @@ __device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) dmma884_bk(acc[a][b], af[a], bf[b]);
     }
-    // per half of the fragment rows: all 8 loads of A first, then the stores
-    // (a load -> store chain per element would serialise on the memory latency)
+    // epilogue through shared memory: the tile's products land in ct
+    // [64][65], then A's tile rows are read / written as whole 512-byte row
+    // segments, and the mirror (upper) tile is written from ct transposed
+    __syncthreads();  // every warp is done with ls / ws
+    double* const ct = sm;  // [64][kTile + 1]
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      double old[2][2][2];
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int a2 = 0; a2 < 2; ++a2) {
-        const int i = i0 + wr0 + (2 * half + a2) * 8 + fr;
-        const double* ar = F.a + static_cast<int64_t>(i) * n;
+      for (int b = 0; b < 2; ++b)
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int j = j0 + wc0 + b * 8 + 2 * fk;
-          old[a2][b][0] = (i < n && j < n) ? __ldcg(ar + j) : 0.0;
-          old[a2][b][1] = (i < n && j + 1 < n) ? __ldcg(ar + j + 1) : 0.0;
-        }
+        for (int h = 0; h < 2; ++h) ct[(wr0 + a * 8 + fr) * (kTile + 1) + wc0 + b * 8 + 2 * fk + h] = acc[a][b][h];
+    __syncthreads();
+    constexpr int kPer = kTile * kTile / kThreads;  // 16 elements per thread
+    const int cc = threadIdx.x & (kTile - 1), r0 = threadIdx.x / kTile;
+    double old[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = i0 + r0 + 4 * q, j = j0 + cc;
+      old[q] = (i < n && j < n && j <= i) ? __ldcg(F.a + static_cast<int64_t>(i) * n + j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int r = r0 + 4 * q, i = i0 + r, j = j0 + cc;
+      if (i < n && j < n && j <= i) {
+        const double x = old[q] - ct[r * (kTile + 1) + cc];
+        F.a[static_cast<int64_t>(i) * n + j] = x;
+        ct[r * (kTile + 1) + cc] = x;
       }
+    }
+    __syncthreads();
+    // mirror: A(j, i) = A(i, j) for i > j; row j of the upper tile is column j of ct
 #pragma unroll
-      for (int a2 = 0; a2 < 2; ++a2) {
-        const int a = 2 * half + a2;
-        const int i = i0 + wr0 + a * 8 + fr;
-        double* ar = F.a + static_cast<int64_t>(i) * n;
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = j0 + wc0 + b * 8 + 2 * fk + h;
-            if (i < n && j < n && j <= i) {  // (i, j) in the lower triangle: store it and its mirror
-              const double x = old[a2][b][h] - acc[a][b][h];
-              ar[j] = x;
-              F.a[static_cast<int64_t>(j) * n + i] = x;
-            }
-          }
-        }
-      }
+    for (int q = 0; q < kPer; ++q) {
+      const int rr = r0 + 4 * q, j = j0 + rr, i = i0 + cc;
+      if (i < n && j < n && i > j) F.a[static_cast<int64_t>(j) * n + i] = ct[cc * (kTile + 1) + rr];
     }
   }
 }
