@@ -224,6 +224,32 @@ class TestFactorisationKernels:
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("nb", ["0", "1", "7", "64", "128"])
+def test_grid_kernel_panel_widths(monkeypatch, nb):
+    """The grid kernel's blocked mode (GBOPT_LDLT_GRID_NB; 0 = unblocked
+    left-looking) at n > 2048 (its default range) on a KKT matrix whose
+    zero-ish constraint block forces many interchanges and 2x2 pivots, so
+    panels end on both pivot kinds: same inertia as the oracle and accurate
+    solves for every width."""
+    if not has_gpu():
+        pytest.skip("no GPU")
+    import paper_2509_22462_b200 as gb
+    monkeypatch.setenv("GBOPT_LDLT_KERNEL", "grid")
+    monkeypatch.setenv("GBOPT_LDLT_GRID_NB", nb)
+    rng = np.random.default_rng(2100)
+    n, m = 1700, 450
+    H = rng.uniform(-1, 1, (n, n))
+    H = 0.5 * (H + H.T) + np.diag(10.0 ** rng.uniform(-2, 3, n))
+    Jm = rng.uniform(-1, 1, (m, n))
+    A = np.block([[H, Jm.T], [Jm, -1e-8 * np.eye(m)]])
+    f = gb.ldlt_factor(A)
+    assert f.inertia == lo.inertia(A)
+    b = rng.uniform(-1, 1, A.shape[0])
+    x = f.solve(b)
+    assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("solve", ["cta", "grid"])
 def test_substitution_kernels_agree(monkeypatch, solve):
     """One-CTA and grid-wide substitutions (GBOPT_LDLT_SOLVE) on the same
