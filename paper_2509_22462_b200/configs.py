@@ -71,13 +71,18 @@ def _draw(rng: g.Prng, dist, n):
     return rng.uniform(a, b, n) if kind == "uniform" else rng.normal(a, b, n)
 
 
-def make(name: str, batch: int | None = None, widths_override=None) -> Workload:
+def make(name: str, batch: int | None = None, widths_override=None, net: g.NeuralNet | None = None) -> Workload:
     """Build config `name`.  `batch` truncates the point set (the first B
-    points of the full seeded stream, so subsamples are prefixes)."""
+    points of the full seeded stream, so subsamples are prefixes).  `net`
+    reuses an already built network of the same seed for configs whose
+    points come from their own seed (c3 shares c2's weights)."""
     c = CONFIGS[name]
     widths = widths_override or c["widths"]
     rng = g.Prng(c["seed"])
-    net = g.random_net_ex(rng, widths, c["hidden"], c["final"], c["init"], *c["bias"])
+    if net is not None and "input_seed" not in c:
+        raise ValueError(f"make: config {name} draws its points after the weights; cannot reuse a net")
+    if net is None:
+        net = g.random_net_ex(rng, widths, c["hidden"], c["final"], c["init"], *c["bias"])
     if "input_seed" in c:
         rng = g.Prng(c["input_seed"])
     B = c["batch"]

@@ -85,3 +85,77 @@ def evaluate_sharded(X, Lam, m: int, evaluate: Callable, dist, rank: int, world:
         return None
     counts = [shard(P, world, r)[1] for r in range(world)]
     return unpack(gather, counts, rows, m, n, xp=torch)
+
+
+class ShardedOracle:
+    """The multi-GPU public API: one process per GPU, replicated weights,
+    contiguous point shards, one result gather to ``dst``.
+
+    Every rank constructs it with the same ``P`` (points per call) and calls
+    it with its own shard of x/lambda (host arrays, ``shard(P, world, rank)``
+    rows); rank ``dst`` receives (Y, J, H) of all P points in host buffers,
+    the other ranks get None.  Per call: host->device copy of the shard,
+    ``gbopt_net_oracle_batched_device`` on the rank's stream, pack, one
+    ``torch.distributed.gather`` (NCCL over NVLink with CUDA tensors; with
+    the gloo backend the flat buffer goes through host memory), and on
+    ``dst`` one device->host copy of the gathered results.  No reduction.
+    """
+
+    def __init__(self, net, P: int, dist, rank: int, world: int, device, dst: int = 0, pinned: bool = True):
+        import torch
+
+        self.net, self.P, self.dist, self.rank, self.world, self.dst = net, P, dist, rank, world, dst
+        self.dev = device
+        self.n, self.m = net.input_dim, net.output_dim
+        n, m = self.n, self.m
+        self.start, self.count = shard(P, world, rank)
+        self.rows = max_shard(P, world)
+        self.per = m + m * n + n * n
+        B = max(self.count, 1)
+        self.Xd = torch.zeros(B, n, dtype=torch.float64, device=device)
+        self.Ld = torch.zeros(B, m, dtype=torch.float64, device=device)
+        self.Yd = torch.empty(B, m, dtype=torch.float64, device=device)
+        self.Jd = torch.empty(B, m, n, dtype=torch.float64, device=device)
+        self.Hd = torch.empty(B, n, n, dtype=torch.float64, device=device)
+        self.backend = dist.get_backend() if world > 1 else "none"
+        cdev = device if self.backend != "gloo" else torch.device("cpu")
+        self.flat = torch.zeros(self.rows * self.per, dtype=torch.float64, device=device)
+        self.flat_c = self.flat if cdev == device else torch.zeros_like(self.flat, device=cdev)
+        self.gather = ([torch.empty_like(self.flat_c) for _ in range(world)]
+                       if (rank == dst and world > 1) else None)
+        if rank == dst:
+            mk = (lambda *s: torch.empty(*s, dtype=torch.float64).pin_memory()) if pinned and \
+                torch.cuda.is_available() else (lambda *s: torch.empty(*s, dtype=torch.float64))
+            self.out_flat = mk(world * self.rows * self.per)
+        self.stream = torch.cuda.current_stream(device)
+
+    def h2d_bytes(self) -> int:
+        return self.count * (self.n + self.m) * 8
+
+    def d2h_bytes(self) -> int:
+        return self.P * self.per * 8 if self.rank == self.dst else 0
+
+    def __call__(self, X, Lam):
+        import torch
+
+        c = self.count
+        if c:
+            self.Xd[:c].copy_(torch.as_tensor(X), non_blocking=True)
+            self.Ld[:c].copy_(torch.as_tensor(Lam), non_blocking=True)
+            self.net.oracle_batched_device(c, self.Xd.data_ptr(), self.Ld.data_ptr(), self.Yd.data_ptr(),
+                                           self.Jd.data_ptr(), self.Hd.data_ptr(), self.stream.cuda_stream)
+            pack(self.Yd[:c], self.Jd[:c], self.Hd[:c], self.rows, self.m, self.n, self.flat)
+        if self.world > 1:
+            if self.flat_c is not self.flat:
+                self.flat_c.copy_(self.flat)
+            self.dist.gather(self.flat_c, gather_list=self.gather, dst=self.dst)
+        if self.rank != self.dst:
+            return None
+        parts = self.gather if self.world > 1 else [self.flat]
+        L = self.rows * self.per
+        for r, buf in enumerate(parts):
+            self.out_flat[r * L:(r + 1) * L].copy_(buf, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        counts = [shard(self.P, self.world, r)[1] for r in range(self.world)]
+        flats = [self.out_flat[r * L:(r + 1) * L].numpy() for r in range(self.world)]
+        return unpack(flats, counts, self.rows, self.m, self.n)
