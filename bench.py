@@ -6,21 +6,35 @@ Metric (BASELINE.json): NN oracle evals/s, one eval = (y, J, H) at one
 roofline fraction of the dominant kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
-  python bench.py --impl reference ...   # CPU reference arm (oracle port)
+  python bench.py --impl reference ...   # CPU arm: the reference's own nn.cpp
+
+--gpus N > 1 runs one process per GPU: under torchrun it uses the launcher's
+ranks; started directly it launches torchrun itself (127.0.0.1) and exits
+with the ranks' status.
 
 A "step" is one oracle evaluation of one c2 point per GPU (weak scaling:
-each rank evaluates its own points, the shared weights are replicated); for
+each rank evaluates its own point, the shared weights are replicated); for
 N > 1 the step ends with an NCCL gather of every rank's (y, J, H) to rank 0
 (the only collective of the path).  `value` is timed with CUDA
 events on the launching stream, inputs resident in HBM, max over ranks.
-`e2e` is the same metric through the public host-buffer API
-(gbopt_net_oracle_batched): pinned host x/lambda in, y/J/H back out.
+`e2e` is the same metric through the public host-buffer API: at N = 1
+gbopt_net_oracle_batched (pinned host x/lambda in, y/J/H out); at N > 1
+parallel.ShardedOracle (host shard in on every rank, H2D, device oracle,
+NCCL gather, rank 0's D2H of all results).  `sharded` adds the batched (c3,
+B = 64) and contingency (c4, K = 4096) workloads split over the N GPUs.
+
+The CPU legs (`cpu_baseline`, `cpu_baseline_1t`, `--impl reference`) run the
+reference's OWN oracle: proj/src/nn.cpp compiled unmodified into
+oracle/_ref/libgbopt_ref.so (oracle/ref.py); they never load the product
+library.  nn.cpp has no softplus, so on c2/c3 the reference times the same
+shape with tanh hidden layers (identical GEMM chain; stated in `sample`).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -39,20 +53,11 @@ THROTTLE_BITS = {
     0x100: "display_clock_setting",
 }
 
-
-def parse():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--batch", type=int, default=None, help="points per GPU per step (default: config's own)")
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
-
-
+# BASELINE.json configs (pure data; the generators live in
+# paper_2509_22462_b200/configs.py and, independently, oracle/ref.py).
+WIDTHS = {"c1": [784, 512, 512, 10], "c2": [784] + [5120] * 5 + [10], "c3": [784] + [5120] * 5 + [10],
+          "c4": [108, 1024, 1024, 1024, 1], "c5": [784] + [1024] * 20 + [10]}
+SOFTPLUS_CONFIGS = ("c2", "c3")
 CONFIG_DESC = {
     "c1": "c1: single-point FP64 oracle, MLP 784-512-512-10 tanh/identity (Xavier-uniform, seed 0)",
     "c2": "c2: single-point FP64 oracle, MLP 784-[5120]x5-10 softplus/identity, 108,948,490 params "
@@ -61,7 +66,92 @@ CONFIG_DESC = {
     "c4": "c4: K=4096 contingency copies of MLP 108-[1024]x3-1 tanh/sigmoid (Xavier-uniform, seed 3)",
     "c5": "c5: deep-chain FP64 oracle, MLP 784-[1024]x20-10 sigmoid/identity, B=16 (N(0,1/fan_in), seed 4)",
 }
-DEFAULT_BATCH = {"c1": 1, "c2": 1, "c3": 64, "c4": 4096, "c5": 16}
+L2_NOTE = {
+    "c1": "no flush: the 5.4 MB of weights stay L2-resident between steps, as between IPM iterations; "
+          "the 4.9 MB Hessian is rewritten every step",
+    "c2": "no flush needed: the weights streamed every step (871.6 MB) exceed the 126 MB L2",
+    "c3": "no flush needed: the weights streamed every step (871.6 MB) exceed the 126 MB L2",
+    "c4": "no flush needed: every step writes 4096 Hessians of 108^2 (382 MB), beyond the 126 MB L2",
+    "c5": "no flush needed: the weights streamed every step (166.1 MB) exceed the 126 MB L2",
+}
+TOTAL_POINTS = {"c1": 1, "c2": 1, "c3": 64, "c4": 4096, "c5": 16}
+SHARDED = ("c3", "c4", "c5")  # fixed point sets split over the ranks
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: correctness run of the N>1 path (e.g. 2 ranks on one GPU); not a perf number")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    return ap.parse_args()
+
+
+def params_of(widths):
+    return sum(widths[l] * widths[l - 1] + widths[l] for l in range(1, len(widths)))
+
+
+def points_per_gpu(name, world, rank=0):
+    if name in SHARDED:
+        P = TOTAL_POINTS[name]
+        base, extra = divmod(P, world)
+        return base + (1 if rank < extra else 0)
+    return TOTAL_POINTS[name]
+
+
+def config_dict(name, world):
+    """The `config` object of both arms (identical by construction)."""
+    P = TOTAL_POINTS[name]
+    return {
+        "workload": CONFIG_DESC[name],
+        "points_per_step": P * world if name not in SHARDED else P,
+        "points_per_step_per_gpu": points_per_gpu(name, world),
+        "params": params_of(WIDTHS[name]),
+        "l2": L2_NOTE[name],
+        "parallelism": (f"replicated weights, points sharded over {world} GPUs, NCCL gather to rank 0"
+                        if world > 1 else "1 GPU"),
+    }
+
+
+def flops_per_eval(name):
+    w = WIDTHS[name]
+    n = w[0]
+    hidden_nonlinear = True
+    f = 0.0
+    L = len(w) - 1
+    for l in range(1, L + 1):
+        mac = w[l] * w[l - 1]
+        f += 2 * mac
+        if l >= 2:
+            f += 2 * mac + 2 * mac * n
+        nonlinear = hidden_nonlinear if l < L else (name == "c4")  # c4's output is sigmoid, others linear
+        if nonlinear:
+            f += w[l] * n * (n + 1)
+    return f
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_launch_ranks(args):
+    """--gpus N > 1 outside a launcher: start N ranks with torchrun."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -118,77 +208,81 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (the oracle port; reference nn.cpp:113-292 restated)
+# CPU arm: the reference's own nn.cpp (oracle/_ref), never the product
 # ---------------------------------------------------------------------------
-def oracle_net_from(net):
-    from oracle import gbopt_oracle as orc
-    layers = []
-    for l in range(net.layer_count):
-        w, b, a = net.layer(l)
-        layers.append(orc.Layer(w, b, a))
-    return orc.NeuralNet(layers)
+def reference_sample(name, threads: int, budget_s: float, min_evals: int = 1, max_steps: int = 10 ** 6,
+                     warmup: int = 1, per_step=None):
+    """Times forward + jacobian + lagrangian_hessian per point (the three
+    reduced-space callbacks, formulations.cpp:317-340) with the reference
+    build on `threads` host threads.  Returns (evals/s, evals, seconds,
+    steps, description, per-step seconds).  A step is `per_step` points
+    (point-parallel over the threads when it is >= the thread count, else
+    one point at a time with the BLAS on all threads)."""
+    from oracle import ref
 
+    hidden = ref.TANH if name in SOFTPLUS_CONFIGS else None
+    P = TOTAL_POINTS[name]
+    if per_step is None:
+        per_step = min(P, 4 * threads) if name == "c4" else 1
+    pool = min(P, max(per_step, 4))
+    wl = ref.make_config(name, batch=pool, hidden=hidden)
+    rn = wl.net()
+    point_parallel = per_step >= threads and threads > 1
+    ref.set_threads(1 if point_parallel else threads)
+    tthreads = threads if point_parallel else 1
 
-def time_cpu_reference(wl, n_points: int, budget_s: float = 12.0, min_evals: int = 2):
-    """Evals/s of the CPU oracle (reference algorithm: forward, reverse-mode
-    Jacobian, forward-over-reverse Hessian) on all host threads, over a
-    bounded sample: at least `min_evals` evaluations and about `budget_s`
-    seconds of CPU work, cycling over the first `n_points` points."""
-    ref = oracle_net_from(wl.net)
-    t_total, evals = 0.0, 0
+    def step(k):
+        idx = [(k * per_step + i) % pool for i in range(per_step)]
+        rn.oracle_batched(wl.X[idx], wl.Lam[idx], threads=tthreads)
+
+    for i in range(warmup):
+        step(i)
+    times = []
     t_start = time.perf_counter()
-    i = 0
-    while evals < min_evals or (time.perf_counter() - t_start < budget_s and evals < 2000):
-        x, lam = wl.X[i % wl.X.shape[0]], wl.Lam[i % wl.X.shape[0]]
+    k = 0
+    while k < max_steps and (len(times) * per_step < min_evals or time.perf_counter() - t_start < budget_s):
         t0 = time.perf_counter()
-        ref.forward(x)
-        ref.jacobian(x)
-        ref.lagrangian_hessian(x, lam)
-        t_total += time.perf_counter() - t0
-        evals += 1
-        i += 1
-        if time.perf_counter() - t_start > budget_s:
+        step(k)
+        times.append(time.perf_counter() - t0)
+        k += 1
+        if len(times) * per_step >= min_evals and time.perf_counter() - t_start >= budget_s:
             break
-    return evals / t_total, evals, t_total
+    evals = len(times) * per_step
+    tot = sum(times)
+    how = (f"point-parallel on {threads} threads" if point_parallel else
+           f"OpenBLAS on {threads} thread{'s' if threads > 1 else ''}")
+    desc = (f"{evals} evals of {name} in {tot:.2f}s, {per_step} point(s) per step; reference nn.cpp "
+            f"(proj/src/nn.cpp:113-292 compiled unmodified, oracle/_ref) forward+jacobian+lagrangian_hessian, "
+            f"{how}")
+    if hidden is not None:
+        desc += "; tanh hidden layers in place of softplus (nn.cpp has none), same GEMM chain"
+    return evals / tot, evals, tot, len(times), desc, times
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    from paper_2509_22462_b200 import configs
+    from oracle import ref
+
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle/ref_build)"}))
+        return 0
     name = args.config
-    B = args.batch or DEFAULT_BATCH[name]
-    wl = configs.make(name, batch=min(B, 4))
-    cores = os.cpu_count()
-    # warmup W evals (bounded), then K steps each = one eval (bounded sample).
-    ref = oracle_net_from(wl.net)
-    for i in range(min(args.warmup, 1)):
-        ref.lagrangian_hessian(wl.X[0], wl.Lam[0])
-    times = []
-    t_start = time.perf_counter()
-    for k in range(args.steps):
-        x, lam = wl.X[k % wl.X.shape[0]], wl.Lam[k % wl.X.shape[0]]
-        t0 = time.perf_counter()
-        ref.forward(x)
-        ref.jacobian(x)
-        ref.lagrangian_hessian(x, lam)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > 120:
-            break
-    val = len(times) / sum(times)
+    cores = os.cpu_count() or 1
+    v, evals, tot, steps, desc, times = reference_sample(name, cores, budget_s=150.0, min_evals=1,
+                                                         max_steps=args.steps, warmup=min(args.warmup, 1))
     line = {
-        "metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * tot / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_DESC[name], "points_per_step": 1},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{len(times)} single-point evals of {name} (reference algorithm "
-                                   f"nn.cpp:113-292, numpy/OpenBLAS on {cores} threads)"},
-        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": config_dict(name, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    if len(times) < args.steps:
-        line["note"] = f"stopped after {len(times)} of {args.steps} steps (120 s CPU budget)"
+    if steps < args.steps:
+        line["note"] = f"stopped after {steps} of {args.steps} steps (150 s CPU budget)"
     print(json.dumps(line), flush=True)
     return 0
 
@@ -233,6 +327,111 @@ def load_traffic():
         return None, None
 
 
+def max_over_ranks(torch, dist, world, dev, t):
+    if world <= 1:
+        return t
+    tt = torch.tensor([t], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def oracle_parity(name, wl, X, Lam, Y, J, H, k):
+    """(y, J, H) max rel err over the first k benchmarked points against the
+    reference nn.cpp build (oracle/_ref), or, for softplus nets (which nn.cpp
+    lacks), against the numpy restatement of nn.cpp (oracle/gbopt_oracle.py)."""
+    from oracle import gbopt_oracle as orc
+    from oracle import ref
+
+    layers = [wl.net.layer(l) for l in range(wl.net.layer_count)]
+    if name in SOFTPLUS_CONFIGS or not ref.available():
+        on = orc.NeuralNet([orc.Layer(w, b, a) for w, b, a in layers])
+        RY = [on.forward(X[i]) for i in range(k)]
+        RJ = [on.jacobian(X[i]) for i in range(k)]
+        RH = [on.lagrangian_hessian(X[i], Lam[i]) for i in range(k)]
+        against = "oracle port (numpy restatement of nn.cpp:113-292; nn.cpp has no softplus)"
+    else:
+        ref.set_threads(os.cpu_count() or 1)
+        rn = ref.RefNet.from_layers(layers)
+        RY, RJ, RH = rn.oracle_batched(X[:k], Lam[:k])
+        against = "reference nn.cpp compiled unmodified (oracle/_ref)"
+    e = [max(orc.rel_err(Y[i], RY[i]) for i in range(k)), max(orc.rel_err(J[i], RJ[i]) for i in range(k)),
+         max(orc.rel_err(H[i], RH[i]) for i in range(k))]
+    return {"y": e[0], "J": e[1], "H": e[2], "points": k, "against": against, "bar": 1e-10,
+            "pass": max(e) <= 1e-10}
+
+
+def run_sharded(torch, dist, gb, configs, parallel, name, world, rank, dev, peak, steps, warmup, net=None):
+    """One fixed point set of config `name` split over the ranks; every step
+    evaluates the rank's shard (device-resident inputs) and gathers the
+    results to rank 0.  Returns the record on rank 0."""
+    wl = configs.make(name, net=net) if net is not None else configs.make(name)
+    rnet = wl.net
+    if net is None:
+        rnet.bind_device(dev.index)
+    P = wl.X.shape[0]
+    start, count = parallel.shard(P, world, rank)
+    rows = parallel.max_shard(P, world)
+    n, m = rnet.input_dim, rnet.output_dim
+    per = m + m * n + n * n
+    Xd = torch.from_numpy(wl.X[start:start + count].copy()).to(dev)
+    Ld = torch.from_numpy(wl.Lam[start:start + count].copy()).to(dev)
+    Yd = torch.empty(count, m, dtype=torch.float64, device=dev)
+    Jd = torch.empty(count, m, n, dtype=torch.float64, device=dev)
+    Hd = torch.empty(count, n, n, dtype=torch.float64, device=dev)
+    flat = torch.zeros(rows * per, dtype=torch.float64, device=dev) if world > 1 else None
+    gloo = world > 1 and dist.get_backend() == "gloo"
+    flat_c = flat.cpu() if gloo else flat
+    gat = [torch.empty_like(flat_c) for _ in range(world)] if (world > 1 and rank == 0) else None
+    stream = torch.cuda.current_stream(dev)
+
+    def compute():
+        rnet.oracle_batched_device(count, Xd.data_ptr(), Ld.data_ptr(), Yd.data_ptr(), Jd.data_ptr(),
+                                   Hd.data_ptr(), stream.cuda_stream)
+
+    def collect():
+        if world > 1:
+            parallel.pack(Yd, Jd, Hd, rows, m, n, flat)
+            if gloo:
+                flat_c.copy_(flat)
+            dist.gather(flat_c, gather_list=gat, dst=0)
+
+    for _ in range(warmup):
+        compute()
+        collect()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        compute()
+        collect()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = max_over_ranks(torch, dist, world, dev, e0.elapsed_time(e1) / 1e3)
+    # the gather alone (same buffers), to show its share
+    tg = 0.0
+    if world > 1:
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(steps):
+            collect()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        tg = max_over_ranks(torch, dist, world, dev, g0.elapsed_time(g1) / 1e3)
+    if rank != 0:
+        return None
+    F = flops_per_eval(name)
+    v = P * steps / t
+    return {"config": name, "workload": CONFIG_DESC[name], "points_total": P, "points_per_gpu_max": rows,
+            "n_gpus": world, "steps": steps, "evals_s": v, "ms_per_step": 1e3 * t / steps,
+            "gather_ms_per_step": 1e3 * tg / steps, "gather_bytes_per_step": world * rows * per * 8 if world > 1 else 0,
+            "achieved_tflops_per_gpu": F * v / world / 1e12,
+            "frac_of_peak": (F * v / world / 1e12) / peak if peak else None,
+            "schedule": rnet.last_schedule}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -240,38 +439,50 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and rank == 0:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    ndev = torch.cuda.device_count()
+    gloo = args.dist_backend == "gloo"
+    if local >= ndev and not gloo:
+        print(f"bench.py: rank {rank} needs GPU {local} but only {ndev} visible", file=sys.stderr)
+        return 2
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_2509_22462_b200 as gb
     from paper_2509_22462_b200 import configs, parallel
 
     name = args.config
-    B = args.batch or DEFAULT_BATCH[name]
-    if name == "c3" and world > 1:
-        B = max(1, DEFAULT_BATCH["c3"] // world)  # 64 points sharded
-    if name == "c4" and world > 1:
-        B = max(1, DEFAULT_BATCH["c4"] // world)
+    P = TOTAL_POINTS[name]
     wl = configs.make(name)
     net = wl.net
-    net.bind_device(local)
+    net.bind_device(dev_index)
     n, m = net.input_dim, net.output_dim
-    # this rank's points: a contiguous shard of the config's seeded stream
-    # (c2: every rank evaluates point `rank` of the stream, wrapping).
-    P = wl.X.shape[0]
-    idx = [(rank * B + i) % P for i in range(B)]
+    # this rank's points: weak-scaling configs (c1, c2) evaluate point `rank`
+    # of the seeded stream (wrapping); c3/c4/c5 split their fixed point set.
+    if name in SHARDED:
+        start, B = parallel.shard(P, world, rank)
+        idx = list(range(start, start + B))
+    else:
+        B = P
+        idx = [(rank * B + i) % wl.X.shape[0] for i in range(B)]
+    rows = max(len(idx), 1) if name not in SHARDED else parallel.max_shard(P, world)
     Xd = torch.from_numpy(wl.X[idx]).to(dev)
     Ld = torch.from_numpy(wl.Lam[idx]).to(dev)
     Yd = torch.empty(B, m, dtype=torch.float64, device=dev)
     Jd = torch.empty(B, m, n, dtype=torch.float64, device=dev)
     Hd = torch.empty(B, n, n, dtype=torch.float64, device=dev)
-    flat = torch.empty(B * (m + m * n + n * n), dtype=torch.float64, device=dev) if world > 1 else None
-    gather = [torch.empty_like(flat) for _ in range(world)] if (world > 1 and rank == 0) else None
-
+    per = m + m * n + n * n
+    flat = torch.zeros(rows * per, dtype=torch.float64, device=dev) if world > 1 else None
+    flat_c = (flat.cpu() if gloo else flat) if world > 1 else None
+    gather = [torch.empty_like(flat_c) for _ in range(world)] if (world > 1 and rank == 0) else None
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -279,9 +490,10 @@ def run_b200(args):
                                   stream.cuda_stream)
         if world > 1:
             # result gather to rank 0: the path's only collective
-            # (paper_2509_22462_b200/parallel.py; CPU-tested over gloo)
-            parallel.pack(Yd, Jd, Hd, B, m, n, flat)
-            dist.gather(flat, gather_list=gather, dst=0)
+            parallel.pack(Yd, Jd, Hd, rows, m, n, flat)
+            if gloo:
+                flat_c.copy_(flat)
+            dist.gather(flat_c, gather_list=gather, dst=0)
 
     peak = measure_fp64_peak(torch, dev) if rank == 0 else None
 
@@ -289,9 +501,9 @@ def run_b200(args):
         step()
     torch.cuda.synchronize()
     launches_per_step = net.last_launch_count
-    schedule = net.last_schedule  # auto: measured on the first evaluation (layer-by-layer graph or dataflow launch)
+    schedule = net.last_schedule
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -304,17 +516,44 @@ def run_b200(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    t = e0.elapsed_time(e1) / 1e3
-    if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-    value = world * B * args.steps / t
+    t = max_over_ranks(torch, dist, world, dev, e0.elapsed_time(e1) / 1e3)
+    total_points = (P * world if name not in SHARDED else P)
+    value = total_points * args.steps / t
     clocks = clk.summary()
 
-    # ---- parity spot check of the benchmarked outputs (rank 0) ----
-    # (full parity lives in tests/; here: H symmetric and finite)
+    # ---- the N>1 path end to end: gathered results == per-shard calls ----
     ok = bool(torch.isfinite(Hd).all().item()) and bool(torch.equal(Hd, Hd.transpose(1, 2)))
+    shards = ([parallel.shard(P, world, r) for r in range(world)] if name in SHARDED else
+              [(r * B, B) for r in range(world)])
+    all_idx = [i % wl.X.shape[0] for s0, c in shards for i in range(s0, s0 + c)]
+    multi = None
+    if world > 1 and rank == 0:
+        counts = [c for _, c in shards]
+        GY, GJ, GH = parallel.unpack([g.cpu().numpy() for g in gather], counts, rows, m, n)
+        # the same shards evaluated one after another by a single process on
+        # this GPU through the same device entry and batch size each rank used
+        # (batching may change the kernels, so the comparison is per shard):
+        # bit for bit
+        same = True
+        o = 0
+        for s0, c in shards:
+            if c == 0:
+                continue
+            sel = all_idx[o:o + c]
+            sX = torch.from_numpy(wl.X[sel]).to(dev)
+            sL = torch.from_numpy(wl.Lam[sel]).to(dev)
+            sY = torch.empty(c, m, dtype=torch.float64, device=dev)
+            sJ = torch.empty(c, m, n, dtype=torch.float64, device=dev)
+            sH = torch.empty(c, n, n, dtype=torch.float64, device=dev)
+            net.oracle_batched_device(c, sX.data_ptr(), sL.data_ptr(), sY.data_ptr(), sJ.data_ptr(), sH.data_ptr(),
+                                      stream.cuda_stream)
+            SY, SJ, SH = sY.cpu().numpy(), sJ.cpu().numpy(), sH.cpu().numpy()
+            same = same and np.array_equal(GY[o:o + c], SY) and np.array_equal(GJ[o:o + c], SJ) and \
+                np.array_equal(GH[o:o + c], SH)
+            o += c
+        multi = {"gathered_points": int(GY.shape[0]), "bitwise_equal_to_single_process_shards": bool(same),
+                 "backend": args.dist_backend}
+        ok = ok and same
 
     # ---- roofline of the dominant kernel: per-launch CUDA events ----
     roof = None
@@ -337,73 +576,106 @@ def run_b200(args):
         cnt, ms, fl, _ = agg[dom]
         achieved = (fl / cnt) / (ms / cnt / 1e3) / 1e12
         traffic, tsrc = load_traffic()
-        tr = None
-        per = traffic.get("per_launch_dram_bytes", {}) if traffic else {}
-        tr = per.get(f"{dom}@{args.config}")
+        per_l = traffic.get("per_launch_dram_bytes", {}) if traffic else {}
         roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": tr,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": per_l.get(f"{dom}@{name}"),
                 "algorithmic_flops_per_launch": fl / cnt, "avg_launch_ms": ms / cnt,
                 "peak_source": "cuBLAS DGEMM 8192^3 burst, measured live in this run (FP64; no FP64 entry in "
-                               "MEASURED_PEAKS.json)",
+                               "MEASURED_PEAKS.json); DMMA issue ceiling 37.1 TFLOP/s (tools/fp64_probe.cu)",
                 "traffic_source": tsrc}
 
     # ---- e2e through the public host-buffer API (pinned host memory) ----
     e2e = None
+    Yh = Jh = Hh = None
     if not args.no_e2e:
         Xh = torch.from_numpy(wl.X[idx]).pin_memory().numpy()
         Lh = torch.from_numpy(wl.Lam[idx]).pin_memory().numpy()
-        Yh = torch.empty(B, m, dtype=torch.float64).pin_memory().numpy()
-        Jh = torch.empty(B, m, n, dtype=torch.float64).pin_memory().numpy()
-        Hh = torch.empty(B, n, n, dtype=torch.float64).pin_memory().numpy()
+        if world == 1:
+            Yh = torch.empty(B, m, dtype=torch.float64).pin_memory().numpy()
+            Jh = torch.empty(B, m, n, dtype=torch.float64).pin_memory().numpy()
+            Hh = torch.empty(B, n, n, dtype=torch.float64).pin_memory().numpy()
+            call = lambda: net.oracle_batched(Xh, Lh, out=(Yh, Jh, Hh))  # noqa: E731
+            h2d, d2h, api = B * (n + m) * 8, B * per * 8, "gbopt_net_oracle_batched (host buffers, synchronous)"
+        else:
+            so = parallel.ShardedOracle(net, total_points if name in SHARDED else B * world, dist, rank, world, dev)
+            call = lambda: so(Xh, Lh)  # noqa: E731
+            h2d, d2h = total_points * (n + m) * 8, total_points * per * 8
+            api = ("parallel.ShardedOracle (host shard in on every rank, H2D, device oracle, "
+                   f"{args.dist_backend} gather, rank-0 D2H of all results)")
         for _ in range(2):
-            net.oracle_batched(Xh, Lh, out=(Yh, Jh, Hh))
+            call()
         if world > 1:
             dist.barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            net.oracle_batched(Xh, Lh, out=(Yh, Jh, Hh))
-        te = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
-        e2e = {"value": world * B * args.steps / te, "unit": UNIT,
-               "h2d_bytes_per_step": B * (n + m) * 8, "d2h_bytes_per_step": B * (m + m * n + n * n) * 8,
-               "api": "gbopt_net_oracle_batched (host buffers, synchronous)"}
-        ok = ok and bool(np.array_equal(Hh, Hd.cpu().numpy()))
+            out = call()
+        torch.cuda.synchronize()
+        te = max_over_ranks(torch, dist, world, dev, time.perf_counter() - t0)
+        e2e = {"value": total_points * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "api": api, "timer": "wall clock around the synchronous calls, max over ranks"}
+        if world == 1:
+            ok = ok and bool(np.array_equal(Hh, Hd.cpu().numpy()))
+        elif rank == 0:
+            Yh, Jh, Hh = out
 
-    # ---- CPU baseline: oracle port on rank 0 at N=1 ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        wls = configs.make(name, batch=min(B, 4))
-        v, ne, tt = time_cpu_reference(wls, n_points=min(B, 4), budget_s=12.0)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{ne} single-point evals of {name} in {tt:.1f}s (reference algorithm nn.cpp:113-292, "
-                         f"numpy/OpenBLAS, all host threads)"}
+    # ---- sharded workloads (batched c3 and contingency c4) ----
+    sharded = None
+    if not args.no_sharded and name == "c2":
+        sharded = []
+        sub_steps = max(2, min(args.steps, 5))
+        r3 = run_sharded(torch, dist, gb, configs, parallel, "c3", world, rank, dev, peak, sub_steps, 2, net=net)
+        r4 = run_sharded(torch, dist, gb, configs, parallel, "c4", world, rank, dev, peak, max(3, min(args.steps, 10)), 2)
+        sharded = [r for r in (r3, r4) if r is not None]
+
+    if world > 1:
+        dist.barrier()
+
+    # ---- CPU legs on rank 0, after the GPU phase: reference nn.cpp ----
+    cpu = cpu1 = parity = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import ref
+        if ref.available():
+            cores = os.cpu_count() or 1
+            v, ne, tt, _, desc, _ = reference_sample(name, cores, budget_s=12.0)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc}
+            v1, ne1, tt1, _, desc1, _ = reference_sample(name, 1, budget_s=3.0, per_step=1)
+            cpu1 = {"value": v1, "unit": UNIT, "cores": 1, "kind": "reference",
+                    "sample": desc1 + " (the reference build has no OpenMP, proj/CMakeLists.txt:17-20)"}
+    if rank == 0 and not args.no_parity:
+        if Yh is not None:      # e2e outputs: every point of the job (rank 0)
+            PY, PJ, PH, sel = Yh, Jh, Hh, all_idx
+        else:                   # device outputs of rank 0's own points
+            PY, PJ, PH, sel = Yd.cpu().numpy(), Jd.cpu().numpy(), Hd.cpu().numpy(), idx
+        k = min(2, PY.shape[0])
+        parity = oracle_parity(name, wl, wl.X[sel[:k]], wl.Lam[sel[:k]], PY, PJ, PH, k)
 
     if rank == 0:
-        F = configs.flops(name)
+        F = flops_per_eval(name)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[name], "points_per_step_per_gpu": B,
-                       "params": int(net.param_count),
-                       "l2": "no flush needed: the weights streamed every step (%.1f MB) exceed the 126 MB L2"
-                             % (8e-6 * net.param_count),
-                       "parallelism": f"replicated weights, points sharded over {world} GPU(s), NCCL gather"
-                       if world > 1 else "1 GPU"},
+            "scaling": "weak" if name not in SHARDED else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": config_dict(name, world),
             "roofline": roof,
             "roofline_eval": {"flops_per_eval": F, "achieved_tflops": F * value / world / 1e12,
                               "frac_of_peak": (F * value / world / 1e12) / peak if peak else None},
             "cpu_baseline": cpu,
+            "cpu_baseline_1t": cpu1,
             "e2e": e2e,
+            "parity": parity,
+            "sharded": sharded,
+            "multi_rank": multi,
             "gpu_launches": int(launches_per_step * args.steps),
             "schedule": schedule,
             "clocks": clocks,
-            "outputs_checked": ok,
+            "outputs_checked": bool(ok and (parity is None or parity["pass"])),
             "kernel_breakdown": prof_summary,
         }
+        if gloo:
+            line["note"] = ("gloo backend: a correctness run of the N>1 path (device oracle -> pack -> gather); "
+                            "not a performance number")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -413,6 +685,9 @@ def run_b200(args):
 
 def main():
     args = parse()
+    rc = maybe_launch_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -197,6 +197,17 @@ class NeuralNet {
                                  jac ? jac->data.data() : nullptr, hess_lower->data(), hess_lower->size()));
   }
 
+  // Batched (y, J, H) of `batch` points (X: batch x n, Lambda: batch x m,
+  // row-major; Y, J, H likewise, any may be null) split over `devices`:
+  // one weight replica and one host thread per entry, each device writing
+  // its rows straight into the outputs (gbopt_net_oracle_batched_multi).
+  void oracle_batched_multi(const std::vector<int>& devices, int64_t batch, const double* X, const double* Lambda,
+                            double* Y, double* J, double* H) const {
+    check(gbopt_net_oracle_batched_multi(h_.get(), devices.data(), devices.size(), static_cast<size_t>(batch), X,
+                                         static_cast<size_t>(input_dim()), Lambda,
+                                         static_cast<size_t>(output_dim()), Y, J, H));
+  }
+
   // nn.hpp:31-36, nn.cpp:127-146
   ForwardTrace forward_trace(const RealVec& x) const {
     check_len(x, input_dim(), "forward_trace");

@@ -226,6 +226,37 @@ gbopt_status gbopt_net_oracle_batched_device(const gbopt_net* net,
                                              size_t m, double* dY, double* dJ,
                                              double* dH, void* stream);
 
+/* Multi-device evaluation inside one process (new in this build; SURVEY
+ * §8e "batched points and contingency copies sharded across the GPUs of one
+ * box").  The handle's host weights are replicated to every listed device
+ * (uploaded once per device, kept for later calls); `devices[i]` runs slot
+ * i, a device may be listed more than once (independent workspaces on one
+ * GPU).  The `batch` points are split into contiguous shards, the first
+ * batch % n_devices slots taking one extra point, each slot on its own host
+ * thread.  No reduction between devices.  Replaces a loop of
+ * NeuralNet::lagrangian_hessian calls (reference nn.hpp:58-74) for callers
+ * holding one network (formulations.cpp:276).
+ *
+ * _multi: host buffers as gbopt_net_oracle_batched; every device writes its
+ *   rows of Y / J / H straight into the caller's buffers.  Synchronous.
+ * _multi_gather: X, Lambda, Y, J, H are device buffers on devices[0]; each
+ *   other device pulls its shard of X / Lambda and pushes its rows of the
+ *   results back into devices[0]'s buffers with peer copies over NVLink
+ *   (the result gather; copy engines, no SM time).  Returns when every
+ *   shard has landed (synchronous, no stream argument).
+ * The per-shard results are bit-identical to evaluating each shard alone
+ * with gbopt_net_oracle_batched on one device. */
+gbopt_status gbopt_net_oracle_batched_multi(const gbopt_net* net,
+                                            const int* devices,
+                                            size_t n_devices, size_t batch,
+                                            const double* X, size_t n,
+                                            const double* Lambda, size_t m,
+                                            double* Y, double* J, double* H);
+gbopt_status gbopt_net_oracle_batched_multi_gather(
+    const gbopt_net* net, const int* devices, size_t n_devices, size_t batch,
+    const double* dX, size_t n, const double* dLambda, size_t m, double* dY,
+    double* dJ, double* dH);
+
 /* Oracle schedule of this handle's fused (y, J, H) evaluations:
  *   -1  automatic (default; GBOPT_DATAFLOW=0/1 in the environment at bind
  *       time forces 0/1): the persistent dataflow launch when every tangent

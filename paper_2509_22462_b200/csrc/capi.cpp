@@ -17,6 +17,7 @@
 
 #include "device_net.hpp"
 #include "kkt.hpp"
+#include "multi.hpp"
 #include "ldlt.hpp"
 #include "net.hpp"
 
@@ -364,6 +365,42 @@ gbopt_status gbopt_net_oracle_batched(const gbopt_net* net, size_t batch, const 
   if (batch > (1u << 30)) return fail_argument("gbopt_net_oracle: batch too large");
   return guarded([&] {
     net->net->device().evaluate_host(static_cast<int>(batch), X, Lambda, Y, J, H, nullptr);
+  });
+}
+
+static gbopt_status multi_args(const gbopt_net* net, const int* devices, size_t n_devices, size_t batch,
+                               const double* X, size_t n, const double* Lambda, size_t m, const double* H,
+                               const char* who) {
+  if (net == nullptr || X == nullptr || devices == nullptr)
+    return fail_argument((std::string(who) + ": net, devices and X must be non-null").c_str());
+  if (n_devices == 0 || n_devices > 1024) return fail_argument((std::string(who) + ": n_devices out of range").c_str());
+  if (H != nullptr && Lambda == nullptr) return fail_argument((std::string(who) + ": lambda is required for the Hessian").c_str());
+  if (!dims_ok(net, n, m)) return fail_argument((std::string(who) + ": lengths do not match the network dimensions").c_str());
+  if (batch == 0 || batch > (1u << 30)) return fail_argument((std::string(who) + ": batch out of range").c_str());
+  return GBOPT_OK;
+}
+
+gbopt_status gbopt_net_oracle_batched_multi(const gbopt_net* net, const int* devices, size_t n_devices, size_t batch,
+                                            const double* X, size_t n, const double* Lambda, size_t m, double* Y,
+                                            double* J, double* H) {
+  const gbopt_status a = multi_args(net, devices, n_devices, batch, X, n, Lambda, m, H,
+                                    "gbopt_net_oracle_batched_multi");
+  if (a != GBOPT_OK) return a;
+  return guarded([&] {
+    net->net->multi().evaluate_host(std::vector<int>(devices, devices + n_devices), static_cast<int>(batch), X,
+                                    Lambda, Y, J, H);
+  });
+}
+
+gbopt_status gbopt_net_oracle_batched_multi_gather(const gbopt_net* net, const int* devices, size_t n_devices,
+                                                   size_t batch, const double* dX, size_t n, const double* dLambda,
+                                                   size_t m, double* dY, double* dJ, double* dH) {
+  const gbopt_status a = multi_args(net, devices, n_devices, batch, dX, n, dLambda, m, dH,
+                                    "gbopt_net_oracle_batched_multi_gather");
+  if (a != GBOPT_OK) return a;
+  return guarded([&] {
+    net->net->multi().evaluate_gather(std::vector<int>(devices, devices + n_devices), static_cast<int>(batch), dX,
+                                      dLambda, dY, dJ, dH);
   });
 }
 

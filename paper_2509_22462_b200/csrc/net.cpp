@@ -2,6 +2,7 @@
 // Follows reference src/nn.cpp:21-41 (names), 74-103 (validation) and
 // 336-367 (random_net).
 #include "net.hpp"
+#include "multi.hpp"
 
 #include "device_net.hpp"
 #include "parallel_host.hpp"

@@ -27,6 +27,7 @@ struct HostLayer {
 };
 
 struct DeviceNet;  // oracle.cu
+class MultiPool;   // multi.cpp
 
 class Net {
  public:
@@ -47,6 +48,8 @@ class Net {
   DeviceNet& device(int ordinal = -1);  // binds (uploads) on first use
   DeviceNet* device_if_bound() const { return dev_.get(); }
   int bound_ordinal() const;
+  // Replicas on several devices for multi-device calls (multi.hpp).
+  MultiPool& multi();
   bool use_graphs = true;
   int schedule = -1;  // oracle schedule: -1 auto, 0 layer-by-layer launches, 1 dataflow where the shape allows
 
@@ -54,6 +57,7 @@ class Net {
   std::vector<HostLayer> layers_;
   std::int64_t param_count_ = 0;
   std::unique_ptr<DeviceNet> dev_;
+  std::unique_ptr<MultiPool> multi_;  // declared after dev_: its slots may point at *dev_
 };
 
 // reference random_net (nn.cpp:336-367)

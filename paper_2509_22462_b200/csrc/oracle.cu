@@ -32,6 +32,7 @@
 
 #include "dataflow.cuh"
 #include "device_net.hpp"
+#include "multi.hpp"
 #include "kernels.cuh"
 #include "net.hpp"
 
@@ -1748,6 +1749,11 @@ DeviceNet& Net::device(int ordinal) {
 }
 
 int Net::bound_ordinal() const { return dev_ ? dev_->ordinal() : -1; }
+
+MultiPool& Net::multi() {
+  if (!multi_) multi_ = std::make_unique<MultiPool>(*this);
+  return *multi_;
+}
 
 const char* kernel_tag_name(int tag) {
   static const char* names[kTagCount] = {"fwd_rows",     "softmax",       "adj_seed",     "adj_cols",

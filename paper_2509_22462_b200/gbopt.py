@@ -74,6 +74,10 @@ _net_oracle = _fn("gbopt_net_oracle", _status, _vp, _dp, _sz, _dp, _sz, _dp, _dp
 _net_oracle_batched = _fn("gbopt_net_oracle_batched", _status, _vp, _sz, _dp, _sz, _dp, _sz, _dp, _dp, _dp)
 _net_oracle_batched_device = _fn("gbopt_net_oracle_batched_device", _status, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _vp,
                                  _vp, _vp)
+_net_oracle_multi = _fn("gbopt_net_oracle_batched_multi", _status, _vp, ctypes.POINTER(ctypes.c_int), _sz, _sz, _dp,
+                        _sz, _dp, _sz, _dp, _dp, _dp)
+_net_oracle_multi_gather = _fn("gbopt_net_oracle_batched_multi_gather", _status, _vp, ctypes.POINTER(ctypes.c_int),
+                               _sz, _sz, _vp, _sz, _vp, _sz, _vp, _vp, _vp)
 _net_forward_trace = _fn("gbopt_net_forward_trace", _status, _vp, _dp, _sz, _dp, _dp, _sz)
 _net_oracle_lower = _fn("gbopt_net_oracle_lower", _status, _vp, _sz, _dp, _sz, _dp, _sz, _dp, _dp, _dp, _sz)
 _net_last_launch_count = _fn("gbopt_net_last_launch_count", _i64, _vp)
@@ -406,6 +410,31 @@ class NeuralNet:
             raise ArgumentError("oracle_batched: Lambda must be B x m")
         _check(_net_oracle_batched(self._h, B, _dptr(X), X.shape[1], _dptr(Lam), m, _dptr(Y), _dptr(J), _dptr(H)))
         return Y, J, H
+
+    def oracle_batched_multi(self, devices: Sequence[int], X, Lam, want_y=True, want_j=True, want_h=True):
+        """B points split into contiguous shards over `devices` (one replica of
+        the weights and one host thread per entry; duplicates allowed), each
+        device writing its rows straight into the host outputs
+        (gbopt_net_oracle_batched_multi)."""
+        X = np.ascontiguousarray(np.asarray(X, dtype=np.float64))
+        Lam = None if Lam is None else np.ascontiguousarray(np.asarray(Lam, dtype=np.float64))
+        B, n, m = X.shape[0], self.input_dim, self.output_dim
+        Y = np.empty((B, m)) if want_y else None
+        J = np.empty((B, m, n)) if want_j else None
+        H = np.empty((B, n, n)) if want_h else None
+        devs = (ctypes.c_int * len(devices))(*devices)
+        _check(_net_oracle_multi(self._h, devs, len(devices), B, _dptr(X), X.shape[1], _dptr(Lam), m, _dptr(Y),
+                                 _dptr(J), _dptr(H)))
+        return Y, J, H
+
+    def oracle_batched_multi_gather(self, devices: Sequence[int], batch: int, dX: int, dLam: int, dY: int, dJ: int,
+                                    dH: int):
+        """Device buffers on devices[0] (raw CUDA addresses); the other devices
+        pull their shards and push their results back with peer copies
+        (gbopt_net_oracle_batched_multi_gather).  Synchronous."""
+        devs = (ctypes.c_int * len(devices))(*devices)
+        _check(_net_oracle_multi_gather(self._h, devs, len(devices), batch, dX, self.input_dim, dLam,
+                                        self.output_dim, dY, dJ, dH))
 
     def intermediate(self, name: str, layer: int, batch: int = 1) -> np.ndarray:
         """Per-layer vector of the last evaluation (white-box tests; the last

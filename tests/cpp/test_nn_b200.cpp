@@ -118,6 +118,29 @@ int main(int argc, char** argv) {
   rs.jacobian(xb, jv);
   rs.lag_hessian(xb, lam, hv);
   CHECK(rs.evaluations() == evals);  // cached: no new device work at the same iterate
+  {  // multi-device call (two and three replicas on device 0): each shard is
+     // bit-identical to evaluating that shard alone on one device
+    NeuralNet mn = random_net({9, 33, 17, 3}, "sigmoid", "tanh", 21);
+    const int64_t B = 7, n = 9, m = 3;
+    std::vector<double> X(B * n), Lm(B * m);
+    for (size_t i = 0; i < X.size(); ++i) X[i] = std::sin(0.37 * static_cast<double>(i));
+    for (size_t i = 0; i < Lm.size(); ++i) Lm[i] = std::cos(0.11 * static_cast<double>(i));
+    for (int S : {2, 3}) {
+      std::vector<int> devs(static_cast<size_t>(S), 0);
+      std::vector<double> Y(B * m), J(B * m * n), H(B * n * n);
+      mn.oracle_batched_multi(devs, B, X.data(), Lm.data(), Y.data(), J.data(), H.data());
+      for (int r = 0; r < S; ++r) {
+        const int64_t cnt = B / S + (r < B % S ? 1 : 0);
+        const int64_t st = r * (B / S) + std::min<int64_t>(r, B % S);
+        std::vector<double> y1(cnt * m), j1(cnt * m * n), h1(cnt * n * n);
+        check(gbopt_net_oracle_batched(mn.handle(), cnt, X.data() + st * n, n, Lm.data() + st * m, m, y1.data(),
+                                       j1.data(), h1.data()));
+        CHECK(std::equal(y1.begin(), y1.end(), Y.begin() + st * m));
+        CHECK(std::equal(j1.begin(), j1.end(), J.begin() + st * m * n));
+        CHECK(std::equal(h1.begin(), h1.end(), H.begin() + st * n * n));
+      }
+    }
+  }
   std::printf("%s host+device checks\n", g_fail ? "FAILED" : "passed");
   return g_fail ? 1 : 0;
 }
