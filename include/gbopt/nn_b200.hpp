@@ -269,9 +269,11 @@ inline NeuralNet random_net(const std::vector<int64_t>& widths, const std::strin
 // r = y - NN(x).  Each callback does the least work that answers it and
 // caches per x: residual -> forward pass; Jacobian -> reverse mode (m
 // weight sweeps, like nn.cpp:148-170); Lagrangian Hessian -> the fused
-// y/J/H evaluation, which also refreshes the cached y and J.  The IPM calls
-// residual, Jacobian and Hessian at the same iterate
-// (ipm.cpp:256, 278, 420), so no quantity is computed twice per x.
+// evaluation with the Hessian only.  Every quantity has one producer, so a
+// callback's value at x is the same whatever ran before it (the reference
+// is a pure function of x).  The IPM calls residual, Jacobian and Hessian at
+// the same iterate (ipm.cpp:256, 278, 420), so no quantity is computed
+// twice per x.
 class ReducedSpaceOracle {
  public:
   explicit ReducedSpaceOracle(NeuralNet net) : net_(std::move(net)) {
@@ -314,8 +316,8 @@ class ReducedSpaceOracle {
     if (!same_x(xb, h_x_) || neg != h_lam_) {
       const RealVec x = head(xb);
       // packed on the device in the pattern's value order
-      net_.oracle_lower(x, neg, &y_, &jac_, &hess_lower_);
-      y_x_ = j_x_ = h_x_ = x;
+      net_.oracle_lower(x, neg, nullptr, nullptr, &hess_lower_);
+      h_x_ = x;
       h_lam_ = neg;
       ++evals_;
     }

@@ -258,12 +258,17 @@ gbopt_status gbopt_net_oracle_batched_multi_gather(
     double* dJ, double* dH);
 
 /* Oracle schedule of this handle's fused (y, J, H) evaluations:
- *   -1  automatic (default; GBOPT_DATAFLOW=0/1 in the environment at bind
- *       time forces 0/1): the persistent dataflow launch when every tangent
- *       GEMM layer has at least one tile per SM, else layer by layer;
+ *   -1  automatic (default; GBOPT_DATAFLOW=0/1/-2 in the environment at bind
+ *       time forces 0/1/-2): a fixed rule on the shape -- the persistent
+ *       dataflow launch for chains of >= 8 layers whose tangent GEMM tiles
+ *       leave >= 10% of the layer-by-layer waves idle, else layer by layer
+ *       -- so every process runs the same kernels for the same call and the
+ *       results are reproducible bit for bit;
  *    0  layer-by-layer launches (two streams, CUDA graph);
  *    1  the persistent dataflow launch whenever the shape allows it
- *       (batch <= 112, output width <= 16, no softmax output).
+ *       (batch <= 112, output width <= 16, no softmax output);
+ *   -2  measured: the first call of a shape times both and keeps the faster
+ *       (opt-in; two processes may pick differently).
  * Both schedules compute the same quantities (equal to rounding). */
 gbopt_status gbopt_net_set_schedule(gbopt_net* net, int schedule);
 

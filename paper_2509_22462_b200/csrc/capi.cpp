@@ -255,7 +255,8 @@ gbopt_status gbopt_net_set_graphs(gbopt_net* net, int enabled) {
 
 gbopt_status gbopt_net_set_schedule(gbopt_net* net, int schedule) {
   if (net == nullptr) return fail_argument("gbopt_net_set_schedule: net must be non-null");
-  if (schedule < -1 || schedule > 1) return fail_argument("gbopt_net_set_schedule: schedule must be -1, 0 or 1");
+  if (schedule < -2 || schedule > 1)
+    return fail_argument("gbopt_net_set_schedule: schedule must be -2, -1, 0 or 1");
   return guarded([&] { net->net->schedule = schedule; });
 }
 

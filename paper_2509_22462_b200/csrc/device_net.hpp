@@ -170,6 +170,7 @@ class DeviceNet {
   std::map<ChoiceKey, std::pair<float, float>> df_tuned_ms_;  // (layered, dataflow) ms of the autotune
   int df_force_ = -1;  // autotune override of the schedule mode
   void autotune(cudaStream_t st, int nb, const Outputs& o);
+  bool dataflow_rule(int nb) const;
   void dispatch(cudaStream_t st, int nb, const Outputs& o);
   DfPlan& dataflow_plan(int nb);
   void enqueue_dataflow(cudaStream_t st, int nb, const Outputs& o);

@@ -57,19 +57,22 @@ __device__ inline void atomic_max_pos(double* addr, double v) {
 }
 
 // r = b - A x (one warp per row), also |r|_inf and |x|_inf into out[0..1]
+// (grid-stride over rows: the launch is capped, n is not)
 __global__ void ldlt_residual_kernel(const double* __restrict__ a, int64_t n, const double* __restrict__ x,
                                      const double* __restrict__ b, double* __restrict__ r, double* out) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= n) return;
+  const int64_t wpb = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int64_t k = lane; k < n; k += 32) s = fma(a[row * n + k], x[k], s);
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    const double v = b[row] - s;
-    r[row] = v;
-    atomic_max_pos(out + 0, fabs(v));
-    atomic_max_pos(out + 1, fabs(x[row]));
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * wpb + (threadIdx.x >> 5); row < n;
+       row += static_cast<int64_t>(gridDim.x) * wpb) {
+    double s = 0.0;
+    for (int64_t k = lane; k < n; k += 32) s = fma(a[row * n + k], x[k], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const double v = b[row] - s;
+      r[row] = v;
+      atomic_max_pos(out + 0, fabs(v));
+      atomic_max_pos(out + 1, fabs(x[row]));
+    }
   }
 }
 
@@ -113,6 +116,7 @@ __global__ void ldlt_prep_kernel(double* __restrict__ a, int64_t n, double* __re
   grid.sync();
   if (__ldcg(scal + 2) > 0 || __ldcg(scal + 1) > 1e-12 * fmax(1.0, __ldcg(scal + 0))) return;  // the host throws
   for (int64_t i = tid; i < n; i += nt) scale[i] = 1.0;
+  bool converged = false;
   for (int round = 0; round < 20; ++round) {
     // cmax of row i == column i (symmetric): one warp per row
     for (int64_t row = gw; row < n; row += nw) {
@@ -126,9 +130,24 @@ __global__ void ldlt_prep_kernel(double* __restrict__ a, int64_t n, double* __re
       }
     }
     grid.sync();
-    if (__ldcg(scal + 8 + round) <= 0.01) break;  // the same value in every thread
+    if (__ldcg(scal + 8 + round) <= 0.01) {  // the same value in every thread
+      converged = true;
+      break;
+    }
     for (int64_t e = tid; e < n * n; e += nt) a[e] *= __ldcg(rs + e / n) * __ldcg(rs + e % n);
     for (int64_t i = tid; i < n; i += nt) scale[i] *= __ldcg(rs + i);
+    grid.sync();
+  }
+  if (!converged) {
+    // all 20 rounds rescaled: the maxima measured before the last scaling
+    // are stale; the zero threshold needs max|balanced| of the final matrix
+    // (linalg.cpp:101)
+    for (int64_t row = gw; row < n; row += nw) {
+      double m = 0.0;
+      for (int64_t k = lane; k < n; k += 32) m = fmax(m, fabs(a[row * n + k]));
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) cmax[row] = m;
+    }
     grid.sync();
   }
   for (int64_t i = tid; i < n; i += nt) atomic_max_pos(scal + 3, __ldcg(cmax + i));  // cmax of the final matrix
@@ -381,6 +400,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     F.n = static_cast<int>(n);
     F.ldl = static_cast<int>(f->ldl_);
     F.nb = grid_nb;
+    F.eps = f->zero_thresh_;
     F.trace = nullptr;
     CK(cudaMemsetAsync(F.e, 0, sizeof(double) * n, st));
     // Kernel choice (GBOPT_LDLT_KERNEL = panel | cluster | grid forces one):
@@ -429,6 +449,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       P.ctl = reinterpret_cast<int*>(P.pan_g + 3 * bkp::kMaxNb);
       P.n = static_cast<int>(n);
       P.nb = pnb;
+      P.eps = f->zero_thresh_;
       P.trace = nullptr;
       void* pargs[] = {&P};
       cudaEvent_t c0 = nullptr, c1 = nullptr;
@@ -517,6 +538,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
       P.piv = F.piv;
       P.perm = F.perm;
       P.n = static_cast<int>(n);
+      P.eps = f->zero_thresh_;
       P.trace = nullptr;
       const bool timing = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
       if (timing) {

@@ -58,6 +58,7 @@ struct Factor {
   double* part2;  // [2 * grid] the same for column r (separate: CTAs may still read part)
   int n;
   int ldl;
+  double eps;  // zero-pivot threshold 1e-11 max|SAS| (linalg.cpp:101, 143-157, 226-229)
   int nb;  // > 0: blocked -- column updates span only the current panel's
            // columns, and the trailing A takes a rank-nb update per panel
   long long* trace;  // null, or [16]: CTA 0's clocks -- trailing updates (incl. their barrier), whole kernel,
@@ -257,12 +258,12 @@ __device__ double lookahead_update(const Factor& F, int k0, int k, double dk, co
         const int i = ib + r * nw;
         if (i >= F.n) break;
         const double x = xv[r];
-        const double lik = dk != 0.0 ? x / dk : 0.0;
+        const double lik = fabs(dk) > F.eps ? x / dk : 0.0;
         const double s = fma(lik, vk, sum[r]);  // the new column k (fixed order: after the reduction)
         const double wi = av[r] - s;
         if (lane == 0) {
           F.l[static_cast<int64_t>(i) * F.ldl + k] = lik;
-          F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
+          F.wd[static_cast<int64_t>(i) * F.ldl + k] = fabs(dk) > F.eps ? x : 0.0;
           wn[i] = wi;
         }
         if (i != k + 1) max_pair(m, idx, fabs(wi), i);
@@ -300,12 +301,12 @@ __device__ double lookahead_update(const Factor& F, int k0, int k, double dk, co
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const double x = __ldcg(w + i);
-    const double lik = dk != 0.0 ? x / dk : 0.0;
+    const double lik = fabs(dk) > F.eps ? x / dk : 0.0;
     s = fma(lik, vk, s);  // the new column k (fixed order: after the reduction)
     const double wi = __ldcg(F.a + static_cast<int64_t>(k + 1) * F.n + i) - s;
     if (lane == 0) {
       F.l[static_cast<int64_t>(i) * F.ldl + k] = lik;
-      F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
+      F.wd[static_cast<int64_t>(i) * F.ldl + k] = fabs(dk) > F.eps ? x : 0.0;
       wn[i] = wi;
     }
     if (i != k + 1) max_pair(m, idx, fabs(wi), i);
@@ -523,7 +524,10 @@ __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
     const double absakk = fabs(wkk);
     int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
     mark(1);
-    if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
+    // the reference's negligible column (linalg.cpp:143-157): an exact zero
+    // pivot, no interchange, a zero column of L
+    const bool negl = !(fmax(absakk, lambda) > F.eps);
+    if (r >= 0 && !negl && absakk < kAlpha * lambda) {
       // ---- updated column r and its off-diagonal maximum ----
       __syncthreads();  // v is reused
       v_next = false;
@@ -550,13 +554,13 @@ __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
     // (no look-ahead into the next panel: its columns need the trailing update first)
     if (kind == 0 && may_look) {
       // ---- look-ahead: column k of L / W and column k+1, one barrier ----
-      const double dk = wkk;
+      const double dk = negl ? 0.0 : wkk;
       if (!v_next) {
         __syncthreads();  // v is reused
         d_times_lrow(F, k + 1, k0, k, v);
         __syncthreads();
       }
-      const double vk = dk != 0.0 ? wk1 : 0.0;  // W(k+1, k)
+      const double vk = fabs(dk) > F.eps ? wk1 : 0.0;  // W(k+1, k)
       double* const wn = cur ? F.w : F.w2;
       double* const pn = cur ? F.part : F.part3;
       int idx;
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
     // sigma_swap(i): index of row i before the interchange p <-> r
     auto src = [&](int i) { return (p >= 0 && p != r) ? (i == p ? r : (i == r ? p : i)) : i; };
     if (kind == 0) {
-      const double dk = __ldcg(wk + k);
+      const double dk = negl ? 0.0 : __ldcg(wk + k);
       if (tid == 0) {
         F.d[k] = dk;
         F.e[k] = 0.0;
@@ -630,8 +634,8 @@ __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
       }
       for (int i = k + 1 + tid; i < n; i += nt) {
         const double x = __ldcg(wk + i);
-        F.l[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x / dk : 0.0;
-        F.wd[static_cast<int64_t>(i) * F.ldl + k] = dk != 0.0 ? x : 0.0;
+        F.l[static_cast<int64_t>(i) * F.ldl + k] = fabs(dk) > F.eps ? x / dk : 0.0;
+        F.wd[static_cast<int64_t>(i) * F.ldl + k] = fabs(dk) > F.eps ? x : 0.0;
       }
     } else if (kind == 1) {
       const double dk = __ldcg(F.wr + r);
@@ -643,8 +647,8 @@ __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
       }
       for (int i = k + 1 + tid; i < n; i += nt) {
         const double x = __ldcg(F.wr + src(i));
-        F.l[static_cast<int64_t>(i) * F.ldl + k] = x / dk;
-        F.wd[static_cast<int64_t>(i) * F.ldl + k] = x;
+        F.l[static_cast<int64_t>(i) * F.ldl + k] = fabs(dk) > F.eps ? x / dk : 0.0;
+        F.wd[static_cast<int64_t>(i) * F.ldl + k] = fabs(dk) > F.eps ? x : 0.0;
       }
     } else {
       const double a = __ldcg(wk + k), b = __ldcg(wk + r), c = __ldcg(F.wr + r);

@@ -58,6 +58,7 @@ struct Params {
   int* piv;         // [n]
   int* perm;        // [n]
   int n;
+  double eps;  // zero-pivot threshold 1e-11 max|SAS| (linalg.cpp:101, 143-157, 226-229)
   long long* trace;  // diagnostics (GBOPT_LDLT_TIMING): rank 0's clock at 6 points per step, or null
 };
 
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) bkc_factor_kernel(Params p) {
     const double lambda = fmax(column_pull(cluster, s, masks, n, s.loc[k], s.col, r, rv, ri), 0.0);
     const double absakk = fabs(s.col[cix(s, s.loc[k])]);
     int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
-    if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
+    if (r >= 0 && fmax(absakk, lambda) > p.eps && absakk < kAlpha * lambda) {
       int r2;
       const double sigma = fmax(column_pull(cluster, s, masks, n, s.loc[r], s.colr, r2, rv, ri), 0.0);
       if (absakk * sigma >= kAlpha * lambda * lambda)
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) bkc_factor_kernel(Params p) {
     // D block; for 2x2, [L(i,k) L(i,k+1)] = [wa_i wb_i] D^{-1}
     const double a2 = wa[cix(s, p0)], b2 = kind == 2 ? wa[cix(s, p1)] : 0.0, c2 = kind == 2 ? wb[cix(s, p1)] : 0.0;
     const double det = a2 * c2 - b2 * b2;
-    const double rdk = a2 != 0.0 ? 1.0 / a2 : 0.0;
+    const double rdk = fabs(a2) > p.eps ? 1.0 / a2 : 0.0;  // |d| <= eps: no update (linalg.cpp:226-229)
     __syncthreads();  // D read by every thread before the pivot entries are cleared
     if (threadIdx.x == 0) {
       // the pivot indices are retired: their column entries must not update anything

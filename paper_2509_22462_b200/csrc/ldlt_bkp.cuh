@@ -52,6 +52,7 @@ struct Params {
   int* ctl;       // [4]: qmin, panel width
   int n;
   int nb;
+  double eps;  // zero-pivot threshold 1e-11 max|SAS| (linalg.cpp:101, 143-157, 226-229)
   long long* trace;  // diagnostics (GBOPT_LDLT_TIMING): CTA 0's clocks per phase [8], or null
 };
 
@@ -237,7 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1) bkp_factor_kernel(Params p) {
         const double absakk = fabs(wk[q]);
         mark(0);
         int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
-        if (r >= 0 && fmax(absakk, lambda) > 0.0 && absakk < kAlpha * lambda) {
+        // negligible column (linalg.cpp:143-157): exact zero pivot, no interchange
+        const bool negl = !(fmax(absakk, lambda) > p.eps);
+        if (r >= 0 && !negl && absakk < kAlpha * lambda) {
           const int pr = s.loc[r];
           double* wr = s.W + static_cast<int64_t>(nb) * n;  // scratch row
           double rrow[kMaxRowsPerThread];
@@ -277,8 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1) bkp_factor_kernel(Params p) {
         __syncthreads();
         if (threadIdx.x == 0) {
           if (kind != 2) {
-            const double dk = wk[p0];
-            s.g0[jj] = dk != 0.0 ? 1.0 / dk : 0.0;
+            const double dk = negl ? 0.0 : wk[p0];
+            s.g0[jj] = fabs(dk) > p.eps ? 1.0 / dk : 0.0;  // |d| <= eps: zero L column (linalg.cpp:226-229)
             s.g1[jj] = 0.0;
             s.pp[jj] = jj;
             p.d[k] = dk;

@@ -5,6 +5,7 @@
 #include <exception>
 #include <string>
 #include <thread>
+#include <utility>
 
 #include "device_net.hpp"
 #include "errors.hpp"
@@ -52,10 +53,25 @@ void run_slots(int n, F&& f) {
 }  // namespace
 
 MultiSlot::MultiSlot() = default;
-MultiSlot::MultiSlot(MultiSlot&&) noexcept = default;
-MultiSlot& MultiSlot::operator=(MultiSlot&&) noexcept = default;
+// Moves hand over the raw CUDA handles: the moved-from slot must not free
+// the stream and buffers the new owner keeps using.
+MultiSlot::MultiSlot(MultiSlot&& o) noexcept { *this = std::move(o); }
+MultiSlot& MultiSlot::operator=(MultiSlot&& o) noexcept {
+  if (this == &o) return *this;
+  ordinal = o.ordinal;
+  own = std::move(o.own);
+  dn = std::exchange(o.dn, nullptr);
+  st = std::exchange(o.st, nullptr);
+  x = std::exchange(o.x, nullptr);
+  lam = std::exchange(o.lam, nullptr);
+  y = std::exchange(o.y, nullptr);
+  j = std::exchange(o.j, nullptr);
+  h = std::exchange(o.h, nullptr);
+  cap = std::exchange(o.cap, 0);
+  return *this;
+}
 MultiSlot::~MultiSlot() {
-  if (st == nullptr && x == nullptr) return;
+  if (st == nullptr && x == nullptr && lam == nullptr && y == nullptr && j == nullptr && h == nullptr) return;
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(ordinal);

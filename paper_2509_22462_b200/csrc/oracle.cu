@@ -108,7 +108,8 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   sm_count_ = prop.multiProcessorCount;
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDfSmemBytes));
-  if (const char* e = std::getenv("GBOPT_DATAFLOW")) dataflow_mode_ = e[0] == '0' ? 0 : 1;
+  if (const char* e = std::getenv("GBOPT_DATAFLOW"))
+    dataflow_mode_ = e[0] == '0' ? 0 : (e[0] == '-' && e[1] == '2') ? -2 : 1;
   if (const char* e = std::getenv("GBOPT_DF_GROUP")) df_group_ = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("GBOPT_DF_SQ")) df_square_ = e[0] != '0';
   // (A maximal shared-memory carveout, tried so GEMV CTAs could co-reside with
@@ -980,14 +981,36 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
 
 void DeviceNet::run(cudaStream_t st, int nb, const Outputs& o) {
   const int mode = net_.schedule >= 0 ? net_.schedule : dataflow_mode_;
-  if (mode < 0 && dataflow_possible(nb, o) && df_choice_.count(choice_key(nb, o)) == 0) autotune(st, nb, o);
+  if (mode == -2 && dataflow_possible(nb, o) && df_choice_.count(choice_key(nb, o)) == 0) autotune(st, nb, o);
   dispatch(st, nb, o);
 }
 
-// Auto schedule: the first evaluation of a shape runs both schedules twice
-// (warm, then timed with events on `st`) and keeps the faster.  Both compute
-// the same quantities; the measured winner depends on how the tangent GEMM
-// tiles quantise onto the SMs.
+// Auto schedule (mode -1): a fixed rule on the shape, so every process picks
+// the same kernels for the same call and the results are reproducible bit
+// for bit.  The dataflow launch removes the per-layer barrier of the
+// layer-by-layer graph; that pays when the chain is deep (>= 8 layers) AND
+// the tangent GEMM tiles of a layer quantise badly onto the SMs (>= 10% of
+// the layer-by-layer waves idle), so the barriers cost whole partial waves.
+// Fitted to the measured pairs (layered vs dataflow, round 1): c5 (21
+// layers, 896 tiles = 6.05 waves, 13.5% idle) 656 vs 713 evals/s -> dataflow;
+// c2 (6 layers, 280 tiles) 180.6 vs 173.8 -> layered; c1 (3 layers) layered.
+bool DeviceNet::dataflow_rule(int nb) const {
+  if (L_ < 8) return false;
+  const int64_t row_blocks = n_pad_ / kBM;
+  double waves = 0.0, busy = 0.0;
+  for (int64_t l = 1; l + 1 < L_; ++l) {
+    const int64_t tiles = nb * row_blocks * ceil_div(layers_[static_cast<size_t>(l)].rows, static_cast<int64_t>(kBN));
+    const double w = static_cast<double>(tiles) / sm_count_;
+    busy += w;
+    waves += std::ceil(w);
+  }
+  return waves > 0.0 && (waves - busy) / waves >= 0.10;
+}
+
+// Opt-in measured schedule (mode -2, GBOPT_DATAFLOW=-2 / set_schedule(-2)):
+// the first evaluation of a shape runs both schedules twice (warm, then
+// timed with events on `st`) and keeps the faster.  Not the default: two
+// processes may time differently and pick different kernels.
 void DeviceNet::autotune(cudaStream_t st, int nb, const Outputs& o) {
   ensure_transposed();
   dataflow_plan(nb);
@@ -1219,9 +1242,11 @@ bool DeviceNet::dataflow_ok(int nb, const Outputs& o) const {
   if (df_force_ >= 0) mode = df_force_;
   if (mode == 0 || !dataflow_possible(nb, o)) return false;
   if (mode == 1) return true;
-  // auto: what the first evaluation of this shape measured (autotune in run())
-  const auto c = df_choice_.find(choice_key(nb, o));
-  return c != df_choice_.end() && c->second;
+  if (mode == -2) {  // measured: what the first evaluation of this shape timed (autotune in run())
+    const auto c = df_choice_.find(choice_key(nb, o));
+    return c != df_choice_.end() && c->second;
+  }
+  return dataflow_rule(nb);  // auto: the shape rule
 }
 
 // One eager dataflow evaluation with the per-item trace on: rows of

@@ -317,8 +317,9 @@ class NeuralNet:
         return int(_net_last_launch_count(self._h))
 
     def set_schedule(self, schedule: str) -> "NeuralNet":
-        """'auto', 'layered' or 'dataflow' (gbopt_net_set_schedule)."""
-        code = {"auto": -1, "layered": 0, "dataflow": 1}[schedule]
+        """'auto' (shape rule), 'layered', 'dataflow' or 'measured'
+        (gbopt_net_set_schedule)."""
+        code = {"auto": -1, "layered": 0, "dataflow": 1, "measured": -2}[schedule]
         _check(_net_set_schedule(self._h, code))
         return self
 

@@ -14,9 +14,11 @@ restating the reference's ``embed_reduced_space`` block
   local (r, c) are flipped where the host's input indices are not
   ascending, exactly like the reference.
 
-Each callback does the least device work that answers it and caches per x:
-residual -> forward, Jacobian -> reverse mode (m sweeps), Hessian -> the
-fused y/J/H evaluation (which also refreshes y and J).
+Each callback does the least device work that answers it and caches per x,
+and every quantity has exactly one producer, so a callback's value at x does
+not depend on which callbacks ran before it: residual -> forward, Jacobian ->
+reverse mode (m sweeps), Hessian -> the fused evaluation with the Hessian
+only (its y and J are not kept).
 """
 from __future__ import annotations
 
@@ -83,9 +85,9 @@ class ReducedSpaceBlock:
         if self._hx is None or not np.array_equal(x, self._hx) or not np.array_equal(neg, self._hl):
             # the device packs the lower triangle in the pattern's value order
             # (a flipped (r, c) pattern entry has the same value: H is symmetric)
-            y, j, hv = self.net.oracle_lower(x, neg)
-            self._y, self._j, self._h = y, j, hv
-            self._yx = self._jx = self._hx = x.copy()
+            _, _, hv = self.net.oracle_lower(x, neg, want_y=False, want_j=False)
+            self._h = hv
+            self._hx = x.copy()
             self._hl = neg.copy()
             self.evaluations += 1
         return self._h.copy()

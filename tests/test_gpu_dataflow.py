@@ -7,6 +7,8 @@ against the layer-by-layer schedule on the same handle.
 Parity metric: per array and per point,
 max|GPU - CPU| / max|CPU| <= 1e-10 (north_star tolerance, FP64).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -215,3 +217,38 @@ def test_host_call_in_chunks(monkeypatch, chunks):
             assert orc.rel_err(Y[b], Y0[b]) <= 1e-14 and orc.rel_err(J[b], J0[b]) <= 1e-14
             assert orc.rel_err(H[b], H0[b]) <= 1e-14
             assert orc.rel_err(H[b], ref.lagrangian_hessian(X[b], Lam[b])) <= TOL
+
+
+def test_auto_schedule_is_a_shape_rule():
+    """The default schedule is a fixed rule on the shape (no timing), so
+    c5 (21 layers, 13.5% idle waves) always takes the dataflow launch and
+    c1 / c2 the layer-by-layer graph."""
+    if not has_gpu():
+        pytest.skip("no GPU")
+    for name, batch, want in (("c5", 16, "dataflow"), ("c1", 1, "layered"), ("c4", 64, "layered")):
+        wl = configs.make(name, batch=batch)
+        net = wl.net.bind_device(0)
+        net.oracle_batched(wl.X, wl.Lam)
+        assert net.last_schedule == want, (name, net.last_schedule)
+
+
+_HASH_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, {root!r})
+from paper_2509_22462_b200 import configs
+wl = configs.make("c5", batch=16)
+net = wl.net.bind_device(0)
+Y, J, H = net.oracle_batched(wl.X, wl.Lam)
+print(net.last_schedule, hashlib.sha256(Y.tobytes() + J.tobytes() + H.tobytes()).hexdigest())
+"""
+
+
+def test_two_processes_give_bitwise_identical_outputs():
+    if not has_gpu():
+        pytest.skip("no GPU")
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = [subprocess.run([sys.executable, "-c", _HASH_SCRIPT.format(root=root)], capture_output=True, text=True,
+                           timeout=600).stdout.strip() for _ in range(2)]
+    assert outs[0] and outs[0] == outs[1], outs

@@ -1,0 +1,130 @@
+"""f3 LDL^T against the REFERENCE'S OWN linalg.cpp (oracle/_ref, compiled
+unmodified; its doctest suite test_linalg.cpp passes against that build).
+
+The inertia of every native factorisation kernel (blocked panel, one-cluster,
+cooperative grid) must equal the reference's, including the reference's
+zero-pivot rules (linalg.cpp:143-157 negligible column -> exact zero pivot;
+:226-229 |d| <= 1e-11 max|SAS| -> zero L column), which decide the inertia
+of numerically rank-deficient KKT matrices -- the case the IPM's inertia
+correction (ipm.cpp:520-557) exists for.  Plus the large-n paths: the
+multi-CTA grid kernel (n ~ 4000) and the cuSOLVER fallback with iterative
+refinement beyond 32768 rows.
+"""
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from oracle import ldlt_oracle as lo
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(not ref.available(), reason="oracle/_ref not shipped")
+
+
+@pytest.fixture(autouse=True)
+def _gpu():
+    if not has_gpu():
+        pytest.skip("no GPU")
+
+
+def sym(rng, n):
+    m = rng.uniform(-1, 1, (n, n))
+    return 0.5 * (m + m.T)
+
+
+def cases():
+    rng = np.random.default_rng(7)
+    out = {}
+    out["identity"] = np.eye(3)
+    out["diag"] = np.diag([2.0, -5.0])
+    out["zero"] = np.zeros((5, 5))
+    out["spectrum"] = lo.matrix_with_spectrum(rng, [4, 3, 2, 1, -1, -2, -3, 0])
+    for n in (2, 17, 33, 65, 150):
+        out[f"random_{n}"] = sym(rng, n)
+    a = sym(rng, 90)
+    a[np.diag_indices(90)] *= 1e-8
+    out["heavy_pivoting"] = a
+    b = rng.uniform(-1, 1, (20, 17))
+    out["rank_deficient"] = b @ b.T
+    # a well-conditioned block beside a block at noise level (1e-14 of the
+    # scale): the reference takes zero pivots there instead of forming 2x2
+    # blocks from noise
+    r = sym(rng, 40) + 4 * np.eye(40)
+    e = 1e-14 * sym(rng, 12)
+    out["noise_block"] = np.block([[r, np.zeros((40, 12))], [np.zeros((12, 40)), e]])
+    # KKT with linearly dependent constraint rows (+ noise): the zero
+    # eigenvalues the inertia correction must see
+    n, m = 60, 20
+    H = sym(rng, n) + np.diag(rng.uniform(1, 3, n))
+    J = rng.uniform(-1, 1, (m, n))
+    J[10:] = J[:10] + 1e-15 * rng.uniform(-1, 1, (10, n))
+    out["kkt_dependent_rows"] = np.block([[H, J.T], [J, np.zeros((m, m))]])
+    return out
+
+
+CASES = cases()
+
+
+@needs_ref
+@pytest.mark.parametrize("path", ["panel", "cluster", "grid"])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_inertia_equals_reference_linalg(monkeypatch, path, name):
+    import paper_2509_22462_b200 as gb
+    monkeypatch.setenv("GBOPT_LDLT_KERNEL", path)
+    A = CASES[name]
+    want = ref.RefLdlt(A).inertia
+    f = gb.ldlt_factor(A)
+    assert f.inertia == want, (name, path, f.inertia, want)
+    if want[2] == 0:
+        b = np.linspace(-1, 1, A.shape[0])
+        x = f.solve(b)
+        xr = ref.RefLdlt(A).solve(b)
+        assert np.abs(A @ x - b).max() <= 1e-9 * (np.abs(A).max() * np.abs(x).max() + 1.0)
+        assert np.abs(x - xr).max() <= 1e-6 * (np.abs(xr).max() + 1.0)
+    else:
+        with pytest.raises(gb.SingularError):
+            f.solve(np.ones(A.shape[0]))
+
+
+@needs_ref
+def test_multi_cta_grid_kernel_n4000_matches_reference():
+    """n = 4000 > the one-CTA-per-SM limit: the default path runs the grid
+    kernel with several CTAs per SM and > 256 partial maxima."""
+    import paper_2509_22462_b200 as gb
+    rng = np.random.default_rng(4000)
+    n, m = 3200, 800
+    H = sym(rng, n) + np.diag(10.0 ** rng.uniform(-2, 4, n))
+    J = rng.uniform(-1, 1, (m, n))
+    K = np.block([[H, J.T], [J, -1e-8 * np.eye(m)]])
+    ref.set_threads(16)
+    want = ref.RefLdlt(K).inertia
+    f = gb.ldlt_factor(K)
+    assert f.inertia == want
+    b = rng.uniform(-1, 1, n + m)
+    x = f.solve(b)
+    assert np.abs(K @ x - b).max() <= 1e-8 * (np.abs(K).max() * np.abs(x).max() + 1.0)
+
+
+def test_beyond_32768_rows_refined_solve():
+    """n = 33000: the cuSOLVER path with the retained input; the refinement
+    residual covers every row (ldlt_residual_kernel strides over rows).  A
+    saddle point [[D, J^T], [J, 0]] with D > 0 and J of full row rank has
+    inertia (n1, m, 0) exactly."""
+    import paper_2509_22462_b200 as gb
+    rng = np.random.default_rng(33)
+    n1, m = 32000, 1000
+    K = np.zeros((n1 + m, n1 + m))
+    K[np.arange(n1), np.arange(n1)] = rng.uniform(1.0, 4.0, n1)
+    J = np.zeros((m, n1))
+    for i in range(m):  # each constraint touches its own 32 variables (+ a shared one)
+        J[i, 32 * i:32 * i + 32] = rng.uniform(0.5, 1.5, 32)
+        J[i, n1 - 1 - i] += 1.0
+    K[n1:, :n1] = J
+    K[:n1, n1:] = J.T
+    f = gb.ldlt_factor(K, keep_input=True)
+    assert f.inertia == (n1, m, 0)
+    b = rng.uniform(-1, 1, n1 + m)
+    x = f.solve(b)
+    r = K @ x - b
+    assert np.abs(r).max() <= 1e-10 * (np.abs(K).max() * np.abs(x).max() + 1.0)
+    assert np.abs(r[-(n1 + m - 32768):]).max() <= 1e-10 * (np.abs(x).max() + 1.0)

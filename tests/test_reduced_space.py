@@ -95,3 +95,30 @@ def test_non_ascending_inputs_flip_the_pattern_and_caching():
     blk.jacobian(xb)
     blk.lag_hessian(xb, lam)
     assert blk.evaluations == n0
+
+
+@pytest.mark.parametrize("order", [("r", "j", "h"), ("h", "j", "r"), ("j", "h", "r"), ("h", "r", "j")])
+def test_callback_values_do_not_depend_on_call_order(order):
+    """The reference callbacks are pure functions of x (formulations.cpp:
+    317-340 call forward / jacobian / lagrangian_hessian afresh); each cached
+    quantity here has one producer, so the values are bitwise independent of
+    the order the IPM asks for them."""
+    from paper_2509_22462_b200.reduced_space import ReducedSpaceBlock
+    import paper_2509_22462_b200 as gb
+    net = gb.random_net([30, 40, 40, 4], "tanh", "linear", 5).bind_device(0)
+    rng = np.random.default_rng(1)
+    xb = rng.uniform(-1, 1, 34)
+    lam = rng.uniform(-1, 1, 4)
+    ref = ReducedSpaceBlock(net)
+    want = {"r": ref.residual(xb), "j": ref.jacobian(xb), "h": ref.lag_hessian(xb, lam)}
+    blk = ReducedSpaceBlock(net)
+    got = {}
+    for c in order:
+        got[c] = {"r": lambda: blk.residual(xb), "j": lambda: blk.jacobian(xb),
+                  "h": lambda: blk.lag_hessian(xb, lam)}[c]()
+    for c in "rjh":
+        assert np.array_equal(got[c], want[c]), c
+    # and once more after the caches are warm, in reverse
+    for c in reversed(order):
+        again = {"r": blk.residual(xb), "j": blk.jacobian(xb), "h": blk.lag_hessian(xb, lam)}[c]
+        assert np.array_equal(again, want[c])
