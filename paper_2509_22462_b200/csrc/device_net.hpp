@@ -227,6 +227,13 @@ class DeviceNet {
   double* stage_ = nullptr;  // pinned staging for results bound for pageable host buffers
   size_t stage_cap_ = 0;
   bool last_dataflow_ = false;
+  // persistent single-point forward (fwd_stream.cuh)
+  bool fwd_stream_ok() const;
+  size_t fwd_stream_smem() const;
+  void launch_fwd_stream(cudaStream_t st);
+  unsigned* fs_arrive_ = nullptr;
+  bool fs_attr_set_ = false;
+  int fwd_stream_mode_ = 1;  // GBOPT_FWD_STREAM=0: per-layer GEMV launches instead
 };
 
 }  // namespace gbb

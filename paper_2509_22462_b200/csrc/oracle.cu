@@ -34,6 +34,7 @@
 #include "device_net.hpp"
 #include "multi.hpp"
 #include "kernels.cuh"
+#include "fwd_stream.cuh"
 #include "net.hpp"
 
 namespace gbb {
@@ -84,6 +85,18 @@ CUtensorMap make_tmap(const double* base, int64_t cols, int64_t rows, int64_t pi
 }
 
 int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// Several DeviceNets may run on host threads at once (multi-device calls,
+// multi.cpp; or a caller's own threads with distinct handles).  Graph
+// capture, and the allocation / device-wide synchronisation that first calls
+// of a shape do, must not interleave across threads (a cudaMalloc / cudaFree /
+// cudaDeviceSynchronize while another thread captures fails that capture), so
+// they take this process-wide lock.  Steady-state calls (graph launches) do
+// not.
+std::recursive_mutex& setup_mutex() {
+  static std::recursive_mutex m;
+  return m;
+}
 
 // From this many points on, the forward and adjoint chains run as DMMA GEMMs
 // over the batch instead of GEMV sweeps.
@@ -192,11 +205,13 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaMalloc(&sq_tiles_, sizeof(int2) * sq.size()));
   CK(cudaMemcpy(sq_tiles_, sq.data(), sizeof(int2) * sq.size(), cudaMemcpyHostToDevice));
   if (const char* e = std::getenv("GBOPT_SQ")) square_syrk_ = e[0] != '0';
+  if (const char* e = std::getenv("GBOPT_FWD_STREAM")) fwd_stream_mode_ = e[0] == '0' ? 0 : 1;
 }
 
 DeviceNet::~DeviceNet() {
   DeviceGuard g(ordinal_);
   free_workspace();
+  if (fs_arrive_) cudaFree(fs_arrive_);
   if (stage_) cudaFreeHost(stage_);
   for (auto& d : layers_) {
     cudaFree(d.w);
@@ -262,6 +277,7 @@ DeviceNet::AdjLayout DeviceNet::adj_layout(const DevLayer& d, bool multi) const 
 
 void DeviceNet::ensure_workspace(int batch) {
   if (batch <= ws_cap_) return;
+  std::lock_guard<std::recursive_mutex> lock(setup_mutex());
   free_workspace();
   const int cap = batch;
   const int64_t vcap = static_cast<int64_t>(cap) * std::max<int64_t>(m_, 1);
@@ -362,6 +378,7 @@ void DeviceNet::ensure_workspace(int batch) {
 // made once, on first use, by a device transpose.
 void DeviceNet::ensure_transposed() {
   if (transposed_) return;
+  std::lock_guard<std::recursive_mutex> lock(setup_mutex());
   for (auto& d : layers_) {
     d.ldwt = round_up(d.rows, 16);
     CK(cudaMalloc(&d.wt, sizeof(double) * d.cols * d.ldwt));
@@ -1052,6 +1069,7 @@ void DeviceNet::dispatch(cudaStream_t st, int nb, const Outputs& o) {
   }
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
+    std::lock_guard<std::recursive_mutex> lock(setup_mutex());
     launches_ = 0;
     cudaGraph_t graph = nullptr;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -1074,6 +1092,79 @@ void DeviceNet::dispatch(cudaStream_t st, int nb, const Outputs& o) {
   }
   CK(cudaGraphLaunch(it->second.exec, st));
   last_launches_ = it->second.launches;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent single-point forward (fwd_stream.cuh).
+// ---------------------------------------------------------------------------
+size_t DeviceNet::fwd_stream_smem() const {
+  int64_t ycap = 16, max_rows = 1;
+  for (const DevLayer& d : layers_) {
+    ycap = std::max(ycap, d.ldw);
+    max_rows = std::max<int64_t>(max_rows, (d.rows + sm_count_ - 1) / sm_count_ + 1);
+  }
+  return static_cast<size_t>(dev::kFsStages) * dev::kFsStageBytes + 8 * static_cast<size_t>(ycap) +
+         8 * static_cast<size_t>(max_rows) * dev::kFsConsumerWarps + 16 * dev::kFsStages;
+}
+
+bool DeviceNet::fwd_stream_ok() const {
+  if (fwd_stream_mode_ == 0) return false;
+  if (L_ > dev::kFsMaxLayers || profiling_) return false;
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ordinal_) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return fwd_stream_smem() <= static_cast<size_t>(optin);
+}
+
+// x already in ws_.x (point 0); z, y, s1, s2 of every layer to the workspace.
+void DeviceNet::launch_fwd_stream(cudaStream_t st) {
+  Workspace& w = ws_;
+  if (!fs_arrive_) {
+    std::lock_guard<std::recursive_mutex> lock(setup_mutex());
+    CK(cudaMalloc(&fs_arrive_, sizeof(unsigned) * dev::kFsMaxLayers));
+  }
+  static thread_local dev::FsParams p;  // ~3 KB, copied at launch
+  p.nl = static_cast<int>(L_);
+  p.x = w.x;
+  p.arrive = fs_arrive_;
+  int64_t ycap = 16, max_rows = 1;
+  for (int64_t l = 0; l < L_; ++l) {
+    const DevLayer& d = layers_[static_cast<size_t>(l)];
+    dev::FsLayer& f = p.L[l];
+    f.w = d.w;
+    f.b = d.b;
+    f.z = w.z[static_cast<size_t>(l)];
+    f.y = w.y[static_cast<size_t>(l)];
+    f.s1 = w.s1[static_cast<size_t>(l)];
+    f.s2 = w.s2[static_cast<size_t>(l)];
+    f.rows = static_cast<int>(d.rows);
+    f.cols = static_cast<int>(d.cols);
+    f.ldw = static_cast<int>(d.ldw);
+    f.act = d.act == kSoftmax ? kLinear : d.act;
+    ycap = std::max(ycap, d.ldw);
+    max_rows = std::max<int64_t>(max_rows, (d.rows + sm_count_ - 1) / sm_count_ + 1);
+  }
+  p.ycap = static_cast<int>(ycap);
+  p.max_cta_rows = static_cast<int>(max_rows);
+  const size_t smem = fwd_stream_smem();
+  if (!fs_attr_set_) {
+    CK(cudaFuncSetAttribute(dev::fwd_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    fs_attr_set_ = true;
+  }
+  CK(cudaMemsetAsync(fs_arrive_, 0, sizeof(unsigned) * dev::kFsMaxLayers, st));
+  void* args[] = {&p};
+  prof_begin(st, kTagFwd, 0.0, 0.0);
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::fwd_stream_kernel), dim3(sm_count_),
+                                 dim3(dev::kFsThreads), args, smem, st));
+  after_launch(st);
+  if (L_ > 0 && layers_[static_cast<size_t>(L_ - 1)].act == kSoftmax) {
+    dev::softmax_kernel<<<1, 128, 0, st>>>(w.z[static_cast<size_t>(L_ - 1)], w.y[static_cast<size_t>(L_ - 1)],
+                                            static_cast<int>(m_), w.ld[static_cast<size_t>(L_ - 1)], 1);
+    after_launch(st);
+  }
 }
 
 // Host-buffer entry: copy in, evaluate, copy out, synchronise.
@@ -1106,6 +1197,7 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
     out_bytes += sizeof(double) * outs[i].per_point * nb;
   }
   if (staged > stage_cap_) {
+    std::lock_guard<std::recursive_mutex> lock(setup_mutex());  // cudaFreeHost synchronises the device
     if (stage_) cudaFreeHost(stage_);
     stage_ = nullptr;
     stage_cap_ = 0;
@@ -1121,6 +1213,21 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   // smaller chunks cost more than they hide.  Measured: c4 (4096 points) 4
   // chunks 56.0k -> 59.6k e2e evals/s (8 chunks: 59.4k); c5 (16 points, 8.8k
   // flop/B) 2 chunks 700 -> 717 (4 chunks: 699).
+  // Forward only (the line-search residual, forward_trace): one persistent
+  // launch streams every layer's weights (fwd_stream.cuh).
+  if (nb == 1 && !jac && !hess && !grad && fwd_stream_ok()) {
+    launches_ = 0;
+    CK(cudaMemcpyAsync(w.x, x, sizeof(double) * n_, cudaMemcpyHostToDevice, stream_));
+    launch_fwd_stream(stream_);
+    if (y) {
+      double* d = pinned[0] ? y : stage_;
+      CK(cudaMemcpyAsync(d, w.y[static_cast<size_t>(L_ - 1)], sizeof(double) * m_, cudaMemcpyDeviceToHost, stream_));
+    }
+    CK(cudaStreamSynchronize(stream_));
+    if (y && !pinned[0]) std::memcpy(y, stage_, sizeof(double) * m_);
+    last_launches_ = launches_;
+    return;
+  }
   double flops = 0.0;  // F_jac + F_hess per point
   for (size_t l = 0; l < layers_.size(); ++l) {
     if (l > 0) flops += 2.0 * static_cast<double>(layers_[l].rows * layers_[l].cols * n_);
@@ -1331,6 +1438,7 @@ void DeviceNet::free_plans() {
 DfPlan& DeviceNet::dataflow_plan(int nb) {
   auto found = df_plans_.find(nb);
   if (found != df_plans_.end()) return found->second;
+  std::lock_guard<std::recursive_mutex> lock(setup_mutex());
   Workspace& w = ws_;
   const int L = static_cast<int>(L_);
   const int tiles_m = static_cast<int>(n_pad_ / kBM);

@@ -1,6 +1,9 @@
-"""KKT factorisation row (f3): GPU LDL^T (gbopt_ldlt_factor + one solve)
-against the CPU oracle path (Ruiz + LAPACK sytrf via scipy, all threads)
-on seeded IPM-like KKT matrices.  python tools/bench_ldlt.py [n ...]"""
+"""KKT factorisation row (f3): GPU LDL^T (gbopt_ldlt_factor + one refined
+solve, host matrix in) against the reference's OWN linalg.cpp (oracle/_ref:
+ldlt_factor with Ruiz equilibration + blocked Bunch-Kaufman, then solve with
+iterative refinement; OpenBLAS products on all host threads) on seeded
+IPM-like KKT matrices.  Both sides do the same work: one factorisation and
+one refined solve.  python tools/bench_ldlt.py [n ...]"""
 import json
 import os
 import sys
@@ -10,7 +13,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_22462_b200 as gb  # noqa: E402
-from oracle import ldlt_oracle as lo  # noqa: E402
+from oracle import ref  # noqa: E402
 
 
 def kkt(n, m, seed):
@@ -21,6 +24,8 @@ def kkt(n, m, seed):
     return np.block([[H, J.T], [J, -1e-8 * np.eye(m)]]), rng.uniform(-1, 1, n + m)
 
 
+threads = os.cpu_count() or 1
+ref.set_threads(threads)
 out = []
 for n in [int(v) for v in sys.argv[1:]] or [784, 2000, 4000]:
     K, b = kkt(n, n // 8, n)
@@ -30,9 +35,11 @@ for n in [int(v) for v in sys.argv[1:]] or [784, 2000, 4000]:
     x = f.solve(b)
     tg = time.perf_counter() - t0
     t0 = time.perf_counter()
-    inert = lo.inertia(K)
-    xc = np.linalg.solve(K, b)
+    rf = ref.RefLdlt(K)
+    xr = rf.solve(b)
     tc = time.perf_counter() - t0
-    out.append({"dim": K.shape[0], "gpu_factor_solve_s": tg, "cpu_oracle_s": tc, "inertia_gpu": f.inertia,
-                "inertia_cpu": inert, "residual": float(np.abs(K @ x - b).max()), "cpu_threads": os.cpu_count()})
+    out.append({"dim": K.shape[0], "gpu_factor_solve_s": tg, "ref_linalg_factor_solve_s": tc,
+                "inertia_gpu": f.inertia, "inertia_ref": rf.inertia,
+                "residual_gpu": float(np.abs(K @ x - b).max()), "residual_ref": float(np.abs(K @ xr - b).max()),
+                "cpu_threads": threads, "cpu": "reference linalg.cpp (oracle/_ref), OpenBLAS products"})
     print(json.dumps(out[-1]), flush=True)
