@@ -232,8 +232,12 @@ class DeviceNet {
   size_t fwd_stream_smem() const;
   void launch_fwd_stream(cudaStream_t st);
   unsigned* fs_arrive_ = nullptr;
+  unsigned fs_gen_ = 0;
   bool fs_attr_set_ = false;
-  int fwd_stream_mode_ = 1;  // GBOPT_FWD_STREAM=0: per-layer GEMV launches instead
+  // GBOPT_FWD_STREAM=1 opts in; off by default: measured slower than the
+  // per-layer GEMV graph (c2 165 vs 155 us device time, c5 130 vs 80 us;
+  // profiles/r02_fwd_stream.md)
+  int fwd_stream_mode_ = 0;
 };
 
 }  // namespace gbb

@@ -1,3 +1,12 @@
+// OPT-IN (GBOPT_FWD_STREAM=1), not the default: measured slower than the
+// per-layer GEMV launches of the CUDA graph on every BASELINE shape (device
+// time, CUDA events: c2 165 vs 155 us, c5 130 vs 80 us, c1 ~45 vs ~35 us;
+// profiles/r02_fwd_stream.md).  The inter-layer barrier (CTA barrier,
+// release/acquire round trip, epilogue) costs ~2.4 us per layer, more than the
+// graph's kernel boundaries, and one CTA per SM with a 5-stage TMA ring reads
+// no faster than 8 warps of 16-byte loads per row.  Kept as a measured
+// alternative.
+//
 // Forward pass of one point through the whole network in ONE persistent
 // launch (the line-search residual and forward_trace, reference
 // nn.cpp:113-146 / ipm.cpp:342-343): every layer is an HBM-bound GEMV, so
@@ -8,7 +17,7 @@
 //    CTA's weights of a layer are ONE contiguous byte range (row-major W,
 //    pitch ldw): the producer streams it with 1-D TMA bulk copies
 //    (cp.async.bulk, 40 KB chunks = whole rows, or row segments for rows
-//    wider than a chunk) into a 4-stage shared-memory ring guarded by
+//    wider than a chunk) into a 5-stage shared-memory ring guarded by
 //    full / empty mbarriers;
 //  * the producer never waits on the layer dependency: it runs straight on
 //    into the next layer's rows while the consumers finish the current
@@ -21,8 +30,10 @@
 //    applied (the same epilogue as fwd_row1_kernel), and z, y, s1, s2 go to
 //    the workspace;
 //  * inter-layer barrier among the consumer warps only (one arrival counter
-//    per layer, release/acquire at gpu scope), then y_l is staged in shared
-//    memory for layer l + 1.
+//    per layer, release/acquire at gpu scope); each warp then loads its
+//    k-slice of y_l into registers for layer l + 1 (whole-row chunks), so the
+//    ring gets all of shared memory (5 x 40 KB) to keep loads in flight
+//    across the barrier.
 #pragma once
 
 #include <cstdint>
@@ -32,7 +43,8 @@ namespace dev {
 
 constexpr int kFsConsumerWarps = 8;
 constexpr int kFsThreads = (kFsConsumerWarps + 1) * 32;
-constexpr int kFsStages = 4;
+constexpr int kFsStages = 5;
+constexpr int kFsYRegs = 16;  // double2 per lane: a warp's input slice up to 16 x 64 doubles
 constexpr int kFsStageBytes = 40960;  // one 5120-wide FP64 row
 constexpr int kFsMaxLayers = 48;
 
@@ -46,7 +58,9 @@ struct FsLayer {
 struct FsParams {
   FsLayer L[kFsMaxLayers];
   const double* x;     // layer 0's input
-  unsigned* arrive;    // [nl] per-layer arrival counters (zeroed before the launch)
+  unsigned* arrive;    // [nl] per-layer arrival counters, never reset: launch number
+                       // `gen` (1, 2, ...) waits for gen * gridDim.x arrivals
+  unsigned gen;
   int nl;
   int max_cta_rows;    // partial-sum rows per CTA
   int ycap;            // y staging capacity (doubles, even)
@@ -91,8 +105,7 @@ __device__ __forceinline__ void fs_wait(uint64_t* bar, uint32_t parity) {
 __global__ void __launch_bounds__(kFsThreads, 1) fwd_stream_kernel(const __grid_constant__ FsParams p) {
   extern __shared__ __align__(128) unsigned char fs_smem[];
   double* stage = reinterpret_cast<double*>(fs_smem);
-  double* yv = reinterpret_cast<double*>(fs_smem + kFsStages * kFsStageBytes);
-  double* part = yv + p.ycap;  // [max_cta_rows][kFsConsumerWarps]
+  double* part = reinterpret_cast<double*>(fs_smem + kFsStages * kFsStageBytes);  // [max_cta_rows][warps]
   uint64_t* full = reinterpret_cast<uint64_t*>(part + static_cast<int64_t>(p.max_cta_rows) * kFsConsumerWarps);
   uint64_t* empty = full + kFsStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -151,48 +164,90 @@ __global__ void __launch_bounds__(kFsThreads, 1) fwd_stream_kernel(const __grid_
     const FsLayer& L = p.L[l];
     const FsGeom G = fs_geom(L, cta, ncta);
     const int nrows = G.r1 - G.r0;
-    // stage this layer's input vector (after the previous layer's barrier)
     const double* yin = l == 0 ? p.x : p.L[l - 1].y;
-    for (int k = ct; k < L.ldw; k += kFsConsumerWarps * 32) yv[k] = k < L.cols ? __ldcg(yin + k) : 0.0;
-    for (int i = ct; i < nrows * kFsConsumerWarps; i += kFsConsumerWarps * 32) part[i] = 0.0;
-    asm volatile("bar.sync 1, %0;" ::"n"(kFsConsumerWarps * 32) : "memory");
-    // warp's k-slice of a row segment of `len` doubles: whole 64-double steps
+    // this warp's partial column of the layer's rows starts at 0 (only warp
+    // w ever touches column w: no CTA barrier needed)
+    for (int i = lane; i < nrows; i += 32) part[i * kFsConsumerWarps + warp] = 0.0;
+    // Whole-row chunks: the warp's k-slice is the same for every row, so its
+    // slice of the input vector lives in registers, loaded once per layer
+    // straight from L2 with every load in flight (the previous layer's y was
+    // written by other CTAs: ld.cg after the barrier's acquire).
+    const int steps_row = (L.ldw + 63) / 64;
+    const int wst0 = steps_row * warp / kFsConsumerWarps, wst1 = steps_row * (warp + 1) / kFsConsumerWarps;
+    const bool yreg = G.spr > 0 && wst1 - wst0 <= kFsYRegs;
+    double2 yr[kFsYRegs];
+#pragma unroll
+    for (int u = 0; u < kFsYRegs; ++u) {
+      const int k = (wst0 + u) * 64 + 2 * lane;
+      yr[u] = make_double2(0.0, 0.0);
+      if (yreg && wst0 + u < wst1) {
+        if (k < L.cols) yr[u].x = __ldcg(yin + k);
+        if (k + 1 < L.cols) yr[u].y = __ldcg(yin + k + 1);
+      }
+    }
+    __syncwarp();
     for (int q = 0; q < G.nchunks; ++q, ++g) {
       const int s = g % kFsStages;
       fs_wait(full + s, (g / kFsStages) & 1);
       const double* sb = stage + s * (kFsStageBytes / 8);
-      int rr0, nr, k0, len, pitch;
-      if (G.spr > 0) {
-        rr0 = q * G.spr;
-        nr = min(G.spr, nrows - rr0);
-        k0 = 0;
-        len = L.ldw;
-        pitch = L.ldw;
-      } else {
-        rr0 = q / G.nseg;
-        nr = 1;
-        k0 = (q % G.nseg) * G.seg;
-        len = min(G.seg, L.ldw - k0);
-        pitch = len;
-      }
-      const int steps = (len + 63) / 64;
-      const int st0 = steps * warp / kFsConsumerWarps, st1 = steps * (warp + 1) / kFsConsumerWarps;
-      for (int r = 0; r < nr; ++r) {
-        const double* wr = sb + static_cast<int64_t>(r) * pitch;
-        double a0 = 0.0, a1 = 0.0;
-        for (int t = st0; t < st1; ++t) {
-          const int k = t * 64 + 2 * lane;
-          if (k < len) {
-            const double2 wv = *reinterpret_cast<const double2*>(wr + k);
-            const double2 xv = *reinterpret_cast<const double2*>(yv + k0 + k);
-            a0 = fma(wv.x, xv.x, a0);
-            a1 = fma(wv.y, xv.y, a1);
-          }
-        }
-        double v = a0 + a1;
+      if (yreg) {
+        const int rr0 = q * G.spr;
+        const int nr = min(G.spr, nrows - rr0);
+        for (int r = 0; r < nr; ++r) {
+          const double* wr = sb + static_cast<int64_t>(r) * L.ldw;
+          double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) part[(rr0 + r) * kFsConsumerWarps + warp] += v;
+          for (int u = 0; u < kFsYRegs; ++u) {
+            const int k = (wst0 + u) * 64 + 2 * lane;
+            if (wst0 + u < wst1 && k < L.ldw) {
+              const double2 wv = *reinterpret_cast<const double2*>(wr + k);
+              a0 = fma(wv.x, yr[u].x, a0);
+              a1 = fma(wv.y, yr[u].y, a1);
+            }
+          }
+          double v = a0 + a1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) part[(rr0 + r) * kFsConsumerWarps + warp] += v;
+        }
+      } else {
+        // row segments (rows wider than a chunk) or very wide whole rows:
+        // the input slice comes from L2 with the weights
+        int rr0, nr, k0, len, pitch;
+        if (G.spr > 0) {
+          rr0 = q * G.spr;
+          nr = min(G.spr, nrows - rr0);
+          k0 = 0;
+          len = L.ldw;
+          pitch = L.ldw;
+        } else {
+          rr0 = q / G.nseg;
+          nr = 1;
+          k0 = (q % G.nseg) * G.seg;
+          len = min(G.seg, L.ldw - k0);
+          pitch = len;
+        }
+        const int steps = (len + 63) / 64;
+        const int st0 = steps * warp / kFsConsumerWarps, st1 = steps * (warp + 1) / kFsConsumerWarps;
+        for (int r = 0; r < nr; ++r) {
+          const double* wr = sb + static_cast<int64_t>(r) * pitch;
+          double a0 = 0.0, a1 = 0.0;
+          for (int t = st0; t < st1; ++t) {
+            const int k = t * 64 + 2 * lane;
+            if (k < len) {
+              const double2 wv = *reinterpret_cast<const double2*>(wr + k);
+              const int kk = k0 + k;
+              const double x0 = kk < L.cols ? __ldcg(yin + kk) : 0.0;
+              const double x1 = kk + 1 < L.cols ? __ldcg(yin + kk + 1) : 0.0;
+              a0 = fma(wv.x, x0, a0);
+              a1 = fma(wv.y, x1, a1);
+            }
+          }
+          double v = a0 + a1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) part[(rr0 + r) * kFsConsumerWarps + warp] += v;
+        }
       }
       __syncwarp();
       if (lane == 0)
@@ -216,15 +271,17 @@ __global__ void __launch_bounds__(kFsThreads, 1) fwd_stream_kernel(const __grid_
       L.s2[row] = d2;
     }
     if (l + 1 < p.nl) {
-      // inter-layer barrier over the consumer groups of every CTA
-      __threadfence();
+      // inter-layer barrier over the consumer groups of every CTA: the CTA
+      // barrier orders this CTA's y writes before thread 0's release (which
+      // is cumulative), the acquire + CTA barrier orders the other CTAs'
+      // writes before the next layer's loads
       asm volatile("bar.sync 1, %0;" ::"n"(kFsConsumerWarps * 32) : "memory");
       if (ct == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.arrive + l) : "memory");
         unsigned seen = 0;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.arrive + l) : "memory");
-        } while (seen < static_cast<unsigned>(ncta));
+        } while (seen < p.gen * static_cast<unsigned>(ncta));
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kFsConsumerWarps * 32) : "memory");
     }

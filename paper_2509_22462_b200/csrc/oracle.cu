@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -205,7 +206,7 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaMalloc(&sq_tiles_, sizeof(int2) * sq.size()));
   CK(cudaMemcpy(sq_tiles_, sq.data(), sizeof(int2) * sq.size(), cudaMemcpyHostToDevice));
   if (const char* e = std::getenv("GBOPT_SQ")) square_syrk_ = e[0] != '0';
-  if (const char* e = std::getenv("GBOPT_FWD_STREAM")) fwd_stream_mode_ = e[0] == '0' ? 0 : 1;
+  if (const char* e = std::getenv("GBOPT_FWD_STREAM")) fwd_stream_mode_ = e[0] == '1' ? 1 : 0;
 }
 
 DeviceNet::~DeviceNet() {
@@ -1103,7 +1104,8 @@ size_t DeviceNet::fwd_stream_smem() const {
     ycap = std::max(ycap, d.ldw);
     max_rows = std::max<int64_t>(max_rows, (d.rows + sm_count_ - 1) / sm_count_ + 1);
   }
-  return static_cast<size_t>(dev::kFsStages) * dev::kFsStageBytes + 8 * static_cast<size_t>(ycap) +
+  (void)ycap;
+  return static_cast<size_t>(dev::kFsStages) * dev::kFsStageBytes +
          8 * static_cast<size_t>(max_rows) * dev::kFsConsumerWarps + 16 * dev::kFsStages;
 }
 
@@ -1124,6 +1126,8 @@ void DeviceNet::launch_fwd_stream(cudaStream_t st) {
   if (!fs_arrive_) {
     std::lock_guard<std::recursive_mutex> lock(setup_mutex());
     CK(cudaMalloc(&fs_arrive_, sizeof(unsigned) * dev::kFsMaxLayers));
+    CK(cudaMemset(fs_arrive_, 0, sizeof(unsigned) * dev::kFsMaxLayers));
+    fs_gen_ = 0;
   }
   static thread_local dev::FsParams p;  // ~3 KB, copied at launch
   p.nl = static_cast<int>(L_);
@@ -1154,7 +1158,13 @@ void DeviceNet::launch_fwd_stream(cudaStream_t st) {
                             static_cast<int>(smem)));
     fs_attr_set_ = true;
   }
-  CK(cudaMemsetAsync(fs_arrive_, 0, sizeof(unsigned) * dev::kFsMaxLayers, st));
+  // counters are never reset: this launch waits for gen * grid arrivals per
+  // layer (no memset launch per call); restart from zero before they wrap
+  if (fs_gen_ >= (0xffffffffu / static_cast<unsigned>(sm_count_)) - 1) {
+    CK(cudaMemsetAsync(fs_arrive_, 0, sizeof(unsigned) * dev::kFsMaxLayers, st));
+    fs_gen_ = 0;
+  }
+  p.gen = ++fs_gen_;
   void* args[] = {&p};
   prof_begin(st, kTagFwd, 0.0, 0.0);
   CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::fwd_stream_kernel), dim3(sm_count_),
@@ -1213,12 +1223,29 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
   // smaller chunks cost more than they hide.  Measured: c4 (4096 points) 4
   // chunks 56.0k -> 59.6k e2e evals/s (8 chunks: 59.4k); c5 (16 points, 8.8k
   // flop/B) 2 chunks 700 -> 717 (4 chunks: 699).
-  // Forward only (the line-search residual, forward_trace): one persistent
-  // launch streams every layer's weights (fwd_stream.cuh).
+  // Forward only (the line-search residual, forward_trace), opt-in
+  // (GBOPT_FWD_STREAM=1): one persistent launch streams every layer's weights
+  // (fwd_stream.cuh).  The default is the per-layer GEMV graph below.
   if (nb == 1 && !jac && !hess && !grad && fwd_stream_ok()) {
     launches_ = 0;
     CK(cudaMemcpyAsync(w.x, x, sizeof(double) * n_, cudaMemcpyHostToDevice, stream_));
+    static const bool fwd_events = std::getenv("GBOPT_FWD_EVENTS") != nullptr;  // diagnostics: device time
+    cudaEvent_t fe0 = nullptr, fe1 = nullptr;
+    if (fwd_events) {
+      CK(cudaEventCreate(&fe0));
+      CK(cudaEventCreate(&fe1));
+      CK(cudaEventRecord(fe0, stream_));
+    }
     launch_fwd_stream(stream_);
+    if (fwd_events) {
+      CK(cudaEventRecord(fe1, stream_));
+      CK(cudaEventSynchronize(fe1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, fe0, fe1));
+      std::fprintf(stderr, "GBOPT_FWD_EVENTS stream %.4f ms\n", ms);
+      cudaEventDestroy(fe0);
+      cudaEventDestroy(fe1);
+    }
     if (y) {
       double* d = pinned[0] ? y : stage_;
       CK(cudaMemcpyAsync(d, w.y[static_cast<size_t>(L_ - 1)], sizeof(double) * m_, cudaMemcpyDeviceToHost, stream_));
@@ -1260,7 +1287,23 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
     if (lam)
       CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, lam + static_cast<size_t>(c0) * m_, sizeof(double) * m_,
                            sizeof(double) * m_, nbc, cudaMemcpyHostToDevice, stream_));
+    static const bool fwd_events = std::getenv("GBOPT_FWD_EVENTS") != nullptr;  // diagnostics: device time
+    cudaEvent_t fe0 = nullptr, fe1 = nullptr;
+    if (fwd_events) {
+      CK(cudaEventCreate(&fe0));
+      CK(cudaEventCreate(&fe1));
+      CK(cudaEventRecord(fe0, stream_));
+    }
     run(stream_, nbc, o);
+    if (fwd_events) {
+      CK(cudaEventRecord(fe1, stream_));
+      CK(cudaEventSynchronize(fe1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, fe0, fe1));
+      std::fprintf(stderr, "GBOPT_FWD_EVENTS run %.4f ms\n", ms);
+      cudaEventDestroy(fe0);
+      cudaEventDestroy(fe1);
+    }
     cudaStream_t cs = chunks > 1 ? copy_stream_ : stream_;
     if (chunks > 1) {
       CK(cudaEventRecord(chunk_ev_[static_cast<size_t>(ci)], stream_));

@@ -1,7 +1,8 @@
-"""The persistent single-point forward (csrc/fwd_stream.cuh): one cooperative
-launch streams every layer's weights with 1-D TMA bulk copies; it serves
-forward() (the line-search residual, nn.cpp:113-125) and forward_trace()
-(nn.cpp:127-146).  Checked against the CPU oracle on nets that exercise each
+"""forward() (the line-search residual, nn.cpp:113-125) and forward_trace()
+(nn.cpp:127-146) through both single-point paths: the default per-layer GEMV
+graph and the opt-in persistent launch (csrc/fwd_stream.cuh,
+GBOPT_FWD_STREAM=1: one cooperative launch streaming every layer's weights
+with 1-D TMA bulk copies).  Checked against the CPU oracle on nets that exercise each
 chunk geometry (several rows per chunk, one row per chunk, rows split into
 segments wider than a chunk, fewer rows than SMs, softmax output), against
 the per-layer GEMV path (GBOPT_FWD_STREAM=0, separate process), and for
@@ -34,10 +35,12 @@ def _net(widths, hid, fin, seed):
     return gb.random_net(widths, hid, fin, seed).bind_device(0)
 
 
+@pytest.mark.parametrize("mode", ["1", "0"])
 @pytest.mark.parametrize("widths,hid,fin,seed", NETS)
-def test_forward_stream_matches_oracle(widths, hid, fin, seed):
+def test_forward_stream_matches_oracle(monkeypatch, widths, hid, fin, seed, mode):
     if not has_gpu():
         pytest.skip("no GPU")
+    monkeypatch.setenv("GBOPT_FWD_STREAM", mode)  # read when the handle binds
     net = _net(widths, hid, fin, seed)
     on = orc.NeuralNet([orc.Layer(*net.layer(l)) for l in range(net.layer_count)])
     rng = np.random.default_rng(seed)
@@ -69,7 +72,7 @@ def test_forward_stream_agrees_with_per_layer_path(widths, hid, fin, seed):
     if not has_gpu():
         pytest.skip("no GPU")
     outs = []
-    for mode in ("1", "0"):
+    for mode in ("1", "0"):  # opt-in persistent launch vs the default per-layer graph
         code = _SCRIPT.format(root=ROOT, widths=widths, hid=hid, fin=fin, seed=seed, n=widths[0])
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
                            env=dict(os.environ, GBOPT_FWD_STREAM=mode))
