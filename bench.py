@@ -327,6 +327,16 @@ def load_traffic():
         return None, None
 
 
+def hbm_peak_gbs():
+    """Measured copy bandwidth of this pool's B200s (MEASURED_PEAKS.json,
+    driver-written), else the profiling recipe's fallback."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
 def max_over_ranks(torch, dist, world, dev, t):
     if world <= 1:
         return t
@@ -584,6 +594,33 @@ def run_b200(args):
                                "MEASURED_PEAKS.json); DMMA issue ceiling 37.1 TFLOP/s (tools/fp64_probe.cu)",
                 "traffic_source": tsrc}
 
+    # ---- HBM-bound single-point paths of the IPM callbacks (rank 0) ----
+    # the line-search residual (forward only, ipm.cpp:342-343) and the
+    # Jacobian callback (reverse mode, m seed vectors in one adjoint sweep),
+    # device-timed through the same device entry with only dY / only dJ
+    hbm_paths = None
+    if rank == 0 and name in ("c1", "c2"):
+        hbm_peak, hbm_src = hbm_peak_gbs()
+        wbytes = 8.0 * params_of(WIDTHS[name])
+        hbm_paths = {}
+        for tag, dy, dj, nbytes in (("line_search_forward", Yd.data_ptr(), 0, wbytes),
+                                    ("jacobian_reverse", 0, Jd.data_ptr(), 2.0 * wbytes)):
+            call = lambda: net.oracle_batched_device(1, Xd.data_ptr(), 0, dy, dj, 0, stream.cuda_stream)  # noqa: E731
+            for _ in range(5):
+                call()
+            torch.cuda.synchronize()
+            reps = 50
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(reps):
+                call()
+            f1.record(stream)
+            torch.cuda.synchronize()
+            ms = f0.elapsed_time(f1) / reps
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            hbm_paths[tag] = {"ms": ms, "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "peak_gbs": hbm_peak,
+                              "frac": gbs / hbm_peak, "peak_source": hbm_src, "launches": net.last_launch_count}
+
     # ---- e2e through the public host-buffer API (pinned host memory) ----
     e2e = None
     Yh = Jh = Hh = None
@@ -666,6 +703,7 @@ def run_b200(args):
             "e2e": e2e,
             "parity": parity,
             "sharded": sharded,
+            "hbm_paths": hbm_paths,
             "multi_rank": multi,
             "gpu_launches": int(launches_per_step * args.steps),
             "schedule": schedule,
