@@ -221,7 +221,10 @@ int blocks_for(int64_t work, int per) { return static_cast<int>(std::min<int64_t
 
 }  // namespace
 
-constexpr int64_t kNativeMaxN = 20000;
+// Native Bunch-Kaufman for every size (round 2: the grid kernel's shared
+// memory no longer grows with n); cuSOLVER dsytrf only past this bound,
+// where int32 indexing of the factor kernels would overflow.
+constexpr int64_t kNativeMaxN = 46340;
 constexpr int kScal = 32;  // device scalars after the four n-vectors of d_vec_ (ldlt_prep_kernel)
 constexpr int64_t kCtaSolveMaxN = 3000;  // one-CTA substitution below (n 804: 0.20 vs 0.44 ms; 4500: 3.08 vs 2.45)
 
@@ -355,8 +358,14 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     // left-looking, every column update spanning all previous columns)
     int grid_nb = 64;
     if (const char* e = std::getenv("GBOPT_LDLT_GRID_NB")) grid_nb = std::max(0, std::min(std::atoi(e), bk::kMaxGridNb));
+    // the unblocked mode keeps an n-long vector in shared memory; blocked
+    // panels need only the panel's columns (bk_factor_kernel)
+    int smem_cap = 0;
+    CK(cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    if (grid_nb == 0 && 8 * (n + 64) > smem_cap) grid_nb = 64;
+    const int64_t v_doubles = grid_nb > 0 ? grid_nb + 4 : n;
     const size_t smem =
-        sizeof(double) * static_cast<size_t>(std::max<int64_t>({n, bk::trailing_smem_doubles(grid_nb), 32 * 33}));
+        sizeof(double) * static_cast<size_t>(std::max<int64_t>({v_doubles, bk::trailing_smem_doubles(grid_nb), 32 * 33}));
     CK(cudaFuncSetAttribute(bk::bk_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bk::bk_factor_kernel, bk::kThreads, smem));
     if (per_sm < 1) throw DeviceError("ldlt_factor: the Bunch-Kaufman kernel does not fit on an SM");

@@ -444,7 +444,11 @@ __device__ void trailing_update(const Factor& F, int k0, int k1, double* sm) {
 
 __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
   extern __shared__ double smem[];
-  double* v = smem;               // [n]
+  // v = W(row, panel) for the column updates.  Blocked mode (F.nb > 0): only
+  // the panel's columns [k0 & ~1, k) are live, so v is panel-relative (its
+  // base shifted by k0 & ~1; the functions index it by absolute column) and
+  // shared memory no longer grows with n -- no size limit on n.  Unblocked
+  // mode: absolute, [n].
   __shared__ double sv[kWarps];
   __shared__ int si[kWarps];
   cg::grid_group grid = cg::this_grid();
@@ -496,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 2) bk_factor_kernel(Factor F) {
     c_mark = t;
   };
   for (int k = 0; k < n;) {
+    double* const v = F.nb > 0 ? smem - (k0 & ~1) : smem;
     double* const wk = cur ? F.w2 : F.w;
     double* const pk = cur ? F.part3 : F.part;
     if (!pre) {

@@ -268,6 +268,9 @@ int DeviceNet::syrk_split(int points, int k_blocks) const {
 // the grid would not cover two waves).
 DeviceNet::AdjLayout DeviceNet::adj_layout(const DevLayer& d, bool multi) const {
   AdjLayout a;
+  // (tried in round 2: a 10-vector pass for m = 10 instead of 12 with two
+  // dead vectors, and 4 columns per thread with 64-row chunks for c2's J --
+  // both slower, 72 -> 90 us per 5120^2 layer; profiles/r02_notes.md)
   a.kw = multi && ceil_div(d.cols, 4 * dev::kAdjThreads) * ceil_div(d.rows, dev::kAdjRows) >= 2 * sm_count_ ? 4 : 2;
   a.gx = static_cast<int>(ceil_div(d.cols, a.kw * dev::kAdjThreads));
   a.crows = dev::kAdjRows;
@@ -473,15 +476,20 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
   ensure_workspace(nb);
   Workspace& w = ws_;
   Outputs o;
-  o.y = w.y_out;
-  o.j = w.j_out;
-  o.h = w.h_out;
+  // GBOPT_PROFILE_OUTPUTS = "yjh" subset (default all three): which outputs
+  // the profiled evaluation computes, e.g. "j" for the reverse-mode Jacobian
+  const char* mask = std::getenv("GBOPT_PROFILE_OUTPUTS");
+  const std::string ms(mask ? mask : "yjh");
+  o.y = ms.find('y') != std::string::npos ? w.y_out : nullptr;
+  o.j = ms.find('j') != std::string::npos ? w.j_out : nullptr;
+  o.h = ms.find('h') != std::string::npos ? w.h_out : nullptr;
   prepare(nb, o);
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy2DAsync(w.x, sizeof(double) * w.ld_in, dx, sizeof(double) * n_, sizeof(double) * n_, nb,
                        cudaMemcpyDeviceToDevice, stream_));
-  CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, dlam, sizeof(double) * m_, sizeof(double) * m_, nb,
-                       cudaMemcpyDeviceToDevice, stream_));
+  if (dlam)
+    CK(cudaMemcpy2DAsync(w.lam, sizeof(double) * w.ld_lam, dlam, sizeof(double) * m_, sizeof(double) * m_, nb,
+                         cudaMemcpyDeviceToDevice, stream_));
   profiling_ = true;
   prof_timeline_ = timeline;
   prof_.clear();
@@ -718,6 +726,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
           if (kw == 4) GBB_ADJ(16, 4); else GBB_ADJ(16, 2);
         } else if (pass == 12) {
           if (kw == 4) GBB_ADJ(12, 4); else GBB_ADJ(12, 2);
+
         } else if (pass == 8) {
           if (kw == 4) GBB_ADJ(8, 4); else GBB_ADJ(8, 2);
         } else if (pass == 4) {
