@@ -34,6 +34,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace gbb {
 namespace dev {
 
@@ -197,6 +199,9 @@ struct NtParams {
   double* c2;
   const double* c2_scale;
   int64_t c2_scale_stride;
+  // > 0: number of tiles when the grid is capped below it (persistent CTAs
+  // walk tile ids blockIdx.x + j * gridDim.x); 0: one tile per CTA
+  int total_tiles;
 };
 
 // Grouped rasterisation of a dense tile grid: kGroupM consecutive M tiles
@@ -255,7 +260,7 @@ constexpr int kNtAcc = kMI * kNJ;
 template <int MI, int NJ, int SET = kBlkAll, bool SCALED = true>
 __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char* smem, uint64_t* full,
                                             uint64_t* empty, int nkb, int kb_begin, const double* sp, int ra,
-                                            int rb, int t, int lane, int b_off = kABytes) {
+                                            int rb, int t, int lane, int b_off, int g0) {
   if (!SCALED) sp = nullptr;
   double sc_next[4];
   if (sp && nkb > 0) {
@@ -263,7 +268,10 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
     for (int q = 0; q < 4; ++q) sc_next[q] = __ldg(sp + kb_begin * kBK + 4 * q + t);
   }
   for (int i = 0; i < nkb; ++i) {
-    const int s = i % kStages;
+    // the smem ring runs on across the tiles of a persistent CTA: stage and
+    // phase follow the CTA's global k-block count g0 + i
+    const int g = g0 + i;
+    const int s = g % kStages;
     double sc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) sc[q] = sp ? sc_next[q] : 1.0;
@@ -271,7 +279,7 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
 #pragma unroll
       for (int q = 0; q < 4; ++q) sc_next[q] = __ldg(sp + (kb_begin + i + 1) * kBK + 4 * q + t);
     }
-    mbar_wait(&full[s], (i / kStages) & 1);
+    mbar_wait(&full[s], (g / kStages) & 1);
     const char* sa = smem + s * kStageBytes;
     const char* sb = sa + b_off;
 #pragma unroll
@@ -299,12 +307,12 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
 // Epilogue of one warp's MI x NJ blocks (first mi_n block rows live).
 // Tile-relative rows r0 + 8 mi (+ pg), columns c0 + 8 nj (+ pc0 / pc1).
 template <int MI, int NJ, int SET = kBlkAll>
-__device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const NtParams& p, int split_idx, int point,
-                                         int tm, int tn, int tile_n, int r0, int c0, int mi_n, int pg, int pc0,
-                                         int pc1) {
+__device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const NtParams& p, int tile, int split_idx,
+                                         int point, int tm, int tn, int tile_n, int r0, int c0, int mi_n, int pg,
+                                         int pc0, int pc1) {
   if (p.mode == kPartial) {
     double* out = p.partial + ((static_cast<int64_t>(split_idx) * p.points * p.n_tiles +
-                                static_cast<int64_t>(blockIdx.x / p.split)) *
+                                static_cast<int64_t>(tile / p.split)) *
                                kBM * kBN);
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
@@ -348,12 +356,67 @@ __device__ __forceinline__ void nt_store(const double (&acc)[kNtAcc][2], const N
   }
 }
 
+// One tile of an nt_mma launch: split-K slice, point, tile coordinates and
+// the k-block range (a plain function: a lambda capturing the kernel
+// parameters by reference forced them into local memory).
+struct NtTile {
+  int split_idx, point, tm, tn, kb_begin, nkb, a_row0, b_row0;
+  bool diag;
+};
+__device__ __forceinline__ NtTile nt_decode(const NtParams& p, int tile, bool sq, int tile_n) {
+  NtTile T;
+  int bid = tile;
+  T.split_idx = bid % p.split;
+  bid /= p.split;
+  if (p.tiles != nullptr) {
+    T.point = bid / p.n_tiles;
+    const int2 tt = p.tiles[bid % p.n_tiles];
+    T.tm = tt.x;
+    T.tn = tt.y;
+  } else {
+    const int per_point = p.tiles_m * p.tiles_n;
+    T.point = bid / per_point;
+    decode_dense_tile(bid % per_point, p.tiles_m, p.tiles_n, T.tm, T.tn);
+  }
+  T.kb_begin = static_cast<int>((static_cast<int64_t>(p.k_blocks) * T.split_idx) / p.split);
+  const int kb_end = static_cast<int>((static_cast<int64_t>(p.k_blocks) * (T.split_idx + 1)) / p.split);
+  T.nkb = kb_end - T.kb_begin;
+  T.a_row0 = static_cast<int>(p.a_point_rows * T.point) + T.tm * kBM;
+  T.b_row0 = static_cast<int>(p.b_point_rows * T.point) + T.tn * tile_n;
+  T.diag = sq && T.tm == T.tn && p.a_point_rows == p.b_point_rows;
+  return T;
+}
+
+// The consumer side of dense GEMM tiles, looping over this CTA's tiles
+// (persistent launches) with the smem ring position carried across tiles.
+template <bool kScaled>
+__device__ __forceinline__ void nt_dense_tiles(const NtParams& p, const char* smem, uint64_t* full, uint64_t* empty,
+                                               int total, int tile_n, int ra, int rb, int r0, int c0, int pg, int pc0,
+                                               int pc1, int t, int lane) {
+  int gk = 0;  // k-blocks consumed so far by this CTA (ring position)
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const NtTile T = nt_decode(p, tile, false, tile_n);
+    double acc[kNtAcc][2];
+#pragma unroll
+    for (int i = 0; i < kNtAcc; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const double* sp = kScaled ? p.scale + p.s_stride * T.point : nullptr;
+    nt_mainloop<kMI, kNJ, kBlkAll, kScaled>(acc, smem, full, empty, T.nkb, T.kb_begin, sp, ra, rb, t, lane, kABytes,
+                                            gk);
+    nt_store<kMI, kNJ>(acc, p, tile, T.split_idx, T.point, T.tm, T.tn, tile_n, r0, c0, kMI, pg, pc0, pc1);
+    gk += T.nkb;
+  }
+}
+
 // Square SYRK tiles (p.square): the tile is 112 x 112 (B rows tn * 112, a
 // 112-row B box) over the lower triangle -- 87.6% useful work at n = 784
 // against 76.7% for 112 x 128 tiles.  SM sub-partition q = warp & 3 owns the
 // 56 x 56 quadrant q, split between its two warps as 25 + 24 of its 7 x 7
 // blocks (blk_live), so each sub-partition's DMMA pipe gets 49 blocks.
-__global__ void __launch_bounds__(kThreads, 1)
+// (register cap instead of __launch_bounds__(kThreads, 1): with the persistent
+// tile loop ptxas capped itself at 168 registers and spilled; 185 fit, one CTA
+// per SM either way -- shared memory decides that)
+__global__ void __maxnreg__(216)
+   
     nt_mma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const NtParams p) {
   extern __shared__ unsigned char smem_raw[];
@@ -368,28 +431,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool sq = p.square != 0;
   const int tile_n = sq ? kBM : kBN;
 
-  // ---- decode tile ----
-  int bid = blockIdx.x;
-  const int split_idx = bid % p.split;
-  bid /= p.split;
-  int point, tm, tn;
-  if (p.tiles != nullptr) {
-    point = bid / p.n_tiles;
-    const int2 t = p.tiles[bid % p.n_tiles];
-    tm = t.x;
-    tn = t.y;
-  } else {
-    const int per_point = p.tiles_m * p.tiles_n;
-    point = bid / per_point;
-    decode_dense_tile(bid % per_point, p.tiles_m, p.tiles_n, tm, tn);
-  }
-  const int kb_begin = static_cast<int>((static_cast<int64_t>(p.k_blocks) * split_idx) / p.split);
-  const int kb_end = static_cast<int>((static_cast<int64_t>(p.k_blocks) * (split_idx + 1)) / p.split);
-  const int nkb = kb_end - kb_begin;
-
-  const int a_row0 = static_cast<int>(p.a_point_rows * point) + tm * kBM;
-  const int b_row0 = static_cast<int>(p.b_point_rows * point) + tn * tile_n;
-  const bool diag = sq && tm == tn && p.a_point_rows == p.b_point_rows;
+  // ---- tile decode: the CTA walks tiles blockIdx.x, + gridDim.x, ... (one
+  // tile when the launch has a CTA per tile; persistent when the grid is
+  // capped at the SM count, so the producer streams the next tile's k-blocks
+  // into the ring while the consumers run the current tile's epilogue) ----
+  const int total = p.total_tiles > 0 ? p.total_tiles : static_cast<int>(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -405,17 +451,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
-      // diagonal square SYRK tiles: B == A, one box per stage
-      const uint32_t bytes = diag ? kABytes : kABytes + (sq ? kABytes : kBBytes);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % kStages;
-        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) - 1) & 1);
-        char* sa = smem + s * kStageBytes;
-        char* sb = sa + kABytes;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        const int kc = (kb_begin + i) * kBK;
-        tma_load_2d(sa, &tmA, &full[s], kc, a_row0);
-        if (!diag) tma_load_2d(sb, &tmB, &full[s], kc, b_row0);
+      int gk = 0;  // k-blocks issued so far by this CTA (ring position)
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const NtTile T = nt_decode(p, tile, sq, tile_n);
+        // diagonal square SYRK tiles: B == A, one box per stage
+        const uint32_t bytes = T.diag ? kABytes : kABytes + (sq ? kABytes : kBBytes);
+        for (int i = 0; i < T.nkb; ++i, ++gk) {
+          const int s = gk % kStages;
+          if (gk >= kStages) mbar_wait(&empty[s], ((gk / kStages) - 1) & 1);
+          char* sa = smem + s * kStageBytes;
+          char* sb = sa + kABytes;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          const int kc = (T.kb_begin + i) * kBK;
+          tma_load_2d(sa, &tmA, &full[s], kc, T.a_row0);
+          if (!T.diag) tma_load_2d(sb, &tmB, &full[s], kc, T.b_row0);
+        }
       }
     }
     return;
@@ -424,57 +474,69 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ===== consumer warps =====
   const int g = lane >> 2;  // DMMA group (row of A / col of B)
   const int t = lane & 3;   // thread in group (k)
-  double acc[kNtAcc][2];
-#pragma unroll
-  for (int i = 0; i < kNtAcc; ++i) acc[i][0] = acc[i][1] = 0.0;
-  const double* sp = p.scale ? p.scale + p.s_stride * point : nullptr;
   // DMMA group g reads smem row 8*blk + row_perm(g): with the TMA 128B
   // swizzle this makes each half-warp's 16 LDS.64 hit 32 distinct banks
   // (identity order gives 2-way conflicts).  C inherits the permutation.
   const int pg = row_perm(g);
   const int pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
-  if (diag) {
-    // block rows [diag_r0(w), diag_r1(w)), columns 0 .. row (B fragments from the A box)
-#define GBB_DIAG_WARP(W)                                                                                  \
-  case W: {                                                                                               \
-    constexpr int R0 = diag_r0(W), R1 = diag_r1(W);                                                       \
-    nt_mainloop<R1 - R0, R1, kBlkLower + R0>(acc, smem, full, empty, nkb, kb_begin, sp, 8 * R0 + pg, pg, t, \
-                                            lane, 0);                                                     \
-    nt_store<R1 - R0, R1, kBlkLower + R0>(acc, p, split_idx, point, tm, tn, tile_n, 8 * R0, 0, R1 - R0, pg, \
-                                         pc0, pc1);                                                       \
-    break;                                                                                                \
-  }
-    switch (warp) {
-      GBB_DIAG_WARP(0)
-      GBB_DIAG_WARP(1)
-      GBB_DIAG_WARP(2)
-      GBB_DIAG_WARP(3)
-      GBB_DIAG_WARP(4)
-      GBB_DIAG_WARP(5)
-      GBB_DIAG_WARP(6)
-      GBB_DIAG_WARP(7)
-      default: break;
-    }
-#undef GBB_DIAG_WARP
-  } else if (sq) {
-    const int q = warp & 3, h = warp >> 2;
-    const int r0 = (q >> 1) * 56 + h * 24, c0 = (q & 1) * 56;
-    if (h == 0) {
-      nt_mainloop<4, 7, kBlkSqLo>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
-      nt_store<4, 7, kBlkSqLo>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
-    } else {
-      nt_mainloop<4, 7, kBlkSqHi>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
-      nt_store<4, 7, kBlkSqHi>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
-    }
-  } else {
+  if (!sq) {
+    // dense GEMM tiles: the persistent loop (one code path per launch, so the
+    // accumulators keep one register assignment across the loop)
     const int wm = warp >> 2;  // 0..1
     const int wn = warp & 3;   // 0..3
     const int r0 = wm * kWarpM, c0 = wn * kWarpN;
-    if (sp)
-      nt_mainloop<kMI, kNJ, kBlkAll, true>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
+    if (p.scale)
+      nt_dense_tiles<true>(p, smem, full, empty, total, tile_n, r0 + pg, c0 + pg, r0, c0, pg, pc0, pc1, t, lane);
     else
-      nt_mainloop<kMI, kNJ, kBlkAll, false>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane);
-    nt_store<kMI, kNJ>(acc, p, split_idx, point, tm, tn, tile_n, r0, c0, kMI, pg, pc0, pc1);
+      nt_dense_tiles<false>(p, smem, full, empty, total, tile_n, r0 + pg, c0 + pg, r0, c0, pg, pc0, pc1, t, lane);
+    return;
+  }
+  // square SYRK tiles: one tile per CTA (the host does not cap these grids)
+  {
+    const int tile = blockIdx.x;
+    const int gk = 0;
+    const NtTile T = nt_decode(p, tile, sq, tile_n);
+    const int split_idx = T.split_idx, point = T.point, tm = T.tm, tn = T.tn, nkb = T.nkb, kb_begin = T.kb_begin;
+    double acc[kNtAcc][2];
+#pragma unroll
+    for (int i = 0; i < kNtAcc; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const double* sp = p.scale ? p.scale + p.s_stride * point : nullptr;
+    if (T.diag) {
+      // block rows [diag_r0(w), diag_r1(w)), columns 0 .. row (B fragments from the A box)
+#define GBB_DIAG_WARP(W)                                                                                     \
+  case W: {                                                                                                  \
+    constexpr int R0 = diag_r0(W), R1 = diag_r1(W);                                                          \
+    nt_mainloop<R1 - R0, R1, kBlkLower + R0>(acc, smem, full, empty, nkb, kb_begin, sp, 8 * R0 + pg, pg, t,    \
+                                            lane, 0, gk);                                                    \
+    nt_store<R1 - R0, R1, kBlkLower + R0>(acc, p, tile, split_idx, point, tm, tn, tile_n, 8 * R0, 0, R1 - R0, \
+                                         pg, pc0, pc1);                                                      \
+    break;                                                                                                   \
+  }
+      switch (warp) {
+        GBB_DIAG_WARP(0)
+        GBB_DIAG_WARP(1)
+        GBB_DIAG_WARP(2)
+        GBB_DIAG_WARP(3)
+        GBB_DIAG_WARP(4)
+        GBB_DIAG_WARP(5)
+        GBB_DIAG_WARP(6)
+        GBB_DIAG_WARP(7)
+        default: break;
+      }
+#undef GBB_DIAG_WARP
+    } else {
+      const int q = warp & 3, h = warp >> 2;
+      const int r0 = (q >> 1) * 56 + h * 24, c0 = (q & 1) * 56;
+      if (h == 0) {
+        nt_mainloop<4, 7, kBlkSqLo>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane, kABytes,
+                                    gk);
+        nt_store<4, 7, kBlkSqLo>(acc, p, tile, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
+      } else {
+        nt_mainloop<4, 7, kBlkSqHi>(acc, smem, full, empty, nkb, kb_begin, sp, r0 + pg, c0 + pg, t, lane, kABytes,
+                                    gk);
+        nt_store<4, 7, kBlkSqHi>(acc, p, tile, split_idx, point, tm, tn, tile_n, r0, c0, 4, pg, pc0, pc1);
+      }
+    }
   }
 }
 

@@ -446,9 +446,22 @@ void DeviceNet::batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const
 // --------------------------------------------------------------------------
 // Launch helpers
 // --------------------------------------------------------------------------
+// nt_mma launches of more tiles than SMs run persistent (GBOPT_NT_PERSIST=1):
+// one CTA per SM walks its tiles, so the producer streams the next tile's
+// k-blocks while the consumers store the current one.
 void DeviceNet::launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p,
                           int grid) {
-  dev::nt_mma_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
+  static const int persist = [] {
+    const char* e = std::getenv("GBOPT_NT_PERSIST");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (persist > 0 && grid > sm_count_) {
+    dev::NtParams q = p;
+    q.total_tiles = grid;
+    dev::nt_mma_kernel<<<sm_count_ * persist, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, q);
+  } else {
+    dev::nt_mma_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
+  }
   after_launch(st);
 }
 
