@@ -412,10 +412,9 @@ __device__ __forceinline__ void nt_dense_tiles(const NtParams& p, const char* sm
 // against 76.7% for 112 x 128 tiles.  SM sub-partition q = warp & 3 owns the
 // 56 x 56 quadrant q, split between its two warps as 25 + 24 of its 7 x 7
 // blocks (blk_live), so each sub-partition's DMMA pipe gets 49 blocks.
-// (register cap instead of __launch_bounds__(kThreads, 1): with the persistent
-// tile loop ptxas capped itself at 168 registers and spilled; 185 fit, one CTA
-// per SM either way -- shared memory decides that)
-__global__ void __maxnreg__(216)
+// (168 registers is the real cap: the 9-warp CTA puts 3 warps on one SM
+// sub-partition, 3 x 32 x 168 <= 16384 registers; 185 failed to launch)
+__global__ void __launch_bounds__(kThreads, 1)
    
     nt_mma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const NtParams p) {
