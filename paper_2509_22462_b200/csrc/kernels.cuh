@@ -434,7 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // tile when the launch has a CTA per tile; persistent when the grid is
   // capped at the SM count, so the producer streams the next tile's k-blocks
   // into the ring while the consumers run the current tile's epilogue) ----
-  const int total = p.total_tiles > 0 ? p.total_tiles : static_cast<int>(gridDim.x);
+  // persistent launches (total_tiles > 0) are dense GEMMs only; square SYRK
+  // launches keep one tile per CTA (their consumers below handle one tile)
+  const int total = (p.total_tiles > 0 && !sq) ? p.total_tiles : static_cast<int>(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {

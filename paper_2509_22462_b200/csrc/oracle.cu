@@ -455,7 +455,8 @@ void DeviceNet::launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensor
     const char* e = std::getenv("GBOPT_NT_PERSIST");
     return e ? std::atoi(e) : 0;
   }();
-  if (persist > 0 && grid > sm_count_) {
+  // (dense GEMM tiles only: the square SYRK consumers handle one tile per CTA)
+  if (persist > 0 && grid > sm_count_ && p.square == 0) {
     dev::NtParams q = p;
     q.total_tiles = grid;
     dev::nt_mma_kernel<<<sm_count_ * persist, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, q);
