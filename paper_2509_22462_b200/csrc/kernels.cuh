@@ -389,10 +389,24 @@ __device__ __forceinline__ NtTile nt_decode(const NtParams& p, int tile, bool sq
 
 // The consumer side of dense GEMM tiles, looping over this CTA's tiles
 // (persistent launches) with the smem ring position carried across tiles.
-template <bool kScaled>
+template <bool kScaled, bool kPersist>
 __device__ __forceinline__ void nt_dense_tiles(const NtParams& p, const char* smem, uint64_t* full, uint64_t* empty,
                                                int total, int tile_n, int ra, int rb, int r0, int c0, int pg, int pc0,
                                                int pc1, int t, int lane) {
+  if constexpr (!kPersist) {
+    // one tile per CTA: straight-line code (the loop below costs registers
+    // -- 104 bytes of spills at the 168-register cap -- and 2% on c4)
+    const int tile = blockIdx.x;
+    const NtTile T = nt_decode(p, tile, false, tile_n);
+    double acc[kNtAcc][2];
+#pragma unroll
+    for (int i = 0; i < kNtAcc; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const double* sp = kScaled ? p.scale + p.s_stride * T.point : nullptr;
+    nt_mainloop<kMI, kNJ, kBlkAll, kScaled>(acc, smem, full, empty, T.nkb, T.kb_begin, sp, ra, rb, t, lane, kABytes,
+                                            0);
+    nt_store<kMI, kNJ>(acc, p, tile, T.split_idx, T.point, T.tm, T.tn, tile_n, r0, c0, kMI, pg, pc0, pc1);
+    return;
+  }
   int gk = 0;  // k-blocks consumed so far by this CTA (ring position)
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const NtTile T = nt_decode(p, tile, false, tile_n);
@@ -414,6 +428,7 @@ __device__ __forceinline__ void nt_dense_tiles(const NtParams& p, const char* sm
 // blocks (blk_live), so each sub-partition's DMMA pipe gets 49 blocks.
 // (168 registers is the real cap: the 9-warp CTA puts 3 warps on one SM
 // sub-partition, 3 x 32 x 168 <= 16384 registers; 185 failed to launch)
+template <bool kPersist>
 __global__ void __launch_bounds__(kThreads, 1)
    
     nt_mma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -436,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // into the ring while the consumers run the current tile's epilogue) ----
   // persistent launches (total_tiles > 0) are dense GEMMs only; square SYRK
   // launches keep one tile per CTA (their consumers below handle one tile)
-  const int total = (p.total_tiles > 0 && !sq) ? p.total_tiles : static_cast<int>(gridDim.x);
+  const int total = (kPersist && !sq) ? p.total_tiles : static_cast<int>(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -487,9 +502,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wn = warp & 3;   // 0..3
     const int r0 = wm * kWarpM, c0 = wn * kWarpN;
     if (p.scale)
-      nt_dense_tiles<true>(p, smem, full, empty, total, tile_n, r0 + pg, c0 + pg, r0, c0, pg, pc0, pc1, t, lane);
+      nt_dense_tiles<true, kPersist>(p, smem, full, empty, total, tile_n, r0 + pg, c0 + pg, r0, c0, pg, pc0, pc1, t,
+                                     lane);
     else
-      nt_dense_tiles<false>(p, smem, full, empty, total, tile_n, r0 + pg, c0 + pg, r0, c0, pg, pc0, pc1, t, lane);
+      nt_dense_tiles<false, kPersist>(p, smem, full, empty, total, tile_n, r0 + pg, c0 + pg, r0, c0, pg, pc0, pc1,
+                                      t, lane);
     return;
   }
   // square SYRK tiles: one tile per CTA (the host does not cap these grids)

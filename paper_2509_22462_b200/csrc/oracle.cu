@@ -120,7 +120,8 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaGetDeviceProperties(&prop, ordinal_));
   if (prop.major != 10) throw DeviceError(std::string("gbopt_b200 needs an sm_100 (B200) device, found ") + prop.name);
   sm_count_ = prop.multiProcessorCount;
-  CK(cudaFuncSetAttribute(dev::nt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
+  CK(cudaFuncSetAttribute(dev::nt_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
+  CK(cudaFuncSetAttribute(dev::nt_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDfSmemBytes));
   if (const char* e = std::getenv("GBOPT_DATAFLOW"))
     dataflow_mode_ = e[0] == '0' ? 0 : (e[0] == '-' && e[1] == '2') ? -2 : 1;
@@ -459,9 +460,9 @@ void DeviceNet::launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensor
   if (persist > 0 && grid > sm_count_ && p.square == 0) {
     dev::NtParams q = p;
     q.total_tiles = grid;
-    dev::nt_mma_kernel<<<sm_count_ * persist, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, q);
+    dev::nt_mma_kernel<true><<<sm_count_ * persist, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, q);
   } else {
-    dev::nt_mma_kernel<<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
+    dev::nt_mma_kernel<false><<<grid, dev::kThreads, dev::kSmemBytes, st>>>(ta, tb, p);
   }
   after_launch(st);
 }
