@@ -7,8 +7,8 @@ zero-pivot rules (linalg.cpp:143-157 negligible column -> exact zero pivot;
 :226-229 |d| <= 1e-11 max|SAS| -> zero L column), which decide the inertia
 of numerically rank-deficient KKT matrices -- the case the IPM's inertia
 correction (ipm.cpp:520-557) exists for.  Plus the large-n paths: the
-multi-CTA grid kernel (n ~ 4000) and the cuSOLVER fallback with iterative
-refinement beyond 32768 rows.
+multi-CTA grid kernel (n ~ 4000) and the native grid kernel with iterative
+refinement beyond 32768 rows (cuSOLVER only past the int32 bound, n > 46340).
 """
 import numpy as np
 import pytest
@@ -59,6 +59,14 @@ def cases():
     J = rng.uniform(-1, 1, (m, n))
     J[10:] = J[:10] + 1e-15 * rng.uniform(-1, 1, (10, n))
     out["kkt_dependent_rows"] = np.block([[H, J.T], [J, np.zeros((m, m))]])
+    # [[A, B], [B^T, B^T A^-1 B + E]] with E at 1e-13: rank n1 up to noise,
+    # every row O(1) (Ruiz cannot scale the deficiency away), so the last
+    # pivots are noise-level Schur-complement entries -- the reference takes
+    # zero pivots there (linalg.cpp:143-157, 226-229) instead of 2x2 blocks
+    A = sym(rng, 30) + 4 * np.eye(30)
+    B = rng.uniform(-1, 1, (30, 6))
+    S = B.T @ np.linalg.solve(A, B)
+    out["schur_noise"] = np.block([[A, B], [B.T, 0.5 * (S + S.T) + 1e-13 * sym(rng, 6)]])
     return out
 
 
@@ -106,8 +114,9 @@ def test_multi_cta_grid_kernel_n4000_matches_reference():
 
 
 def test_beyond_32768_rows_refined_solve():
-    """n = 33000: the cuSOLVER path with the retained input; the refinement
-    residual covers every row (ldlt_residual_kernel strides over rows).  A
+    """n = 33000 (the native grid kernel since round 2; cuSOLVER before):
+    the refinement residual covers every row (ldlt_residual_kernel strides
+    over rows).  A
     saddle point [[D, J^T], [J, 0]] with D > 0 and J of full row rank has
     inertia (n1, m, 0) exactly."""
     import paper_2509_22462_b200 as gb
