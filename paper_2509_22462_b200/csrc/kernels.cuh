@@ -870,7 +870,7 @@ constexpr int kAdjRows = 128;
 // NB shared-memory gz values are reused over KW columns -- the multi-vector
 // sweeps (reverse-mode J: NB = 12 / 16) are otherwise bound by those loads.
 template <int NB, int KW = 2>
-__global__ void __launch_bounds__(kAdjThreads)
+__global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
     adj_cols_kernel(const double* __restrict__ w, int64_t ldw, int rows, int k_dim, const double* __restrict__ gz,
                     int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows) {
   static_assert(KW == 2 || KW == 4, "KW");
@@ -890,15 +890,44 @@ __global__ void __launch_bounds__(kAdjThreads)
 #pragma unroll
     for (int c = 0; c < KW; ++c) a[b][c] = 0.0;
   const double* wp = w + static_cast<int64_t>(r0) * ldw + k;
-#pragma unroll (KW == 2 ? 16 : 8)
-  for (int i = 0; i < nr; ++i) {
+  // kRB rows' weights in flight before their FMAs: the multi-vector sweeps
+  // were latency-bound with the loads interleaved (ncu: 2 CTAs per SM, DFMA
+  // stalled on the loads, 3.0 TB/s).  Each accumulator still takes the rows
+  // in ascending order, so the sums are bit-identical.
+  // (measured, c2: single-vector adjoint 39-47 -> 35-41 us per 5120^2 layer,
+  // 12-vector reverse-mode J 72 -> 60-66 us; 4 rows for NB >= 8 was between)
+  constexpr int kRB = KW == 2 ? 8 : 4;
+  int i = 0;
+  for (; i + kRB <= nr; i += kRB) {
+    double wv[kRB][KW];
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+      const double2 w01 = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i + r) * ldw));
+      wv[r][0] = w01.x;
+      wv[r][1] = w01.y;
+      if constexpr (KW == 4) {
+        // k + 2 < ldw always (ldw is a multiple of 16 and k a multiple of 4);
+        // columns past k_dim are the zero padding
+        const double2 w23 = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i + r) * ldw + 2));
+        wv[r][2] = w23.x;
+        wv[r][3] = w23.y;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRB; ++r)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const double g = gs[b][i + r];
+#pragma unroll
+        for (int c = 0; c < KW; ++c) a[b][c] = fma(wv[r][c], g, a[b][c]);
+      }
+  }
+  for (; i < nr; ++i) {
     double wv[KW];
     const double2 w01 = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw));
     wv[0] = w01.x;
     wv[1] = w01.y;
     if constexpr (KW == 4) {
-      // k + 2 < ldw always (ldw is a multiple of 16 and k a multiple of 4);
-      // columns past k_dim are the zero padding
       const double2 w23 = __ldg(reinterpret_cast<const double2*>(wp + static_cast<int64_t>(i) * ldw + 2));
       wv[2] = w23.x;
       wv[3] = w23.y;
