@@ -43,6 +43,7 @@ struct DevLayer {
   double* w = nullptr;  // [rows][ldw]
   double* b = nullptr;  // [rows]
   CUtensorMap tm_w;     // TMA view of w, box 16 x kBN (B operand)
+  CUtensorMap tm_wadj;  // TMA view of w, 16 x 16 boxes (multi-vector adjoint, adj_mma_kernel)
   double* wt = nullptr;  // W^T [cols][ldwt] (created for batched adjoints)
   int64_t ldwt = 0;
   CUtensorMap tm_wt;
@@ -238,6 +239,7 @@ class DeviceNet {
   // per-layer GEMV graph (c2 165 vs 155 us device time, c5 130 vs 80 us;
   // profiles/r02_fwd_stream.md)
   int fwd_stream_mode_ = 0;
+  bool adj_mma_ = true;  // multi-vector adjoints on DMMA (GBOPT_ADJ_MMA=0: CUDA-core sweeps)
 };
 
 }  // namespace gbb

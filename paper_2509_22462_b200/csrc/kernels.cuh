@@ -949,6 +949,120 @@ __global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-vector adjoint on the FP64 tensor cores (2 <= nv <= 16 vectors, e.g.
+// the m = 10 reverse-mode Jacobian seeds of nn.cpp:148-170):
+//   partial[c][v][k] = sum_{i in row chunk c} gz[v][i] W[i][k]
+// as skinny DMMA GEMMs, M = 16 vectors (two 8-row blocks), N = 128 columns of
+// W per CTA, K = the chunk's rows.  W streams through TMA (8 boxes of 16 x 16
+// doubles, 128B-swizzled, per 16-row stage) into a 6-stage mbarrier ring; the
+// chunk's gz values sit in shared memory.  Each consumer warp owns one 16-
+// column box: per 4-row k-step 2 A fragments (gz), 2 B fragments (W) and 4
+// DMMA.8x8x4.  The CUDA-core version does one shared-memory broadcast and
+// one DFMA per vector per weight pair and is issue-bound at ~3.3 TB/s; here
+// the weight stream is the limit.  The split reduction over chunks is
+// adj_reduce_kernel's, in fixed order.
+// ---------------------------------------------------------------------------
+constexpr int kAmStages = 4;
+constexpr int kAmRows = 256;                 // rows per chunk (K of one CTA)
+constexpr int kAmStageBytes = 8 * 16 * 16 * 8;  // 8 boxes of 16 x 16 doubles = 16 KB
+constexpr int kAmGzPitch = 20;               // gz row pitch (doubles): 2 wavefronts per fragment load
+constexpr int kAmSmem = kAmStages * kAmStageBytes + kAmRows * kAmGzPitch * 8 + 1024 + 2 * kAmStages * 8;
+
+__global__ void __launch_bounds__(288, 2)
+    adj_mma_kernel(const __grid_constant__ CUtensorMap tmW, int rows, int k_dim, const double* __restrict__ gz,
+                   int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows) {
+  extern __shared__ unsigned char am_raw[];
+  char* smem = reinterpret_cast<char*>(am_raw) + ((1024u - (smem_u32(am_raw) & 1023u)) & 1023u);
+  double* gzs = reinterpret_cast<double*>(smem + kAmStages * kAmStageBytes);  // [kAmRows][pitch]
+  uint64_t* full = reinterpret_cast<uint64_t*>(gzs + kAmRows * kAmGzPitch);
+  uint64_t* empty = full + kAmStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * 128;
+  const int r0 = blockIdx.y * crows;  // crows <= kAmRows, a multiple of 16
+  const int nr = min(crows, rows - r0);
+  const int steps = (nr + 15) / 16;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kAmStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp < 8) {
+    // the chunk's gz values, gzs[i][v] (zero past nr or past the vectors),
+    // staged by the consumers while the producer's first TMA loads fly; every
+    // load of a thread in flight before its stores (a load -> store chain per
+    // element made the staging cost more than the chunk's weight stream)
+    constexpr int kPer = kAmRows * 16 / 256;
+    double v8[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * 256 + threadIdx.x;
+      const int i = e >> 4, v = e & 15;
+      v8[u] = (i < nr && p0 + v < nb) ? __ldg(gz + static_cast<int64_t>(p0 + v) * ld_gz + r0 + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * 256 + threadIdx.x;
+      gzs[(e >> 4) * kAmGzPitch + (e & 15)] = v8[u];
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmW);
+      for (int st = 0; st < steps; ++st) {
+        const int s = st % kAmStages;
+        if (st >= kAmStages) mbar_wait(&empty[s], ((st / kAmStages) - 1) & 1);
+        char* dst = smem + s * kAmStageBytes;
+        mbar_arrive_expect_tx(&full[s], kAmStageBytes);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 2048, &tmW, &full[s], n0 + 16 * b, r0 + 16 * st);
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int st = 0; st < steps; ++st) {
+    const int s = st % kAmStages;
+    mbar_wait(&full[s], (st / kAmStages) & 1);
+    const char* box = smem + s * kAmStageBytes + warp * 2048;  // this warp's 16 columns
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int il = 4 * q + t;  // row within the stage (k of the DMMA)
+      const double* gr = gzs + (16 * st + il) * kAmGzPitch;
+      const double a0 = gr[g], a1 = gr[8 + g];
+      const double b0 = lds_swz(box, il, g), b1 = lds_swz(box, il, 8 + g);
+      dmma884(acc[0][0], a0, b0);
+      dmma884(acc[0][1], a0, b1);
+      dmma884(acc[1][0], a1, b0);
+      dmma884(acc[1][1], a1, b1);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // C fragment: thread (g, t) holds C[g][2t], C[g][2t + 1] of each 8 x 8 block
+#pragma unroll
+  for (int mb = 0; mb < 2; ++mb) {
+    const int v = p0 + 8 * mb + g;
+    if (v >= nb) continue;
+    double* o = partial + (static_cast<int64_t>(blockIdx.y) * nb + v) * ld_part;
+#pragma unroll
+    for (int nbk = 0; nbk < 2; ++nbk) {
+      const int k = n0 + 16 * warp + 8 * nbk + 2 * t;
+      if (k < k_dim) o[k] = acc[mb][nbk][0];
+      if (k + 1 < k_dim) o[k + 1] = acc[mb][nbk][1];
+    }
+  }
+}
+
 // ybar[b][k] = sum_c partial[c][b][k] (fixed order), then
 // gz = ybar .* s1 and d = ybar .* s2 for the layer below (nn.cpp:188-193).
 // When s1 == nullptr only ybar is written (the input-gradient).

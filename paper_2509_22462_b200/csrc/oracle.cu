@@ -123,6 +123,8 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::nt_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   CK(cudaFuncSetAttribute(dev::df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDfSmemBytes));
+  CK(cudaFuncSetAttribute(dev::adj_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kAmSmem));
+  if (const char* e = std::getenv("GBOPT_ADJ_MMA")) adj_mma_ = e[0] != '0';
   if (const char* e = std::getenv("GBOPT_DATAFLOW"))
     dataflow_mode_ = e[0] == '0' ? 0 : (e[0] == '-' && e[1] == '2') ? -2 : 1;
   if (const char* e = std::getenv("GBOPT_DF_GROUP")) df_group_ = std::max(1, std::atoi(e));
@@ -175,6 +177,7 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
     CK(cudaMalloc(&d.b, sizeof(double) * d.rows));
     CK(cudaMemcpy(d.b, h.b.data(), sizeof(double) * d.rows, cudaMemcpyHostToDevice));
     d.tm_w = make_tmap(d.w, d.cols, d.rows, d.ldw, kBN);
+    d.tm_wadj = make_tmap(d.w, d.cols, d.rows, d.ldw, 16);
     layers_.push_back(d);
   }
   // T_0 = W_0^T, [n_pad][kp(n_1)], padded rows zero.
@@ -726,9 +729,28 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         continue;
       }
       const AdjLayout al = adj_layout(d, nv >= 5);
-      const int kw = al.kw, gx = al.gx, crows = al.crows, chunks = al.chunks;
+      const int kw = al.kw, gx = al.gx, crows = al.crows;
+      int chunks = al.chunks;
       dim3 grid(gx, chunks);
-      for (int p0 = 0; p0 < nv;) {
+      // 4+ vectors (reverse-mode J seeds, small batches): the DMMA kernel
+      const bool mma = adj_mma_ && nv >= 4 && d.cols >= 128 && d.rows >= 64;
+      if (mma) {
+        // 256-row chunks (smaller chunks for narrow layers measured slower:
+        // c2's 784-column W_1 with 32-row chunks 14.9 -> 18.9 us, its reduce
+        // 8.7 -> 27 us over 5x the partials)
+        int am_rows = dev::kAmRows;
+        while (ceil_div(d.rows, am_rows) > w.adj_chunks_max) am_rows *= 2;  // partial buffer capacity
+        chunks = ceil_div(d.rows, am_rows);
+        const dim3 ga(ceil_div(d.cols, 128), chunks);
+        for (int p0 = 0; p0 < nv; p0 += 16) {
+          prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * std::min(16, nv - p0), 8.0 * d.rows * d.cols);
+          dev::adj_mma_kernel<<<ga, 288, dev::kAmSmem, sb>>>(d.tm_wadj, static_cast<int>(d.rows),
+                                                              static_cast<int>(d.cols), w.gz[l], w.ld[l], nv, p0,
+                                                              w.adj_part, w.ld_part, am_rows);
+          after_launch(sb);
+        }
+      }
+      for (int p0 = 0; p0 < nv && !mma;) {
         const int left = nv - p0;
         // one weight sweep per up to 16 vectors (reverse-mode J: m <= 16
         // seeds per point)
