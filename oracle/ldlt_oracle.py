@@ -117,9 +117,12 @@ def assemble_kkt(x, lower, z, lam, grad_f, g, jac_rows, jac_cols, jac_values, he
     return np.array(mat, dtype=np.float64).reshape(n + m, n + m), np.array(rhs, dtype=np.float64)
 
 
-def inertia_correct(mat, n, m, delta0=1e-4, delta_growth=10.0, delta_max=1e40, delta_w_start=0.0):
-    """ipm.cpp:520-557 with this module's inertia(): returns (delta_w,
+def inertia_correct(mat, n, m, delta0=1e-4, delta_growth=10.0, delta_max=1e40, delta_w_start=0.0,
+                    inertia_fn=None):
+    """ipm.cpp:520-557 with this module's inertia() (or `inertia_fn`, e.g. the
+    reference's own ldlt_factor from oracle/ref.py): returns (delta_w,
     delta_c, inertia) of the first shifted matrix with inertia (n, m, 0)."""
+    inertia_of = inertia_fn or inertia
     delta_w, delta_c = delta_w_start, 0.0
     while True:
         t = np.array(mat, dtype=np.float64, copy=True)
@@ -127,7 +130,7 @@ def inertia_correct(mat, n, m, delta0=1e-4, delta_growth=10.0, delta_max=1e40, d
             t[np.arange(n), np.arange(n)] += delta_w
         if delta_c != 0.0:
             t[n + np.arange(m), n + np.arange(m)] -= delta_c
-        got = inertia(t)
+        got = tuple(inertia_of(t))
         if got == (n, m, 0):
             return delta_w, delta_c, got
         if got[2] > 0 and m > 0 and delta_c < K_DELTA_C_MAX:

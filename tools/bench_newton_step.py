@@ -10,9 +10,11 @@ y (m, free)] -- the shape of the reference's reduced-space formulations
 
 GPU: ReducedSpaceBlock (device oracle) + KktPattern.assemble + inertia_correct
 + KktSystem.solve, the matrix never leaving the device.
-CPU: the reference path on the oracle port -- three callbacks each
-recomputing the forward pass, numpy assembly from the triplets, the oracle's
-LDL^T inertia (Ruiz + LAPACK sytrf) and a LAPACK solve, all host threads.
+CPU: the reference path on the reference's own code -- three callbacks each
+recomputing the forward pass (nn.cpp, oracle/_ref; softplus configs timed
+with tanh hidden layers, nn.cpp has none), numpy assembly from the triplets,
+the inertia-correction loop (ipm.cpp:520-557) over the reference's
+ldlt_factor (linalg.cpp) and its refined solve, all host threads.
 
 python tools/bench_newton_step.py [config] [iters]"""
 import json
@@ -26,8 +28,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_22462_b200 as gb  # noqa: E402
 from paper_2509_22462_b200 import configs  # noqa: E402
 from paper_2509_22462_b200.reduced_space import ReducedSpaceBlock  # noqa: E402
-from oracle import gbopt_oracle as orc  # noqa: E402
 from oracle import ldlt_oracle as lo  # noqa: E402
+from oracle import ref as rf  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
@@ -86,7 +88,8 @@ t = time.perf_counter()
 s.solve(cf.fact)
 ph["solve"] = time.perf_counter() - t
 
-ref = orc.NeuralNet([orc.Layer(*net.layer(l)) for l in range(net.layer_count)])
+rf.set_threads(os.cpu_count() or 1)
+ref = rf.make_config(name, batch=1, hidden=rf.TANH if name in ("c2", "c3") else None).net()
 cpu_iters = max(1, min(iters, 2))
 t0 = time.perf_counter()
 for xb, lam, zin, mu in pts[:cpu_iters]:
@@ -105,10 +108,10 @@ for xb, lam, zin, mu in pts[:cpu_iters]:
     K[:n, n:] = Jf.T
     rhs = np.r_[-xb - Jf.T @ lam, -r]
     rhs[:nin] += mu / (x - lower[:nin])
-    dw, dc, _ = lo.inertia_correct(K, n, m)            # ipm.cpp:520-557
-    np.linalg.solve(K + np.diag(np.r_[np.full(n, dw), np.full(m, -dc)]), rhs)
+    dw, dc, _ = lo.inertia_correct(K, n, m, inertia_fn=lambda A: rf.RefLdlt(A, keep_input=False).inertia)
+    rf.RefLdlt(K + np.diag(np.r_[np.full(n, dw), np.full(m, -dc)])).solve(rhs)   # ipm.cpp:298-302
 cpu_s = (time.perf_counter() - t0) / cpu_iters
 print(json.dumps({"config": name, "kkt_dim": n + m, "gpu_s_per_newton_step": gpu_s, "cpu_s_per_newton_step": cpu_s,
-                  "cpu_threads": os.cpu_count(), "speedup": cpu_s / gpu_s, "delta_w_last": cf.delta_w,
+                  "cpu_threads": os.cpu_count(), "cpu": "reference nn.cpp + linalg.cpp (oracle/_ref)", "speedup": cpu_s / gpu_s, "delta_w_last": cf.delta_w,
                   "inertia_last": cf.fact.inertia, "device_evaluations": blk.evaluations,
                   "phases_s_last_step": ph}))

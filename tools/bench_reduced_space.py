@@ -3,8 +3,11 @@ one residual + Jacobian + Lagrangian Hessian at the iterate (the order of
 ipm.cpp:256,278,420) plus `ls` line-search residuals at trial points
 (ipm.cpp:340-355).  GPU: paper_2509_22462_b200.reduced_space.ReducedSpaceBlock
 (cached per x: forward, reverse-mode J, fused H).  CPU: the reference
-callbacks (formulations.cpp:317-340) on the oracle port, each recomputing its
-own forward pass.  python tools/bench_reduced_space.py [config] [iters] [ls]"""
+callbacks (formulations.cpp:317-340) on the reference's own nn.cpp
+(oracle/_ref, OpenBLAS products on all host threads), each recomputing its
+own forward pass; softplus configs (c2, c3) time the same shape with tanh
+hidden layers (nn.cpp has no softplus).
+python tools/bench_reduced_space.py [config] [iters] [ls]"""
 import json
 import os
 import sys
@@ -15,7 +18,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_22462_b200 import configs  # noqa: E402
 from paper_2509_22462_b200.reduced_space import ReducedSpaceBlock  # noqa: E402
-from oracle import gbopt_oracle as orc  # noqa: E402
+from oracle import ref  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 10
@@ -39,17 +42,19 @@ for x, lam, tr in zip(xs, lams, trials):
         blk.residual(t)
 gpu_s = (time.perf_counter() - t0) / iters
 
-ref = orc.NeuralNet([orc.Layer(*net.layer(l)) for l in range(net.layer_count)])
+ref.set_threads(os.cpu_count() or 1)
+rwl = ref.make_config(name, batch=1, hidden=ref.TANH if name in ("c2", "c3") else None)
+rnet = rwl.net()
 cpu_iters = max(1, min(iters, 3))
 t0 = time.perf_counter()
 for x, lam, tr in list(zip(xs, lams, trials))[:cpu_iters]:
     xb = x[:n]
-    x[n:] - ref.forward(xb)
-    ref.jacobian(xb)
-    ref.lagrangian_hessian(xb, -lam)
+    x[n:] - rnet.forward(xb)
+    rnet.jacobian(xb)
+    rnet.lagrangian_hessian(xb, -lam)
     for t in tr:
-        t[n:] - ref.forward(t[:n])
+        t[n:] - rnet.forward(t[:n])
 cpu_s = (time.perf_counter() - t0) / cpu_iters
 print(json.dumps({"config": name, "line_search_residuals": ls, "gpu_s_per_ipm_iter": gpu_s,
-                  "cpu_s_per_ipm_iter": cpu_s, "cpu_threads": os.cpu_count(), "speedup": cpu_s / gpu_s,
+                  "cpu_s_per_ipm_iter": cpu_s, "cpu_threads": os.cpu_count(), "cpu": "reference nn.cpp (oracle/_ref)", "speedup": cpu_s / gpu_s,
                   "device_evaluations": blk.evaluations}))
