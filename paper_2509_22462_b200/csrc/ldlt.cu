@@ -38,6 +38,7 @@
 #include "ldlt_bk.cuh"
 #include "ldlt_bkc.cuh"
 #include "ldlt_bkp.cuh"
+#include "ldlt_bkq.cuh"
 
 namespace gbb {
 
@@ -412,10 +413,13 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     F.eps = f->zero_thresh_;
     F.trace = nullptr;
     CK(cudaMemsetAsync(F.e, 0, sizeof(double) * n, st));
-    // Kernel choice (GBOPT_LDLT_KERNEL = panel | cluster | grid forces one):
+    // Kernel choice (GBOPT_LDLT_KERNEL = panel | cpanel | cluster | grid forces one):
     //   panel   (ldlt_bkp.cuh): blocked; CTA 0 factors nb-column panels in
     //           shared memory, the grid applies rank-nb updates -- n <= 2048
     //           when a panel of nb >= 4 columns fits in shared memory;
+    //   cpanel  (ldlt_bkq.cuh): blocked; an 8-CTA cluster factors each panel,
+    //           a grid launch applies the update + the panel's permutation on
+    //           the FP64 tensor pipe -- the default for 1400 < n <= 9500;
     //   cluster (ldlt_bkc.cuh): the lower triangle in one cluster's shared
     //           memory, one pivot per step;
     //   grid    (ldlt_bk.cuh):  left-looking, every SM, any n <= 20000.
@@ -434,9 +438,114 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
           break;
         }
     }
-    const bool use_panel = pnb > 0 && n <= bkp::kThreads * bkp::kMaxRowsPerThread && (want.empty() || want == "panel");
+    // cpanel (ldlt_bkq.cuh): per panel one 8-CTA cluster launch factors it
+    // (rows spread over the cluster's shared memory), one grid launch applies
+    // the rank-nb update and the panel's permutation on the FP64 tensor pipe
+    // measured crossovers (tools/ldlt_split.py, profiles/r02_ldlt_kernels.md):
+    // panel wins up to n ~ 1400 (1293: 5.69 vs 5.85 ms), cpanel from there
+    // (1687: 7.8 vs 8.9 ms; 4500: 28 vs 40 ms against the grid kernel) to
+    // n ~ 9500 (9000: 94 vs 98 ms; 11250: 168 vs 138 ms)
+    constexpr int64_t kCpanelMinN = 1400, kCpanelMaxN = 9500;
+    const bool cpanel_default = want.empty() && n > kCpanelMinN && n <= kCpanelMaxN;
+    int qnb = 0;
+    if ((want == "cpanel" || cpanel_default) && n <= bkq::kMaxN) {
+      cudaFuncAttributes qa = {};
+      CK(cudaFuncGetAttributes(&qa, bkq::bkq_panel_kernel));
+      const int64_t avail = smem_optin_dev - static_cast<int64_t>(qa.sharedSizeBytes);
+      for (int nb = bkq::kMaxNb; nb >= 4; --nb)
+        if (bkq::smem_bytes(static_cast<int>(n), nb) <= avail) {
+          qnb = nb;
+          break;
+        }
+      if (qnb > 0) {
+        const size_t qsmem = static_cast<size_t>(bkq::smem_bytes(static_cast<int>(n), qnb));
+        CK(cudaFuncSetAttribute(bkq::bkq_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(qsmem)));
+        CK(cudaFuncSetAttribute(bkq::bkq_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bkq::kUpdSmem));
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(bkq::kC);
+        q.blockDim = dim3(bkq::kThreads);
+        q.dynamicSmemBytes = qsmem;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, bkq::bkq_panel_kernel, &q) != cudaSuccess) clusters = 0;
+        cudaGetLastError();
+        if (clusters < 1) qnb = 0;
+      }
+    }
+    const bool use_cpanel = qnb > 0;
+    const bool use_panel = use_cpanel || (pnb > 0 && n <= bkp::kThreads * bkp::kMaxRowsPerThread &&
+                                          ((want.empty() && !cpanel_default) || want == "panel"));
     f->panel_ = use_panel;
-    if (use_panel) {
+    if (use_cpanel) {
+      const size_t qsmem = static_cast<size_t>(bkq::smem_bytes(static_cast<int>(n), qnb));
+      // pan_w | pan_l | the second n x n buffer | orig_a, orig_b, locg, ctl
+      const size_t nn = static_cast<size_t>(n);
+      f->palloc(&f->d_pan_, sizeof(double) * (2 * bkq::kMaxNb * nn + nn * nn + 2 * nn + 8));
+      bkq::Params P;
+      P.a = f->d_fact_;
+      P.lcols = f->d_l_ + static_cast<size_t>(n) * f->ldl_;
+      P.l = f->d_l_;
+      P.ldl = static_cast<int>(f->ldl_);
+      P.d = F.d;
+      P.e = F.e;
+      P.piv = F.piv;
+      P.perm = F.perm;
+      P.pan_w = f->d_pan_;
+      P.pan_l = P.pan_w + bkq::kMaxNb * nn;
+      P.a2 = P.pan_l + bkq::kMaxNb * nn;
+      P.orig_a = reinterpret_cast<int*>(P.a2 + nn * nn);
+      P.orig_b = P.orig_a + nn;
+      P.locg = P.orig_b + nn;
+      P.ctl = P.locg + nn;
+      P.n = static_cast<int>(n);
+      P.nb = qnb;
+      P.eps = f->zero_thresh_;
+      P.trace = nullptr;
+      cudaEvent_t c0 = nullptr, c1 = nullptr;
+      const bool timing = std::getenv("GBOPT_LDLT_TIMING") != nullptr;
+      if (timing) {
+        CK(cudaMalloc(&P.trace, sizeof(long long) * 16));
+        CK(cudaMemset(P.trace, 0, sizeof(long long) * 16));
+        CK(cudaEventCreate(&c0));
+        CK(cudaEventCreate(&c1));
+        CK(cudaEventRecord(c0, st));
+      }
+      // each panel is >= nb - 1 columns wide (a 2x2 block that does not fit
+      // opens the next one); surplus launches return at once (k0 >= n)
+      const int64_t panels = (n + qnb - 2) / (qnb - 1);
+      bkq::bkq_init_kernel<<<blocks_for(n, 256), 256, 0, st>>>(P);
+      CK(cudaGetLastError());
+      for (int64_t pi = 0; pi < panels; ++pi) {
+        double* A = pi & 1 ? P.a2 : P.a;
+        double* A2 = pi & 1 ? P.a : P.a2;
+        const int* orig = pi & 1 ? P.orig_b : P.orig_a;
+        int* orig2 = pi & 1 ? P.orig_a : P.orig_b;
+        bkq::bkq_panel_kernel<<<bkq::kC, bkq::kThreads, qsmem, st>>>(P, A, orig, orig2);
+        bkq::bkq_update_kernel<<<3 * sms, bkq::kUpdThreads, bkq::kUpdSmem, st>>>(P, A, A2);
+      }
+      bkq::bkq_gather_kernel<<<static_cast<int>(std::min<int64_t>(n, 4 * sms)), 256, 0, st>>>(P);
+      CK(cudaGetLastError());
+      if (timing) {
+        CK(cudaEventRecord(c1, st));
+        CK(cudaEventSynchronize(c1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c0, c1));
+        long long tr[16];
+        CK(cudaMemcpy(tr, P.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+        CK(cudaFree(P.trace));
+        std::fprintf(stderr, "ldlt: cpanel update clocks: issue %lld, wait %lld, fma %lld, stores %lld\n", tr[10],
+                     tr[11], tr[12], tr[13]);
+        std::fprintf(stderr,
+                     "ldlt: n %lld cpanel nb %d, %lld panel launches %.3f ms; panel CTA-0 clocks: zs %lld, column %lld, "
+                     "cluster sync %lld, decide %lld, column r %lld, pivot %lld, publish %lld\n",
+                     static_cast<long long>(n), qnb, static_cast<long long>(panels), ms, tr[0], tr[1], tr[2], tr[3],
+                     tr[4], tr[5], tr[6]);
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+      }
+    }
+    if (use_panel && !use_cpanel) {
       const size_t psmem = static_cast<size_t>(bkp::smem_bytes(static_cast<int>(n), pnb));
       CK(cudaFuncSetAttribute(bkp::bkp_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(psmem)));

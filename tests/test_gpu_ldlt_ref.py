@@ -1,8 +1,8 @@
 """f3 LDL^T against the REFERENCE'S OWN linalg.cpp (oracle/_ref, compiled
 unmodified; its doctest suite test_linalg.cpp passes against that build).
 
-The inertia of every native factorisation kernel (blocked panel, one-cluster,
-cooperative grid) must equal the reference's, including the reference's
+The inertia of every native factorisation kernel (blocked panel, cluster
+panel, one-cluster, cooperative grid) must equal the reference's, including the reference's
 zero-pivot rules (linalg.cpp:143-157 negligible column -> exact zero pivot;
 :226-229 |d| <= 1e-11 max|SAS| -> zero L column), which decide the inertia
 of numerically rank-deficient KKT matrices -- the case the IPM's inertia
@@ -74,7 +74,7 @@ CASES = cases()
 
 
 @needs_ref
-@pytest.mark.parametrize("path", ["panel", "cluster", "grid"])
+@pytest.mark.parametrize("path", ["panel", "cpanel", "cluster", "grid"])
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_inertia_equals_reference_linalg(monkeypatch, path, name):
     import paper_2509_22462_b200 as gb
@@ -95,10 +95,14 @@ def test_inertia_equals_reference_linalg(monkeypatch, path, name):
 
 
 @needs_ref
-def test_multi_cta_grid_kernel_n4000_matches_reference():
-    """n = 4000 > the one-CTA-per-SM limit: the default path runs the grid
-    kernel with several CTAs per SM and > 256 partial maxima."""
+@pytest.mark.parametrize("path", ["", "grid"])
+def test_n4000_matches_reference(monkeypatch, path):
+    """n = 4000: the default path (the cluster-panel kernel, ldlt_bkq.cuh:
+    2 rows per thread, compacting updates) and the grid kernel with several
+    CTAs per SM and > 256 partial maxima."""
     import paper_2509_22462_b200 as gb
+    if path:
+        monkeypatch.setenv("GBOPT_LDLT_KERNEL", path)
     rng = np.random.default_rng(4000)
     n, m = 3200, 800
     H = sym(rng, n) + np.diag(10.0 ** rng.uniform(-2, 4, n))
@@ -137,3 +141,25 @@ def test_beyond_32768_rows_refined_solve():
     r = K @ x - b
     assert np.abs(r).max() <= 1e-10 * (np.abs(K).max() * np.abs(x).max() + 1.0)
     assert np.abs(r[-(n1 + m - 32768):]).max() <= 1e-10 * (np.abs(x).max() + 1.0)
+
+
+@needs_ref
+@pytest.mark.parametrize("n1,m,seed", [(1800, 700, 1), (5200, 1800, 2), (7000, 2000, 3)])
+def test_cluster_panel_saddle_point_matches_reference(monkeypatch, n1, m, seed):
+    """The cluster-panel kernel on saddle-point KKT matrices [[H, J^T], [J, 0]]
+    with an indefinite H: most pivots of the constraint block are 2x2 blocks
+    or interchanges with far rows, so each panel displaces rows the next
+    panel's compaction must carry (1, 2 and 3 rows per thread)."""
+    import paper_2509_22462_b200 as gb
+    monkeypatch.setenv("GBOPT_LDLT_KERNEL", "cpanel")
+    rng = np.random.default_rng(seed)
+    H = sym(rng, n1) + np.diag(rng.uniform(-3, 3, n1))
+    J = rng.uniform(-1, 1, (m, n1))
+    K = np.block([[H, J.T], [J, np.zeros((m, m))]])
+    ref.set_threads(16)
+    want = ref.RefLdlt(K).inertia
+    f = gb.ldlt_factor(K)
+    assert f.inertia == want
+    b = rng.uniform(-1, 1, n1 + m)
+    x = f.solve(b)
+    assert np.abs(K @ x - b).max() <= 1e-8 * (np.abs(K).max() * np.abs(x).max() + 1.0)
