@@ -447,38 +447,55 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     // n ~ 9500 (9000: 94 vs 98 ms; 11250: 168 vs 138 ms)
     constexpr int64_t kCpanelMinN = 1400, kCpanelMaxN = 9500;
     const bool cpanel_default = want.empty() && n > kCpanelMinN && n <= kCpanelMaxN;
-    int qnb = 0;
+    int qnb = 0, qctas = 0;
     if ((want == "cpanel" || cpanel_default) && n <= bkq::kMaxN) {
-      cudaFuncAttributes qa = {};
-      CK(cudaFuncGetAttributes(&qa, bkq::bkq_panel_kernel));
-      const int64_t avail = smem_optin_dev - static_cast<int64_t>(qa.sharedSizeBytes);
-      for (int nb = bkq::kMaxNb; nb >= 4; --nb)
-        if (bkq::smem_bytes(static_cast<int>(n), nb) <= avail) {
-          qnb = nb;
-          break;
-        }
-      if (qnb > 0) {
-        const size_t qsmem = static_cast<size_t>(bkq::smem_bytes(static_cast<int>(n), qnb));
-        CK(cudaFuncSetAttribute(bkq::bkq_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(qsmem)));
+      // panel width nb (<= 32) the cluster's shared memory allows, and whether
+      // such a cluster can be resident; 8 CTAs unless GBOPT_LDLT_CPANEL_CTAS=16
+      auto try_ctas = [&](auto kern, int ctas) -> int {
+        cudaFuncAttributes qa = {};
+        if (cudaFuncGetAttributes(&qa, kern) != cudaSuccess) return 0;
+        const int64_t avail = smem_optin_dev - static_cast<int64_t>(qa.sharedSizeBytes);
+        int nb = 0;
+        for (int w = bkq::kMaxNb; w >= 4 && !nb; --w)
+          if (bkq::smem_bytes(static_cast<int>(n), w, ctas) <= avail) nb = w;
+        if (!nb || n > static_cast<int64_t>(ctas) * bkq::kThreads * bkq::kR) return 0;
+        const int qsmem = static_cast<int>(bkq::smem_bytes(static_cast<int>(n), nb, ctas));
+        if (ctas > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+          return 0;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, qsmem) != cudaSuccess) return 0;
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(ctas);
+        q.blockDim = dim3(bkq::kThreads);
+        q.dynamicSmemBytes = static_cast<size_t>(qsmem);
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &q) != cudaSuccess) clusters = 0;
+        return clusters >= 1 ? nb : 0;
+      };
+      const char* env_c = std::getenv("GBOPT_LDLT_CPANEL_CTAS");
+      const int force_c = env_c ? std::atoi(env_c) : 0;
+      if (force_c != 16) {
+        qnb = try_ctas(bkq::bkq_panel_kernel<8>, 8);
+        qctas = qnb ? 8 : 0;
+      }
+      // (16 CTAs measured slower where tried: the wider cluster barrier and
+      // record reads cost more per pivot than nb = 32 saves in update traffic
+      // -- dim 4500 42.0 vs 26.6 ms, 11250 165 vs 168; profiles/r02_ldlt_kernels.md)
+      if (force_c == 16) {
+        const int nb16 = try_ctas(bkq::bkq_panel_kernel<16>, 16);
+        qnb = nb16;
+        qctas = nb16 ? 16 : 0;
+      }
+      cudaGetLastError();
+      if (qnb > 0)
         CK(cudaFuncSetAttribute(bkq::bkq_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 bkq::kUpdSmem));
-        cudaLaunchConfig_t q = {};
-        q.gridDim = dim3(bkq::kC);
-        q.blockDim = dim3(bkq::kThreads);
-        q.dynamicSmemBytes = qsmem;
-        int clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&clusters, bkq::bkq_panel_kernel, &q) != cudaSuccess) clusters = 0;
-        cudaGetLastError();
-        if (clusters < 1) qnb = 0;
-      }
     }
     const bool use_cpanel = qnb > 0;
     const bool use_panel = use_cpanel || (pnb > 0 && n <= bkp::kThreads * bkp::kMaxRowsPerThread &&
                                           ((want.empty() && !cpanel_default) || want == "panel"));
     f->panel_ = use_panel;
     if (use_cpanel) {
-      const size_t qsmem = static_cast<size_t>(bkq::smem_bytes(static_cast<int>(n), qnb));
+      const size_t qsmem = static_cast<size_t>(bkq::smem_bytes(static_cast<int>(n), qnb, qctas));
       // pan_w | pan_l | the second n x n buffer | orig_a, orig_b, locg, ctl
       const size_t nn = static_cast<size_t>(n);
       f->palloc(&f->d_pan_, sizeof(double) * (2 * bkq::kMaxNb * nn + nn * nn + 2 * nn + 8));
@@ -521,7 +538,10 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
         double* A2 = pi & 1 ? P.a : P.a2;
         const int* orig = pi & 1 ? P.orig_b : P.orig_a;
         int* orig2 = pi & 1 ? P.orig_a : P.orig_b;
-        bkq::bkq_panel_kernel<<<bkq::kC, bkq::kThreads, qsmem, st>>>(P, A, orig, orig2);
+        if (qctas == 16)
+          bkq::bkq_panel_kernel<16><<<16, bkq::kThreads, qsmem, st>>>(P, A, orig, orig2);
+        else
+          bkq::bkq_panel_kernel<8><<<8, bkq::kThreads, qsmem, st>>>(P, A, orig, orig2);
         bkq::bkq_update_kernel<<<3 * sms, bkq::kUpdThreads, bkq::kUpdSmem, st>>>(P, A, A2);
       }
       bkq::bkq_gather_kernel<<<static_cast<int>(std::min<int64_t>(n, 4 * sms)), 256, 0, st>>>(P);
@@ -537,9 +557,9 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
         std::fprintf(stderr, "ldlt: cpanel update clocks: issue %lld, wait %lld, fma %lld, stores %lld\n", tr[10],
                      tr[11], tr[12], tr[13]);
         std::fprintf(stderr,
-                     "ldlt: n %lld cpanel nb %d, %lld panel launches %.3f ms; panel CTA-0 clocks: zs %lld, column %lld, "
+                     "ldlt: n %lld cpanel nb %d ctas %d, %lld panel launches %.3f ms; panel CTA-0 clocks: zs %lld, column %lld, "
                      "cluster sync %lld, decide %lld, column r %lld, pivot %lld, publish %lld\n",
-                     static_cast<long long>(n), qnb, static_cast<long long>(panels), ms, tr[0], tr[1], tr[2], tr[3],
+                     static_cast<long long>(n), qnb, qctas, static_cast<long long>(panels), ms, tr[0], tr[1], tr[2], tr[3],
                      tr[4], tr[5], tr[6]);
         cudaEventDestroy(c0);
         cudaEventDestroy(c1);

@@ -43,11 +43,12 @@ namespace bkq {
 
 namespace cg = cooperative_groups;
 
-constexpr int kC = 8;  // CTAs in the panel cluster
+constexpr int kC = 8;    // CTAs in the panel cluster (up to n = 9500) ...
+constexpr int kC16 = 16;  // ... or 16 (non-portable cluster size; larger n: twice the slice room)
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kR = 4;                        // panel rows per thread
-constexpr int kMaxN = kC * kThreads * kR;    // 16384 (16-bit logical index in the key)
+constexpr int kMaxN = kC16 * kThreads * kR;  // 32768 (the key's 16-bit logical index allows 65535)
 constexpr int kMaxNb = 32;
 constexpr int kT = 64;                       // trailing-update tile (kT x kT)
 constexpr int kLdA = kT + 1;                 // its A block's row stride (doubles; odd: column reads)
@@ -77,8 +78,8 @@ struct Params {
 };
 
 // shared-memory bytes of the panel kernel for (n, nb): the W slice
-__host__ __device__ inline int64_t smem_bytes(int n, int nb) {
-  const int64_t lr = (n + kC - 1) / kC;
+__host__ __device__ inline int64_t smem_bytes(int n, int nb, int ctas) {
+  const int64_t lr = (n + ctas - 1) / ctas;
   return 8 * static_cast<int64_t>(nb + 2) * lr + 64;
 }
 // ... and of the update kernel: the A block, L and W staging, loc
@@ -160,16 +161,17 @@ __device__ __forceinline__ void cta_best(unsigned long long key, double val, int
   }
 }
 
-// The cluster's maximum from the kC records (lanes 0..kC-1 of every warp read
+// The cluster's maximum from the kCl records (lanes 0..kCl-1 of every warp read
 // one each, in parallel): its logical index (-1: no candidate), signed value
 // and physical row, plus the diagonal held by CTA `owner`
+template <int kCl>
 __device__ __forceinline__ int cluster_best(cg::cluster_group& cluster, Rec* rec, int owner, double& val, int& phys,
                                             double& diag) {
   const int lane = threadIdx.x & 31;
   unsigned long long key = 0;
   double v = 0.0, dg = 0.0;
   int ph = -1;
-  if (lane < kC) {
+  if (lane < kCl) {
     const Rec* r = cluster.map_shared_rank(rec, lane);
     key = r->key;
     v = r->val;
@@ -178,7 +180,7 @@ __device__ __forceinline__ int cluster_best(cg::cluster_group& cluster, Rec* rec
   }
   diag = __shfl_sync(0xffffffffu, dg, owner);
 #pragma unroll
-  for (int o = kC / 2; o > 0; o >>= 1) {
+  for (int o = kCl / 2; o > 0; o >>= 1) {
     const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
     const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
     const int p2 = __shfl_xor_sync(0xffffffffu, ph, o);
@@ -336,12 +338,13 @@ __device__ void trailing_update(const double* __restrict__ a, double* __restrict
   }
 }
 
-// One panel: cluster 0 (the whole launch, 8 CTAs) factors the nb columns
+// One panel: the cluster (the whole launch, kCl CTAs) factors the nb columns
 // from logical k0 = ctl[0] of the compact storage A (rows mapped to original
 // rows by orig); publishes W / L by storage row, L by original row, loc
 // (locg), the next buffer's orig (orig2) and the final perm entries of the
 // panel, ctl[0] = k0 + width and ctl[1] = width.  No-op once k0 >= n.
-__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
+template <int kCl>
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
     bkq_panel_kernel(Params p, const double* __restrict__ A, const int* __restrict__ orig, int* __restrict__ orig2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long kwk[kWarps];
@@ -359,7 +362,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   const int k0 = __ldcg(p.ctl);
   if (k0 >= n) return;
   const int rank = static_cast<int>(blockIdx.x);  // = cluster rank
-  const int lr = (n + kC - 1) / kC;   // local slice rows
+  const int lr = (n + kCl - 1) / kCl;   // local slice rows
   const int tid = threadIdx.x;
   long long tacc[10] = {};
   long long tlast = clock64();
@@ -376,7 +379,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   // element P of the W column at slot offset `off` in P's owner's slice
   // (generic pointer, DSMEM when remote)
   auto wref = [&](int off, int P) -> const double* {
-    return cluster.map_shared_rank(Wl, P % kC) + off + P / kC;
+    return cluster.map_shared_rank(Wl, P % kCl) + off + P / kCl;
   };
 
   int parity = 0;
@@ -393,7 +396,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
       double arow[kR], anext[kR];
 #pragma unroll
       for (int t = 0; t < kR; ++t) {
-        const int P = (tid + t * kThreads) * kC + rank;
+        const int P = (tid + t * kThreads) * kCl + rank;
         inv_t[t] = P;
         act_t[t] = tid + t * kThreads < lr && P < n && P >= k0;
         anext[t] = act_t[t] ? __ldcg(A + static_cast<int64_t>(k0) * n + P) : 0.0;
@@ -405,7 +408,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
         const int q = loc_of(k, dpos, dval, nd);
 #pragma unroll
         for (int t = 0; t < kR; ++t) {
-          const int P = (tid + t * kThreads) * kC + rank;
+          const int P = (tid + t * kThreads) * kCl + rank;
           arow[t] = q == q_next ? anext[t] : (act_t[t] ? __ldcg(A + static_cast<int64_t>(q) * n + P) : 0.0);
         }
         // 1. zs = D^{-1} W(q, 0:jj) from q's owner
@@ -418,7 +421,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
         q_next = qn;
 #pragma unroll
         for (int t = 0; t < kR; ++t) {
-          const int P = (tid + t * kThreads) * kC + rank;
+          const int P = (tid + t * kThreads) * kCl + rank;
           if (qn >= 0 && act_t[t]) anext[t] = __ldcg(A + static_cast<int64_t>(qn) * n + P);
         }
         // 2. this CTA's entries of the updated column, its (key, value, row) maximum
@@ -428,7 +431,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < kR; ++t) {
           if (!act_t[t]) continue;
-          const int li = tid + t * kThreads, P = li * kC + rank;
+          const int li = tid + t * kThreads, P = li * kCl + rank;
           const double v = arow[t] - panel_dot(Wl, soff, zs, jj, li);
           Wl[soff[jj] + li] = v;
           if (P != q) {
@@ -444,7 +447,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
         // 3. the cluster's maximum and the diagonal, one DSMEM round trip
         double wkr, wkq;  // W(loc[r], k) signed (the column maximum), W(q, k) (the diagonal)
         int pr;           // loc[r]
-        const int r = cluster_best(cluster, &crec[parity][0], q % kC, wkr, pr, wkq);
+        const int r = cluster_best<kCl>(cluster, &crec[parity][0], q % kCl, wkr, pr, wkq);
         const double lambda = fabs(wkr), absakk = fabs(wkq);
         int kind = 0;  // 0: 1x1 at k; 1: 1x1 at r (swap k <-> r); 2: 2x2 (k, r) (swap k+1 <-> r)
         const bool negl = !(fmax(absakk, lambda) > p.eps);  // linalg.cpp:143-157
@@ -455,7 +458,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
           double ar[kR];
 #pragma unroll
           for (int t = 0; t < kR; ++t) {
-            const int P = (tid + t * kThreads) * kC + rank;
+            const int P = (tid + t * kThreads) * kCl + rank;
             ar[t] = act_t[t] ? __ldcg(A + static_cast<int64_t>(pr) * n + P) : 0.0;
           }
           if (tid < jj) zr[tid] = g0[tid] * *wref(soff[tid], pr) + g1[tid] * *wref(soff[pp[tid]], pr);
@@ -466,7 +469,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < kR; ++t) {
             if (!act_t[t]) continue;
-            const int li = tid + t * kThreads, P = li * kC + rank;
+            const int li = tid + t * kThreads, P = li * kCl + rank;
             const double v = ar[t] - panel_dot(Wl, soff, zr, jj, li);
             Wl[soff[jj + 1] + li] = v;
             if (P != pr) {
@@ -479,7 +482,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
           cluster.sync();
           double wsr;
           int pr2;
-          cluster_best(cluster, &crec[parity][1], pr % kC, wsr, pr2, wrr);
+          cluster_best<kCl>(cluster, &crec[parity][1], pr % kCl, wsr, pr2, wrr);
           const double sigma = fabs(wsr);
           if (absakk * sigma >= kAlpha * lambda * lambda)
             kind = 0;
@@ -508,7 +511,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
         // the owners update their rows' registers
 #pragma unroll
         for (int t = 0; t < kR; ++t) {
-          const int P = (tid + t * kThreads) * kC + rank;
+          const int P = (tid + t * kThreads) * kCl + rank;
           if (pa >= 0) {
             if (P == pr) inv_t[t] = a_;
             if (P == pa) inv_t[t] = r;
@@ -564,7 +567,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
       // over [k0, n) and the width
 #pragma unroll
       for (int t = 0; t < kR; ++t) {
-        const int li = tid + t * kThreads, P = li * kC + rank;
+        const int li = tid + t * kThreads, P = li * kCl + rank;
         if (li >= lr || P >= n || P < k0) continue;
         const int o = __ldcg(orig + P);
         for (int c = 0; c < jj; ++c) {
@@ -585,7 +588,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
       cluster.sync();  // the slices are read remotely until here; locg is complete
       // positions [k0, k1) are final (perm); the rest maps the next buffer
       const int k1 = k0 + jj;
-      for (int i = k0 + rank * kThreads + tid; i < n; i += kC * kThreads)
+      for (int i = k0 + rank * kThreads + tid; i < n; i += kCl * kThreads)
         (i < k1 ? p.perm : orig2)[i] = __ldcg(orig + __ldcg(p.locg + i));
       if (rank == 0 && tid == 0) {
         p.ctl[0] = k1;
