@@ -240,6 +240,7 @@ class DeviceNet {
   // profiles/r02_fwd_stream.md)
   int fwd_stream_mode_ = 0;
   bool adj_mma_ = true;  // multi-vector adjoints on DMMA (GBOPT_ADJ_MMA=0: CUDA-core sweeps)
+  bool syrk_fuse_ = true;  // one-tile points: all layers' curvature in one launch (GBOPT_SYRK_FUSE=0: per layer)
 };
 
 }  // namespace gbb

@@ -666,6 +666,96 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int
 }
 
 // ---------------------------------------------------------------------------
+// Per-point Hessian over several K segments in ONE diagonal tile (n <= 112,
+// e.g. the c4 contingencies: n = 108): H_p = sum_s T_s,p^T diag(D_s,p) T_s,p
+// with the hidden layers' K ranges concatenated -- one launch and one store
+// of each point's tile instead of one launch per layer accumulating into H
+// (and no zeroing pass).  Segment s reads its A boxes from tensor map s at
+// row a_point_rows[s] * point (0: the shared T_0 = W_0^T), its per-k scale
+// from scale[s] + s_stride[s] * point.  Same consumers as nt_mma_kernel's
+// diagonal tiles (the block lower triangle, kBlkLower).
+// ---------------------------------------------------------------------------
+constexpr int kMaxSegs = 4;
+struct SyrkSegs {
+  int nseg;
+  int nkb[kMaxSegs];
+  const double* scale[kMaxSegs];
+  int64_t s_stride[kMaxSegs];
+  int64_t a_point_rows[kMaxSegs];
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    nt_syrk_segs_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                        const __grid_constant__ CUtensorMap tm2, const __grid_constant__ CUtensorMap tm3,
+                        const NtParams p, const SyrkSegs sg) {
+  extern __shared__ unsigned char smem_raw[];
+  char* smem = reinterpret_cast<char*>(smem_raw) + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int point = blockIdx.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      int gk = 0;
+      for (int sgi = 0; sgi < sg.nseg; ++sgi) {
+        const CUtensorMap* tm = sgi == 0 ? &tm0 : sgi == 1 ? &tm1 : sgi == 2 ? &tm2 : &tm3;
+        tma_prefetch_desc(tm);
+        const int row0 = static_cast<int>(sg.a_point_rows[sgi] * point);
+        for (int i = 0; i < sg.nkb[sgi]; ++i, ++gk) {
+          const int s = gk % kStages;
+          if (gk >= kStages) mbar_wait(&empty[s], ((gk / kStages) - 1) & 1);
+          char* sa = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], kABytes);
+          tma_load_2d(sa, tm, &full[s], i * kBK, row0);
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int pg = row_perm(g);
+  const int pc0 = row_perm(2 * t), pc1 = row_perm(2 * t + 1);
+  double acc[kNtAcc][2];
+#pragma unroll
+  for (int i = 0; i < kNtAcc; ++i) acc[i][0] = acc[i][1] = 0.0;
+#define GBB_SEG_WARP(W)                                                                                       \
+  case W: {                                                                                                   \
+    constexpr int R0 = diag_r0(W), R1 = diag_r1(W);                                                           \
+    int gk = 0;                                                                                               \
+    for (int sgi = 0; sgi < sg.nseg; ++sgi) {                                                                 \
+      nt_mainloop<R1 - R0, R1, kBlkLower + R0>(acc, smem, full, empty, sg.nkb[sgi], 0,                        \
+                                              sg.scale[sgi] + sg.s_stride[sgi] * point, 8 * R0 + pg, pg, t,   \
+                                              lane, 0, gk);                                                   \
+      gk += sg.nkb[sgi];                                                                                      \
+    }                                                                                                         \
+    nt_store<R1 - R0, R1, kBlkLower + R0>(acc, p, point, 0, point, 0, 0, kBM, 8 * R0, 0, R1 - R0, pg, pc0,    \
+                                         pc1);                                                                \
+    break;                                                                                                    \
+  }
+  switch (warp) {
+    GBB_SEG_WARP(0)
+    GBB_SEG_WARP(1)
+    GBB_SEG_WARP(2)
+    GBB_SEG_WARP(3)
+    GBB_SEG_WARP(4)
+    GBB_SEG_WARP(5)
+    GBB_SEG_WARP(6)
+    GBB_SEG_WARP(7)
+    default: break;
+  }
+#undef GBB_SEG_WARP
+}
+
+// ---------------------------------------------------------------------------
 // Forward GEMV chain: z = W y + b with the activation epilogue.
 // One warp per output row; NB points per pass, y chunk staged in smem.
 // ---------------------------------------------------------------------------

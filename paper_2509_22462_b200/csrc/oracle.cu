@@ -125,6 +125,8 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaFuncSetAttribute(dev::df_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDfSmemBytes));
   CK(cudaFuncSetAttribute(dev::adj_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kAmSmem));
   if (const char* e = std::getenv("GBOPT_ADJ_MMA")) adj_mma_ = e[0] != '0';
+  if (const char* e = std::getenv("GBOPT_SYRK_FUSE")) syrk_fuse_ = e[0] != '0';
+  CK(cudaFuncSetAttribute(dev::nt_syrk_segs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   if (const char* e = std::getenv("GBOPT_DATAFLOW"))
     dataflow_mode_ = e[0] == '0' ? 0 : (e[0] == '-' && e[1] == '2') ? -2 : 1;
   if (const char* e = std::getenv("GBOPT_DF_GROUP")) df_group_ = std::max(1, std::atoi(e));
@@ -828,7 +830,17 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     return;
   }
   // ---- 3. tangent chain + Hessian SYRK ------------------------------------
-  if (want_h) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
+  // One point tile (n <= 112, e.g. c4's contingencies), a batch that fills
+  // the GPU and every tangent resident: all hidden layers' curvature in ONE
+  // multi-segment launch after the last tangent GEMM (nt_syrk_segs_kernel),
+  // storing each point's tile once instead of zeroing H and accumulating a
+  // launch per layer (GBOPT_SYRK_FUSE=0: per layer)
+  int nl_hidden = 0;
+  for (int l = 0; l + 1 < L; ++l) nl_hidden += layers_[static_cast<size_t>(l)].act != kLinear;
+  const bool fuse_syrk = want_h && syrk_fuse_ && square_syrk_ && n_pad_ == kBM && nb >= sm_count_ &&
+                         nl_hidden >= 1 && nl_hidden <= dev::kMaxSegs &&
+                         static_cast<int>(w.t.size()) >= L - 2;
+  if (want_h && !fuse_syrk) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
   const int kfin_layer = L - 1;
   const bool skinny_final = m_ <= dev::kSkMB;
   // T_l lives in: l == 0 -> t0_ (broadcast over points), else ring buffer
@@ -888,7 +900,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   std::vector<cudaEvent_t> syrk_done(static_cast<size_t>(L), nullptr);
   for (int l = 0; l + 1 < L; ++l) {
     // curvature of hidden layer l, on sb once T_l exists (T_0 is constant)
-    if (want_h && layers_[static_cast<size_t>(l)].act != kLinear) {
+    if (want_h && !fuse_syrk && layers_[static_cast<size_t>(l)].act != kLinear) {
       if (l > 0) link(sa, sb);
       syrk(l);
       if (two) {
@@ -982,6 +994,38 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
     prof_begin(sa, kTagGemm, 2.0 * n_ * dn.rows * dn.cols * nb, 0);
     launch_nt(sa, *ta, dn.tm_w, p, nb * p.n_tiles);
+  }
+
+  if (fuse_syrk) {
+    link(sa, sb);  // every tangent T_l exists
+    dev::SyrkSegs sg{};
+    const CUtensorMap* maps[dev::kMaxSegs] = {};
+    double flops = 0.0;
+    for (int l = 0; l + 1 < L; ++l) {
+      const DevLayer& d = layers_[static_cast<size_t>(l)];
+      if (d.act == kLinear) continue;
+      const int s_i = sg.nseg++;
+      maps[s_i] = &tmap_a(l);
+      sg.nkb[s_i] = ceil_div(d.rows, kBK);
+      sg.scale[s_i] = w.d[l];
+      sg.s_stride[s_i] = w.ld[l];
+      sg.a_point_rows[s_i] = t_point_rows(l);
+      flops += static_cast<double>(d.rows) * n_ * (n_ + 1) * nb;
+    }
+    for (int s_i = sg.nseg; s_i < dev::kMaxSegs; ++s_i) maps[s_i] = maps[0];
+    dev::NtParams p{};
+    p.points = nb;
+    p.split = 1;
+    p.b_rows_valid = static_cast<int>(n_);
+    p.m_rows_valid = static_cast<int>(n_);
+    p.c = w.h;
+    p.c_point_stride = n_pad_ * n_pad_;
+    p.ldc = n_pad_;
+    p.mode = dev::kStore;
+    prof_begin(sb, kTagSyrk, flops, 0);
+    dev::nt_syrk_segs_kernel<<<nb, dev::kThreads, dev::kSmemBytes, sb>>>(*maps[0], *maps[1], *maps[2], *maps[3], p,
+                                                                          sg);
+    after_launch(sb);
   }
 
   // ---- 4. final layer -------------------------------------------------------
