@@ -310,3 +310,55 @@ def test_forward_trace_matches_oracle(widths, hid, fin):
     assert np.array_equal(ys[-1], net.forward(x))
     with pytest.raises(gb.ArgumentError):
         net.forward_trace(x[:-1])
+
+
+# one-tile points with a batch that fills the GPU: every hidden layer's
+# curvature in one multi-segment SYRK launch (nt_syrk_segs_kernel) -- up to
+# four nonlinear hidden layers, a linear hidden layer skipped, and five
+# (beyond the segment limit: the per-layer SYRKs)
+SEG_NETS = [
+    ([40, 64, 48, 1], "tanh", "sigmoid", 21),
+    ([30, 32, 32, 32, 32, 2], "sigmoid", "linear", 22),
+    ([30, 32, 32, 32, 32, 32, 2], "softplus", "tanh", 23),
+    ([112, 50, 3], "tanh", "softmax", 24),
+]
+
+
+@pytest.mark.parametrize("widths,hid,fin,seed", SEG_NETS)
+def test_multi_segment_syrk_batches(widths, hid, fin, seed):
+    net = gb.random_net(widths, hid, fin, seed).bind_device(0)
+    ref = to_oracle(net)
+    rng = np.random.default_rng(seed)
+    B = 300  # >= the SM count
+    X = rng.uniform(-1, 1, (B, widths[0]))
+    L = rng.normal(size=(B, widths[-1]))
+    Y, J, H = net.oracle_batched(X, L)
+    for k in (0, 1, 150, B - 1):
+        assert orc.rel_err(Y[k], ref.forward(X[k])) <= TOL
+        assert orc.rel_err(J[k], ref.jacobian(X[k])) <= TOL
+        assert orc.rel_err(H[k], ref.lagrangian_hessian(X[k], L[k])) <= TOL
+        assert np.array_equal(H[k], H[k].T)
+
+
+def test_multi_segment_syrk_matches_per_layer():
+    """The one-launch curvature against the per-layer SYRKs
+    (GBOPT_SYRK_FUSE=0, separate process): same values to rounding."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import json, sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_2509_22462_b200 as gb\n"
+        "net = gb.random_net([40, 64, 48, 1], 'tanh', 'sigmoid', 21).bind_device(0)\n"
+        "rng = np.random.default_rng(5)\n"
+        "X = rng.uniform(-1, 1, (300, 40)); L = rng.normal(size=(300, 1))\n"
+        "print(json.dumps(net.oracle_batched(X, L)[2][::37].tolist()))\n" % root)
+    outs = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, GBOPT_SYRK_FUSE=v))
+        assert r.returncode == 0, r.stderr
+        outs.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
+    assert orc.rel_err(outs[0], outs[1]) <= 1e-13
