@@ -163,3 +163,27 @@ def test_cluster_panel_saddle_point_matches_reference(monkeypatch, n1, m, seed):
     b = rng.uniform(-1, 1, n1 + m)
     x = f.solve(b)
     assert np.abs(K @ x - b).max() <= 1e-8 * (np.abs(K).max() * np.abs(x).max() + 1.0)
+
+
+def test_cluster_panel_four_rows_per_thread_known_inertia(monkeypatch):
+    """n = 16000 through the cluster-panel kernel (forced): 4 rows per thread,
+    nb limited by the slice, several hundred compacting updates.  A saddle
+    point [[D, J^T], [J, 0]] with D > 0 and J of full row rank has inertia
+    (n1, m, 0) exactly, and the refined solve must reach the residual bar."""
+    import paper_2509_22462_b200 as gb
+    monkeypatch.setenv("GBOPT_LDLT_KERNEL", "cpanel")
+    rng = np.random.default_rng(16)
+    n1, m = 15000, 1000
+    K = np.zeros((n1 + m, n1 + m))
+    K[np.arange(n1), np.arange(n1)] = rng.uniform(1.0, 4.0, n1)
+    J = np.zeros((m, n1))
+    for i in range(m):
+        J[i, 15 * i:15 * i + 15] = rng.uniform(0.5, 1.5, 15)
+        J[i, n1 - 1 - i] += 1.0
+    K[n1:, :n1] = J
+    K[:n1, n1:] = J.T
+    f = gb.ldlt_factor(K)
+    assert f.inertia == (n1, m, 0)
+    b = rng.uniform(-1, 1, n1 + m)
+    x = f.solve(b)
+    assert np.abs(K @ x - b).max() <= 1e-10 * (np.abs(K).max() * np.abs(x).max() + 1.0)
