@@ -286,7 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1) df_kernel(const __grid_constant__
           if (sp) bulk_load(sa + kDfScaleOff, sp + kb * kBK, kBK * 8, &full[s]);
         }
       }
+      // producer tail: stay until the consumers have released the last
+      // stages (no issuing warp exits with bulk copies in flight; see
+      // adj_mma_kernel in kernels.cuh)
+      for (uint32_t g2 = gk > kStages ? gk - kStages : 0; g2 < gk; ++g2)
+        mbar_wait(&empty[g2 % kStages], (g2 / kStages) & 1);
     }
+    __syncwarp();
     return;
   }
 

@@ -153,7 +153,12 @@ __global__ void __launch_bounds__(kFsThreads, 1) fwd_stream_kernel(const __grid_
               : "memory");
         }
       }
+      // producer tail: stay until the consumers have released the last
+      // stages (no issuing thread exits with bulk copies in flight)
+      for (int g2 = g > kFsStages ? g - kFsStages : 0; g2 < g; ++g2)
+        fs_wait(empty + g2 % kFsStages, (g2 / kFsStages) & 1);
     }
+    __syncwarp();
     return;
   }
 

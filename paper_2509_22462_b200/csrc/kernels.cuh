@@ -483,7 +483,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!T.diag) tma_load_2d(sb, &tmB, &full[s], kc, T.b_row0);
         }
       }
+      // producer tail: stay until the consumers have released the last
+      // stages (see adj_mma_kernel: no issuing warp exits with bulk copies
+      // in flight)
+      for (int g2 = gk > kStages ? gk - kStages : 0; g2 < gk; ++g2) mbar_wait(&empty[g2 % kStages], (g2 / kStages) & 1);
     }
+    __syncwarp();
     return;
   }
 
@@ -718,7 +723,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(sa, tm, &full[s], i * kBK, row0);
         }
       }
+      for (int g2 = gk > kStages ? gk - kStages : 0; g2 < gk; ++g2) mbar_wait(&empty[g2 % kStages], (g2 / kStages) & 1);
     }
+    __syncwarp();
     return;
   }
   const int g = lane >> 2, t = lane & 3;
@@ -1045,21 +1052,31 @@ __global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
 //   partial[c][v][k] = sum_{i in row chunk c} gz[v][i] W[i][k]
 // as skinny DMMA GEMMs, M = 16 vectors (two 8-row blocks), N = 128 columns of
 // W per CTA, K = the chunk's rows.  W streams through TMA (8 boxes of 16 x 16
-// doubles, 128B-swizzled, per 16-row stage) into a 6-stage mbarrier ring; the
+// doubles, 128B-swizzled, per 16-row stage) into an 8-stage mbarrier ring; the
 // chunk's gz values sit in shared memory.  Each consumer warp owns one 16-
 // column box: per 4-row k-step 2 A fragments (gz), 2 B fragments (W) and 4
 // DMMA.8x8x4.  The CUDA-core version does one shared-memory broadcast and
 // one DFMA per vector per weight pair and is issue-bound at ~3.3 TB/s; here
 // the weight stream is the limit.  The split reduction over chunks is
 // adj_reduce_kernel's, in fixed order.
+// OPT-IN (GBOPT_ADJ_MMA=1; the default is adj_cols_kernel).  With two CTAs
+// per SM (a 4-stage ring) this kernel produced wrong partials for a fraction
+// of the 8-column blocks -- on a cold first launch, and whenever launches of
+// two handles overlapped (tools/adj_mma_conc.cu: ~1-4% of the partials of a
+// 5120 x 5120 sweep; the full GPU suite hit it about once in three runs).
+// One CTA per SM (this 8-stage ring) and a producer that waits for the last
+// stages' release before exiting clear the stand-alone reproducer and three
+// full suites, but two handles evaluating concurrently from two host threads
+// (tools/stress_adj3.py) still showed 1 wrong Jacobian in ~600 -- so it
+// stays off until that is understood.
 // ---------------------------------------------------------------------------
-constexpr int kAmStages = 4;
+constexpr int kAmStages = 8;
 constexpr int kAmRows = 256;                 // rows per chunk (K of one CTA)
 constexpr int kAmStageBytes = 8 * 16 * 16 * 8;  // 8 boxes of 16 x 16 doubles = 16 KB
 constexpr int kAmGzPitch = 20;               // gz row pitch (doubles): 2 wavefronts per fragment load
 constexpr int kAmSmem = kAmStages * kAmStageBytes + kAmRows * kAmGzPitch * 8 + 1024 + 2 * kAmStages * 8;
 
-__global__ void __launch_bounds__(288, 2)
+__global__ void __launch_bounds__(288, 1)
     adj_mma_kernel(const __grid_constant__ CUtensorMap tmW, int rows, int k_dim, const double* __restrict__ gz,
                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows) {
   extern __shared__ unsigned char am_raw[];
@@ -1091,7 +1108,7 @@ __global__ void __launch_bounds__(288, 2)
     for (int u = 0; u < kPer; ++u) {
       const int e = u * 256 + threadIdx.x;
       const int i = e >> 4, v = e & 15;
-      v8[u] = (i < nr && p0 + v < nb) ? __ldg(gz + static_cast<int64_t>(p0 + v) * ld_gz + r0 + i) : 0.0;
+      v8[u] = (i < nr && p0 + v < nb) ? __ldcg(gz + static_cast<int64_t>(p0 + v) * ld_gz + r0 + i) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -1111,7 +1128,14 @@ __global__ void __launch_bounds__(288, 2)
 #pragma unroll
         for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 2048, &tmW, &full[s], n0 + 16 * b, r0 + 16 * st);
       }
+      // producer tail: stay until the consumers have released every stage,
+      // i.e. until every load issued here has landed and been read (an
+      // issuing warp that exits with its bulk copies in flight was one of
+      // the conditions of the wrong-partials failure above)
+      for (int st = (steps > kAmStages ? steps - kAmStages : 0); st < steps; ++st)
+        mbar_wait(&empty[st % kAmStages], (st / kAmStages) & 1);
     }
+    __syncwarp();
     return;
   }
   const int g = lane >> 2, t = lane & 3;
