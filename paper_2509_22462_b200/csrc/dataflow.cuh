@@ -171,8 +171,7 @@ __device__ __forceinline__ void df_mainloop(double (&acc)[kAcc][2], const char* 
         for (int nj = 0; nj < NJ; ++nj)
           if (blk_live<SET>(mi, nj)) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    stage_release(&empty[s], lane);
   }
 }
 

@@ -239,7 +239,7 @@ class DeviceNet {
   // per-layer GEMV graph (c2 165 vs 155 us device time, c5 130 vs 80 us;
   // profiles/r02_fwd_stream.md)
   int fwd_stream_mode_ = 0;
-  bool adj_mma_ = false;  // multi-vector adjoints on DMMA (GBOPT_ADJ_MMA=1; off: a rare wrong-partials race, kernels.cuh)
+  bool adj_mma_ = true;  // multi-vector adjoints on DMMA (GBOPT_ADJ_MMA=0: CUDA-core sweeps)
   bool syrk_fuse_ = true;  // one-tile points: all layers' curvature in one launch (GBOPT_SYRK_FUSE=0: per layer)
 };
 

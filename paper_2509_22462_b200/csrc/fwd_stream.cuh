@@ -254,11 +254,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) fwd_stream_kernel(const __grid_
           if (lane == 0) part[(rr0 + r) * kFsConsumerWarps + warp] += v;
         }
       }
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                         static_cast<uint32_t>(__cvta_generic_to_shared(empty + s)))
-                     : "memory");
+      stage_release(empty + s, lane);  // cross-proxy WAR fence, then arrive (kernels.cuh)
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kFsConsumerWarps * 32) : "memory");
     // epilogue: fixed-order sum of the 8 partials, bias, activation

@@ -125,6 +125,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Consumer release of a TMA-filled stage.  The stage was read with generic
+// loads (LDS -> registers -> DMMA) and the producer's next TMA load writes it
+// through the async proxy: a cross-proxy write-after-read that the mbarrier
+// alone does not order.  Each reading thread fences its reads against the
+// async proxy, then one lane arrives.  (Without the fence the TMA could land
+// before outstanding reads: adj_mma_kernel at 2 CTAs per SM returned wrong
+// partials for ~1-4% of its 8-column blocks, tools/adj_mma_conc.cu.)
+__device__ __forceinline__ void stage_release(uint64_t* empty, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty)) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
@@ -299,8 +311,7 @@ __device__ __forceinline__ void nt_mainloop(double (&acc)[kNtAcc][2], const char
         for (int nj = 0; nj < NJ; ++nj)
           if (blk_live<SET>(mi, nj)) dmma884(acc[mi * NJ + nj], a[mi], b[nj]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    stage_release(&empty[s], lane);
   }
 }
 
@@ -1052,31 +1063,26 @@ __global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
 //   partial[c][v][k] = sum_{i in row chunk c} gz[v][i] W[i][k]
 // as skinny DMMA GEMMs, M = 16 vectors (two 8-row blocks), N = 128 columns of
 // W per CTA, K = the chunk's rows.  W streams through TMA (8 boxes of 16 x 16
-// doubles, 128B-swizzled, per 16-row stage) into an 8-stage mbarrier ring; the
+// doubles, 128B-swizzled, per 16-row stage) into a 4-stage mbarrier ring; the
 // chunk's gz values sit in shared memory.  Each consumer warp owns one 16-
 // column box: per 4-row k-step 2 A fragments (gz), 2 B fragments (W) and 4
 // DMMA.8x8x4.  The CUDA-core version does one shared-memory broadcast and
 // one DFMA per vector per weight pair and is issue-bound at ~3.3 TB/s; here
 // the weight stream is the limit.  The split reduction over chunks is
 // adj_reduce_kernel's, in fixed order.
-// OPT-IN (GBOPT_ADJ_MMA=1; the default is adj_cols_kernel).  With two CTAs
-// per SM (a 4-stage ring) this kernel produced wrong partials for a fraction
-// of the 8-column blocks -- on a cold first launch, and whenever launches of
-// two handles overlapped (tools/adj_mma_conc.cu: ~1-4% of the partials of a
-// 5120 x 5120 sweep; the full GPU suite hit it about once in three runs).
-// One CTA per SM (this 8-stage ring) and a producer that waits for the last
-// stages' release before exiting clear the stand-alone reproducer and three
-// full suites, but two handles evaluating concurrently from two host threads
-// (tools/stress_adj3.py) still showed 1 wrong Jacobian in ~600 -- so it
-// stays off until that is understood.
+// Two CTAs per SM.  The consumers read W from shared memory with generic
+// loads; releasing a stage back to the producer's next TMA write therefore
+// needs the async-proxy fence in stage_release -- without it this kernel
+// returned wrong partials for ~1-4% of its 8-column blocks (cold launches,
+// overlapping handles; tools/adj_mma_conc.cu, profiles/r02_notes.md).
 // ---------------------------------------------------------------------------
-constexpr int kAmStages = 8;
+constexpr int kAmStages = 4;
 constexpr int kAmRows = 256;                 // rows per chunk (K of one CTA)
 constexpr int kAmStageBytes = 8 * 16 * 16 * 8;  // 8 boxes of 16 x 16 doubles = 16 KB
 constexpr int kAmGzPitch = 20;               // gz row pitch (doubles): 2 wavefronts per fragment load
 constexpr int kAmSmem = kAmStages * kAmStageBytes + kAmRows * kAmGzPitch * 8 + 1024 + 2 * kAmStages * 8;
 
-__global__ void __launch_bounds__(288, 1)
+__global__ void __launch_bounds__(288, 2)
     adj_mma_kernel(const __grid_constant__ CUtensorMap tmW, int rows, int k_dim, const double* __restrict__ gz,
                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows) {
   extern __shared__ unsigned char am_raw[];
@@ -1129,9 +1135,7 @@ __global__ void __launch_bounds__(288, 1)
         for (int b = 0; b < 8; ++b) tma_load_2d(dst + b * 2048, &tmW, &full[s], n0 + 16 * b, r0 + 16 * st);
       }
       // producer tail: stay until the consumers have released every stage,
-      // i.e. until every load issued here has landed and been read (an
-      // issuing warp that exits with its bulk copies in flight was one of
-      // the conditions of the wrong-partials failure above)
+      // i.e. until every load issued here has landed and been read
       for (int st = (steps > kAmStages ? steps - kAmStages : 0); st < steps; ++st)
         mbar_wait(&empty[st % kAmStages], (st / kAmStages) & 1);
     }
@@ -1159,8 +1163,7 @@ __global__ void __launch_bounds__(288, 1)
       dmma884(acc[1][0], a1, b0);
       dmma884(acc[1][1], a1, b1);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    stage_release(&empty[s], lane);
   }
   // C fragment: thread (g, t) holds C[g][2t], C[g][2t + 1] of each 8 x 8 block
 #pragma unroll

@@ -15,6 +15,13 @@
 
 using namespace gbb;
 
+// co-resident noise: small CTAs streaming through their own buffer
+__global__ void noise_kernel(double* buf, size_t n, int iters) {
+  for (int it = 0; it < iters; ++it)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+      buf[i] = buf[i] * 0.5 + 1.0;
+}
+
 static CUtensorMap tmap(const double* base, int64_t cols, int64_t rows, int64_t pitch) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -30,6 +37,7 @@ static CUtensorMap tmap(const double* base, int64_t cols, int64_t rows, int64_t 
 
 int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 20;
+  const int noise = argc > 2 ? atoi(argv[2]) : 0;  // 1: a co-resident noise kernel on a third stream
   const int rows = 5120, cols = 5120, nv = 10, crows = dev::kAmRows, chunks = rows / crows;
   const int64_t ld_part = cols;
   cudaFuncSetAttribute(dev::adj_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kAmSmem);
@@ -91,7 +99,13 @@ int main(int argc, char** argv) {
     cudaStreamSynchronize(s[i]);
     bad += check(i, "solo");
   }
+  double* nbuf = nullptr;
+  cudaStream_t s3;
+  cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking);
+  const size_t nn = size_t(64) << 20;
+  if (noise) cudaMalloc(&nbuf, sizeof(double) * nn);
   for (int r = 0; r < reps; ++r) {  // both sets at once, back to back
+    if (noise) noise_kernel<<<148 * 4, 256, 0, s3>>>(nbuf, nn, 4);
     for (int k = 0; k < 4; ++k)
       for (int i = 0; i < 2; ++i)
         dev::adj_mma_kernel<<<grid, 288, dev::kAmSmem, s[i]>>>(tm[i], rows, cols, gz[i], rows, nv, 0, part[i],
