@@ -54,7 +54,7 @@ def test_two_handles_concurrent_reverse_jacobian_bitwise():
     if not has_gpu():
         pytest.skip("no GPU")
     import paper_2509_22462_b200 as gb
-    widths = [784, 2048, 2048, 2048, 10]
+    widths = [784, 5120, 5120, 5120, 10]  # c2-wide layers: 2 DMMA-adjoint CTAs per SM
     x = np.random.default_rng(3).uniform(0, 1, widths[0])
-    bad = _run_two(lambda: gb.random_net(widths, "tanh", "linear", 5).bind_device(0), lambda n: n.jacobian(x), 60)
+    bad = _run_two(lambda: gb.random_net(widths, "tanh", "linear", 5).bind_device(0), lambda n: n.jacobian(x), 150)
     assert not bad, bad
