@@ -99,6 +99,17 @@ __device__ __forceinline__ int loc_of(int i, const int* dpos, const int* dval, i
   return v;
 }
 
+// index of position i in the displaced-position table (nd: not there), one
+// warp-wide probe like loc_of
+__device__ __forceinline__ int loc_slot(int i, const int* dpos, int nd) {
+  const int lane = threadIdx.x & 31;
+  for (int e0 = 0; e0 < nd; e0 += 32) {
+    const unsigned hit = __ballot_sync(0xffffffffu, e0 + lane < nd && dpos[e0 + lane] == i);
+    if (hit) return e0 + __ffs(hit) - 1;
+  }
+  return nd;
+}
+
 __device__ __forceinline__ unsigned long long pack_key(double v, int logical) {
   return (static_cast<unsigned long long>(__double_as_longlong(fabs(v))) & ~0xFFFFull) |
          static_cast<unsigned long long>(0xFFFF - logical);
@@ -496,6 +507,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
         // interchange (logical labels only, replicated in every CTA), retire the pivot rows
         const int a_ = kind == 1 ? k : k + 1;
         const int pa = kind != 0 && a_ != r ? (kind == 1 ? q : loc_of(k + 1, dpos, dval, nd)) : -1;
+        const int e_r = pa >= 0 ? loc_slot(r, dpos, nd) : 0;  // where position r goes in the table
         const int p0 = kind == 1 ? pr : q;
         const int p1 = kind == 2 ? pr : -1;
         const double dk = negl ? 0.0 : (kind == 1 ? wrr : wkq);
@@ -524,11 +536,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kThreads, 1)
           fin[jj] = p0;
           if (kind == 2) fin[jj + 1] = p1;
           if (pa >= 0) {
-            int e = 0;
-            while (e < nd && dpos[e] != r) ++e;
-            dpos[e] = r;
-            dval[e] = pa;
-            if (e == nd) s_nd = nd + 1;
+            dpos[e_r] = r;
+            dval[e_r] = pa;
+            if (e_r == nd) s_nd = nd + 1;
           }
           if (kind == 1) {  // the pivot column is column r: swap the slots, move no data
             const int t = soff[jj];
