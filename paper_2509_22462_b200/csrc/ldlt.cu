@@ -419,7 +419,7 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     //           when a panel of nb >= 4 columns fits in shared memory;
     //   cpanel  (ldlt_bkq.cuh): blocked; an 8-CTA cluster factors each panel,
     //           a grid launch applies the update + the panel's permutation on
-    //           the FP64 tensor pipe -- the default for 1400 < n <= 9500;
+    //           the FP64 tensor pipe -- the default for 2048 < n <= 8500;
     //   cluster (ldlt_bkc.cuh): the lower triangle in one cluster's shared
     //           memory, one pivot per step;
     //   grid    (ldlt_bk.cuh):  left-looking, every SM, any n <= 20000.
@@ -441,11 +441,14 @@ std::unique_ptr<Ldlt> Ldlt::factor_impl(const double* a, bool on_device, int64_t
     // cpanel (ldlt_bkq.cuh): per panel one 8-CTA cluster launch factors it
     // (rows spread over the cluster's shared memory), one grid launch applies
     // the rank-nb update and the panel's permutation on the FP64 tensor pipe
-    // measured crossovers (tools/ldlt_split.py, profiles/r02_ldlt_kernels.md):
-    // panel wins up to n ~ 1400 (1293: 5.69 vs 5.85 ms), cpanel from there
-    // (1687: 7.8 vs 8.9 ms; 4500: 28 vs 40 ms against the grid kernel) to
-    // n ~ 9500 (9000: 94 vs 98 ms; 11250: 168 vs 138 ms)
-    constexpr int64_t kCpanelMinN = 1400, kCpanelMaxN = 9500;
+    // measured crossovers (tools/ldlt_split.py, profiles/r02_ldlt_kernels.md).
+    // The cluster-panel kernel's per-pivot cost follows the box's DSMEM /
+    // cluster-barrier latency (the same build: dim 4500 26.6 ms on one box,
+    // 31.4 on another), the other kernels' does not; the range below wins on
+    // both: the one-CTA panel up to its n = 2048 (1687: 8.9 ms vs cpanel
+    // 7.8 / 9.5), cpanel up to 8500 (4500: 26.6 / 31.4 vs grid 40; 7987: 71 /
+    // 79 vs 83; 9000: 94 / 102 vs 97)
+    constexpr int64_t kCpanelMinN = 2048, kCpanelMaxN = 8500;
     const bool cpanel_default = want.empty() && n > kCpanelMinN && n <= kCpanelMaxN;
     int qnb = 0, qctas = 0;
     if ((want == "cpanel" || cpanel_default) && n <= bkq::kMaxN) {
