@@ -57,6 +57,7 @@ struct Workspace {
   int adj_chunks_max = 0;
   int64_t ld_part = 0;
   double* adj_part = nullptr;
+  unsigned* adj_cnt = nullptr;  // arrival counters of the fused adjoint chunk reduction
   std::vector<double*> t;                   // ring of tangent buffers
   std::vector<double*> s;                   // ring of pre-scaled tangents S_l = T_l diag(sigma'_l)
   double* s0 = nullptr;                     // S_0 = W_0^T diag(sigma'_0) per point [cap][n_pad][ldt0]
@@ -66,7 +67,8 @@ struct Workspace {
   int64_t ldh = 0;
   double* h = nullptr;             // H accumulator [cap][n_pad][n_pad], lower triangle
   double* syrk_part = nullptr;  // split-K partials (SYRK and batched GEMMs; side stream)
-  double* gemm_part = nullptr;  // split-K partials of single-point tangent GEMMs (main stream)
+  double* gemm_part = nullptr;
+  std::vector<double*> syrk_gather;  // per-layer SYRK partials of the gather path  // split-K partials of single-point tangent GEMMs (main stream)
   CUtensorMap tm_x;                   // x as an A operand [cap][n]
   std::vector<CUtensorMap> tm_y, tm_gz;  // y_l / gz_l as A operands [cap][n_l]
   int sk_chunks = 0;
@@ -240,7 +242,9 @@ class DeviceNet {
   // profiles/r02_fwd_stream.md)
   int fwd_stream_mode_ = 0;
   bool adj_mma_ = true;  // multi-vector adjoints on DMMA (GBOPT_ADJ_MMA=0: CUDA-core sweeps)
-  bool syrk_fuse_ = true;  // one-tile points: all layers' curvature in one launch (GBOPT_SYRK_FUSE=0: per layer)
+  bool adj_fuse_ = true;  // chunk reduction in the adjoint sweep's last CTA (GBOPT_ADJ_FUSE=0: separate launch)
+  bool syrk_fuse_ = true;
+  bool syrk_gather_ = true;  // small batches: per-layer SYRK partials, one gather (GBOPT_SYRK_GATHER=0: per-layer reduce)  // one-tile points: all layers' curvature in one launch (GBOPT_SYRK_FUSE=0: per layer)
 };
 
 }  // namespace gbb

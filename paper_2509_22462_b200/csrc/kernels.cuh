@@ -974,24 +974,31 @@ __global__ void adj_seed_kernel(const double* __restrict__ lam, int64_t ld_lam, 
 constexpr int kAdjThreads = 256;
 constexpr int kAdjRows = 128;
 
+// The chunk reduction of adj_reduce_kernel folded into the column sweep
+// (counters != nullptr): the last chunk CTA of each column block to finish
+// (a self-resetting arrival counter per column block) sums that block's
+// partials over the chunks in ascending order -- the same order and the
+// same values as adj_reduce_kernel, so bit-identical -- and emits ybar / gz /
+// d.  Saves one dependent launch per layer of the adjoint chain.
+struct AdjFuse {
+  unsigned* counters;  // [gridDim.x], zero between launches
+  int chunks;
+  const double* s1;
+  const double* s2;
+  int64_t ld;
+  double* ybar;
+  double* gz;
+  double* d;
+  int s_div;
+};
+
 // KW adjacent k per thread (2: one 16-B load per row; 4: two), so a row's
 // NB shared-memory gz values are reused over KW columns -- the multi-vector
 // sweeps (reverse-mode J: NB = 12 / 16) are otherwise bound by those loads.
-template <int NB, int KW = 2>
-__global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
-    adj_cols_kernel(const double* __restrict__ w, int64_t ldw, int rows, int k_dim, const double* __restrict__ gz,
-                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows) {
-  static_assert(KW == 2 || KW == 4, "KW");
-  __shared__ double gs[NB][kAdjRows];
-  const int k = KW * (blockIdx.x * kAdjThreads + threadIdx.x);
-  const int r0 = blockIdx.y * crows;  // crows <= kAdjRows rows per chunk
-  const int nr = min(crows, rows - r0);
-  for (int e = threadIdx.x; e < NB * kAdjRows; e += kAdjThreads) {
-    const int b = e / kAdjRows, i = e % kAdjRows;
-    gs[b][i] = (p0 + b < nb && i < nr) ? gz[static_cast<int64_t>(p0 + b) * ld_gz + r0 + i] : 0.0;
-  }
-  __syncthreads();
-  if (k >= k_dim) return;
+template <int NB, int KW>
+__device__ __forceinline__ void adj_cols_sweep(const double* __restrict__ w, int64_t ldw,
+                                               const double (&gs)[NB][kAdjRows], int k, int k_dim, int r0, int nr,
+                                               int nb, int p0, double* __restrict__ partial, int64_t ld_part) {
   double a[NB][KW];
 #pragma unroll
   for (int b = 0; b < NB; ++b)
@@ -1055,6 +1062,51 @@ __global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
     for (int c = 0; c < KW; ++c)
       if (k + c < k_dim) o[c] = a[b][c];
   }
+}
+
+template <int NB, int KW = 2>
+__global__ void __launch_bounds__(kAdjThreads, NB * KW <= 32 ? 2 : 1)
+    adj_cols_kernel(const double* __restrict__ w, int64_t ldw, int rows, int k_dim, const double* __restrict__ gz,
+                    int64_t ld_gz, int nb, int p0, double* __restrict__ partial, int64_t ld_part, int crows,
+                    AdjFuse f) {
+  static_assert(KW == 2 || KW == 4, "KW");
+  __shared__ double gs[NB][kAdjRows];
+  __shared__ int last;
+  const int k = KW * (blockIdx.x * kAdjThreads + threadIdx.x);
+  const int r0 = blockIdx.y * crows;  // crows <= kAdjRows rows per chunk
+  const int nr = min(crows, rows - r0);
+  for (int e = threadIdx.x; e < NB * kAdjRows; e += kAdjThreads) {
+    const int b = e / kAdjRows, i = e % kAdjRows;
+    gs[b][i] = (p0 + b < nb && i < nr) ? gz[static_cast<int64_t>(p0 + b) * ld_gz + r0 + i] : 0.0;
+  }
+  __syncthreads();
+  if (k < k_dim) adj_cols_sweep<NB, KW>(w, ldw, gs, k, k_dim, r0, nr, nb, p0, partial, ld_part);
+  if (f.counters == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(&f.counters[blockIdx.x], 1u) == gridDim.y - 1;
+    if (last) f.counters[blockIdx.x] = 0;  // the next launch (stream-ordered) starts from zero
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll 1
+  for (int b = p0; b < p0 + NB && b < nb; ++b)
+#pragma unroll
+    for (int c = 0; c < KW; ++c) {
+      const int kc = k + c;
+      if (kc >= k_dim) break;
+      double sum = 0.0;
+      for (int q = 0; q < f.chunks; ++q) sum += __ldcg(partial + (static_cast<int64_t>(q) * nb + b) * ld_part + kc);
+      const int64_t o = static_cast<int64_t>(b) * f.ld + kc;
+      const int64_t os = static_cast<int64_t>(b / f.s_div) * f.ld + kc;
+      f.ybar[o] = sum;
+      if (f.s1) {
+        f.gz[o] = sum * f.s1[os];
+        if (f.d) f.d[o] = sum * f.s2[os];
+      }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1372,6 +1424,62 @@ __global__ void symmetrize_out_kernel(const double* __restrict__ hws, const doub
   if (h1) v += h1[o];
   if (h2) v += h2[o];
   out[e] = v;
+}
+
+// Small batches (points x square tiles < SMs: every layer's SYRK is split
+// over k) keep each layer's split partials in its own buffer instead of
+// reducing them into H per layer; this kernel sums them once -- layers in
+// order, each layer's slices in ascending order first, then the direct
+// final-layer term hws (nullable), i.e. the additions of the per-layer
+// reduce + symmetrise path in the same order, bit-identical -- and writes
+// the symmetric H (or its packed lower rows).  Two layers' SYRKs can then
+// run concurrently on different streams, and the per-layer reduce launches
+// leave the critical path.  Block (bx <= by) of 32 x 8 threads: the 32 x 32
+// lower block (by, bx) and, through shared memory, its mirror.
+constexpr int kMaxGather = 8;
+struct SyrkGather {
+  const double* part[kMaxGather];  // [split][points][n_tiles][kBM][kBN] per layer
+  int split[kMaxGather];
+  int nseg;
+  int n_tiles;  // square lower tiles per point (tile id tm (tm + 1) / 2 + tn)
+  int points;
+};
+__global__ void __launch_bounds__(256) syrk_gather_out_kernel(SyrkGather g, const double* __restrict__ hws,
+                                                              int64_t h_point_stride, int64_t ldh, int n, int packed,
+                                                              double* __restrict__ out) {
+  const int bx = blockIdx.x, by = blockIdx.y, b = blockIdx.z;
+  if (bx > by) return;
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  for (int ry = ty; ry < 32; ry += 8) {
+    const int r = by * 32 + ry, c = bx * 32 + tx;
+    double v = 0.0;
+    const bool live = r < n && c <= r;
+    if (live) {
+      const int tm = r / kBM, tn = c / kBM;
+      const int64_t off = (static_cast<int64_t>(b) * g.n_tiles + tm * (tm + 1) / 2 + tn) * (kBM * kBN) +
+                          (r % kBM) * kBN + (c % kBM);
+      const int64_t slice = static_cast<int64_t>(g.points) * g.n_tiles * (kBM * kBN);
+      for (int q = 0; q < g.nseg; ++q) {
+        double t = 0.0;
+        for (int s = 0; s < g.split[q]; ++s) t += __ldcg(g.part[q] + slice * s + off);
+        v += t;
+      }
+      if (hws) v += hws[h_point_stride * b + static_cast<int64_t>(r) * ldh + c];
+      if (packed)
+        out[static_cast<int64_t>(b) * n * (n + 1) / 2 + static_cast<int64_t>(r) * (r + 1) / 2 + c] = v;
+      else
+        out[nn * b + static_cast<int64_t>(r) * n + c] = v;
+    }
+    tile[ry][tx] = v;
+  }
+  if (packed) return;
+  __syncthreads();
+  for (int ry = ty; ry < 32; ry += 8) {
+    const int r = bx * 32 + ry, c = by * 32 + tx;  // strict upper element (r, c) = H(c, r)
+    if (c < n && c > r) out[nn * b + static_cast<int64_t>(r) * n + c] = tile[tx][ry];
+  }
 }
 
 // dst[b][r][c] = src[b * src_point_rows + r][c] * scale[b * s_stride + c]

@@ -86,6 +86,9 @@ CUtensorMap make_tmap(const double* base, int64_t cols, int64_t rows, int64_t pi
 }
 
 int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+// CTAs per tile of the split-K GEMM reduction (single-point GEMMs, c1):
+// 14 x 256 threads take 4 of the tile's 14336 elements each
+constexpr int kGemmReduceX = 14;
 
 // Several DeviceNets may run on host threads at once (multi-device calls,
 // multi.cpp; or a caller's own threads with distinct handles).  Graph
@@ -126,6 +129,8 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   CK(cudaFuncSetAttribute(dev::adj_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kAmSmem));
   if (const char* e = std::getenv("GBOPT_ADJ_MMA")) adj_mma_ = e[0] != '0';
   if (const char* e = std::getenv("GBOPT_SYRK_FUSE")) syrk_fuse_ = e[0] != '0';
+  if (const char* e = std::getenv("GBOPT_ADJ_FUSE")) adj_fuse_ = e[0] != '0';
+  if (const char* e = std::getenv("GBOPT_SYRK_GATHER")) syrk_gather_ = e[0] != '0';
   CK(cudaFuncSetAttribute(dev::nt_syrk_segs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   if (const char* e = std::getenv("GBOPT_DATAFLOW"))
     dataflow_mode_ = e[0] == '0' ? 0 : (e[0] == '-' && e[1] == '2') ? -2 : 1;
@@ -326,6 +331,11 @@ void DeviceNet::ensure_workspace(int batch) {
     for (bool multi : {false, true}) w.adj_chunks_max = std::max(w.adj_chunks_max, adj_layout(d, multi).chunks);
   w.ld_part = ldt_ > w.ld_in ? ldt_ : w.ld_in;
   w.adj_part = ws_alloc(static_cast<size_t>(w.adj_chunks_max) * vcap * w.ld_part);
+  {  // arrival counters of the fused chunk reduction, one per column block
+    int gx = 1;
+    for (auto& d : layers_) gx = std::max(gx, ceil_div(d.cols, 2 * static_cast<int64_t>(dev::kAdjThreads)));
+    w.adj_cnt = reinterpret_cast<unsigned*>(ws_alloc(static_cast<size_t>(gx)));
+  }
   // tangents (only needed with >= 2 layers)
   // T_l (l >= 1) lives in ring buffer t_buf(l) = (l - 1) % R.  With R >= the
   // number of tangent layers the GEMM chain never waits for a SYRK to free
@@ -360,6 +370,15 @@ void DeviceNet::ensure_workspace(int batch) {
   // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
   w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, std::max(n_syrk_tiles_, n_sq_tiles_))) * kBM * kBN);
   w.gemm_part = ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN);
+  // per-layer SYRK partials of the gather path (single points: points x
+  // square tiles < SMs), one buffer per curvature layer
+  w.syrk_gather.clear();
+  if (n_sq_tiles_ < sm_count_) {
+    int segs = 0;
+    for (auto& d : layers_) segs += d.act != kLinear;
+    if (segs <= dev::kMaxGather)
+      for (int q = 0; q < segs; ++q) w.syrk_gather.push_back(ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN));
+  }
   // final-layer skinny product: U [cap][n_pad][16], partials [chunks][cap][n_pad][16]
   const int64_t kfin = layers_[L - 1].cols;
   w.sk_chunks = ceil_div(kfin, dev::skinny_kchunk(m_ <= 1 ? 1 : (m_ <= 4 ? 4 : 16)));
@@ -752,6 +771,26 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
           after_launch(sb);
         }
       }
+      // the chunk reduction rides on the sweep's last CTA per column block
+      // (adj_fuse_; bit-identical to adj_reduce_kernel)
+      dev::AdjFuse f{};
+      const bool fuse = adj_fuse_ && !mma && w.adj_cnt != nullptr;
+      if (fuse) {
+        f.counters = w.adj_cnt;
+        f.chunks = chunks;
+        f.s_div = l > 0 ? s_div : 1;
+        if (l > 0) {
+          f.s1 = w.s1[l - 1];
+          f.s2 = w.s2[l - 1];
+          f.ld = w.ld[l - 1];
+          f.ybar = w.ybar[l - 1];
+          f.gz = w.gz[l - 1];
+          f.d = want_d ? w.d[l - 1] : nullptr;
+        } else {
+          f.ld = w.ld_in;
+          f.ybar = w.grad;
+        }
+      }
       for (int p0 = 0; p0 < nv && !mma;) {
         const int left = nv - p0;
         // one weight sweep per up to 16 vectors (reverse-mode J: m <= 16
@@ -760,7 +799,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         prof_begin(sb, kTagAdjCols, 2.0 * d.rows * d.cols * std::min(pass, left), 8.0 * d.rows * d.cols);
 #define GBB_ADJ(NBV, KWV)                                                                                          \
   dev::adj_cols_kernel<NBV, KWV><<<grid, dev::kAdjThreads, 0, sb>>>(d.w, d.ldw, d.rows, d.cols, w.gz[l], w.ld[l], nv, \
-                                                                    p0, w.adj_part, w.ld_part, crows)
+                                                                    p0, w.adj_part, w.ld_part, crows, f)
         if (pass == 16) {
           if (kw == 4) GBB_ADJ(16, 4); else GBB_ADJ(16, 2);
         } else if (pass == 12) {
@@ -777,6 +816,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         p0 += pass;
         after_launch(sb);
       }
+      if (fuse) continue;
       const int64_t tot = static_cast<int64_t>(nv) * d.cols;
       prof_begin(sb, kTagAdjReduce, 0, 0);
       if (l > 0) {
@@ -792,6 +832,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     }
   };
 
+  cudaEvent_t adj_done = nullptr;  // the adjoint chain (d_l of every layer) on sb
   if (need_adj) {
     link(sa, sb);  // the adjoint needs the forward chain
     prof_begin(sb, kTagAdjSeed, 0, 0);
@@ -800,6 +841,10 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
     after_launch(sb);
     adjoint_chain(nb, 1, o.g ? 0 : 1, true);
+    if (two) {
+      adj_done = next_event();
+      CK(cudaEventRecord(adj_done, sb));
+    }
     if (o.g) {
       CK(cudaMemcpy2DAsync(o.g, sizeof(double) * n_, w.grad, sizeof(double) * w.ld_in, sizeof(double) * n_, nb,
                            cudaMemcpyDeviceToDevice, sb));
@@ -840,7 +885,6 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   const bool fuse_syrk = want_h && syrk_fuse_ && square_syrk_ && n_pad_ == kBM && nb >= sm_count_ &&
                          nl_hidden >= 1 && nl_hidden <= dev::kMaxSegs &&
                          static_cast<int>(w.t.size()) >= L - 2;
-  if (want_h && !fuse_syrk) CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
   const int kfin_layer = L - 1;
   const bool skinny_final = m_ <= dev::kSkMB;
   // T_l lives in: l == 0 -> t0_ (broadcast over points), else ring buffer
@@ -853,7 +897,26 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   auto tmap_a = [&](int l) -> const CUtensorMap& { return l == 0 ? tm_t0_a_ : w.tm_t_a[static_cast<size_t>(l)]; };
   auto tmap_b = [&](int l) -> const CUtensorMap& { return l == 0 ? tm_t0_b_ : w.tm_t_b[static_cast<size_t>(l)]; };
 
-  auto syrk = [&](int l) {
+  // Gather path (small batches: every SYRK is split over k): each layer's
+  // partials stay in their own buffer, one syrk_gather_out launch sums them
+  // into the output; the last hidden layer's SYRK then runs on sa beside the
+  // side stream's (GBOPT_SYRK_GATHER=0: reduce per layer into H on sb)
+  const bool gather = want_h && !fuse_syrk && syrk_gather_ && square_syrk_ &&
+                      static_cast<int64_t>(nb) * n_sq_tiles_ < sm_count_ &&
+                      static_cast<int>(w.syrk_gather.size()) >= [&] {
+                        int segs = 0;
+                        for (int l = 0; l < L; ++l) segs += layers_[static_cast<size_t>(l)].act != kLinear;
+                        return segs;
+                      }();
+  dev::SyrkGather gat{};
+  gat.n_tiles = n_sq_tiles_;
+  gat.points = nb;
+  // the final layer's curvature as a direct update into H (small K)
+  const DevLayer& dl = layers_[static_cast<size_t>(L - 1)];
+  const bool h_direct = dl.act != kLinear && (softmax_out || m_ <= dev::kSkMB || L == 1);
+  if (want_h && !fuse_syrk && (!gather || h_direct))
+    CK(cudaMemsetAsync(w.h, 0, sizeof(double) * nb * n_pad_ * n_pad_, sb));
+  auto syrk = [&](int l, cudaStream_t ss) {
     const DevLayer& d = layers_[static_cast<size_t>(l)];
     dev::NtParams p{};
     p.tiles = syrk_tiles_;
@@ -877,15 +940,21 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       p.n_tiles = n_sq_tiles_;
       p.square = 1;
     }
-    prof_begin(sb, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
-    launch_nt(sb, tmap_a(l), square_syrk_ ? tmap_a(l) : tmap_b(l), p, nb * p.n_tiles * p.split);
-    if (p.split > 1) {
+    if (gather) {  // this layer's slices into its own buffer (split 1 too: no atomics into a shared H)
+      p.mode = dev::kPartial;
+      p.partial = w.syrk_gather[static_cast<size_t>(gat.nseg)];
+      gat.part[gat.nseg] = p.partial;
+      gat.split[gat.nseg++] = p.split;
+    }
+    prof_begin(ss, kTagSyrk, static_cast<double>(d.rows) * n_ * (n_ + 1) * nb, 0);
+    launch_nt(ss, tmap_a(l), square_syrk_ ? tmap_a(l) : tmap_b(l), p, nb * p.n_tiles * p.split);
+    if (p.split > 1 && !gather) {
       prof_begin(sb, kTagSyrkReduce, 0, 0);
       dim3 grid(8, nb * p.n_tiles);
-      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, sb>>>(w.syrk_part, p.tiles, p.n_tiles, nb, p.split, w.h,
+      dev::syrk_partial_reduce_kernel<<<grid, 256, 0, ss>>>(w.syrk_part, p.tiles, p.n_tiles, nb, p.split, w.h,
                                                             n_pad_ * n_pad_, n_pad_, static_cast<int>(n_),
                                                             square_syrk_ ? kBM : kBN);
-      after_launch(sb);
+      after_launch(ss);
     }
   };
 
@@ -896,13 +965,31 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   for (int l = 0; l + 2 < L && prescaled; ++l)
     if (nb == 1 && (n_pad_ / kBM) * ceil_div(layers_[static_cast<size_t>(l + 1)].rows, kBN) * 2 <= sm_count_)
       prescaled = false;
+  cudaEvent_t t_last = nullptr;  // gather path: T_{L-2} ready on sa (the final layer then runs on sb)
+  bool defer_last = false;        // gather path: SYRK_{L-2} on sa after the final layer
   // syrk_done[l]: event on sb after SYRK_l (nullptr when none ran)
   std::vector<cudaEvent_t> syrk_done(static_cast<size_t>(L), nullptr);
   for (int l = 0; l + 1 < L; ++l) {
     // curvature of hidden layer l, on sb once T_l exists (T_0 is constant)
-    if (want_h && !fuse_syrk && layers_[static_cast<size_t>(l)].act != kLinear) {
+    // gather path, last hidden layer before a skinny final layer: its SYRK
+    // runs on sa (beside the side stream's SYRKs) once its d (sb's adjoint
+    // chain) exists.  With one tangent GEMM (L = 3, c1) it runs right after
+    // that GEMM and the final layer moves to sb, so the two SYRKs overlap
+    // (c1 9.5k -> 10.4k evals/s); with a longer chain the final layer's
+    // bandwidth-bound skinny product goes first on sa, alone on the SMs
+    // (c2: 183.7 vs 182.8 evals/s the other way round)
+    const bool defer = gather && two && l >= 1 && l == L - 2 && l + 1 == kfin_layer && skinny_final &&
+                       adj_done != nullptr && layers_[static_cast<size_t>(l)].act != kLinear;
+    if (defer && L == 3) {
+      t_last = next_event();
+      CK(cudaEventRecord(t_last, sa));
+      CK(cudaStreamWaitEvent(sa, adj_done, 0));
+      syrk(l, sa);
+    }
+    defer_last = defer && L > 3;
+    if (want_h && !fuse_syrk && layers_[static_cast<size_t>(l)].act != kLinear && !defer) {
       if (l > 0) link(sa, sb);
-      syrk(l);
+      syrk(l, sb);
       if (two) {
         syrk_done[static_cast<size_t>(l)] = next_event();
         CK(cudaEventRecord(syrk_done[static_cast<size_t>(l)], sb));
@@ -986,7 +1073,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
         e.s1i = p.c2_scale;
         e.ld = ldt_;
         prof_begin(sa, kTagRowEpi, 0, 0);
-        dev::gemm_partial_reduce_kernel<<<dim3(4, p.n_tiles), 256, 0, sa>>>(
+        dev::gemm_partial_reduce_kernel<<<dim3(kGemmReduceX, p.n_tiles), 256, 0, sa>>>(
             w.gemm_part, p.split, p.tiles_m, p.tiles_n, static_cast<int>(n_pad_), static_cast<int>(dn.rows), e);
         after_launch(sa);
         continue;
@@ -1029,7 +1116,13 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   }
 
   // ---- 4. final layer -------------------------------------------------------
-  if (fwd_all) CK(cudaStreamWaitEvent(sa, fwd_all, 0));  // sigma'/y of the last layers
+  cudaStream_t sfin = sa;
+  if (t_last) {
+    sfin = sb;  // after the forward chain (stream order) and T_{L-2}
+    CK(cudaStreamWaitEvent(sb, t_last, 0));
+  } else if (fwd_all) {
+    CK(cudaStreamWaitEvent(sa, fwd_all, 0));  // sigma'/y of the last layers
+  }
   const DevLayer& df = layers_[static_cast<size_t>(kfin_layer)];
   const double* u;
   int64_t ldu, u_point_rows;
@@ -1039,7 +1132,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     u_point_rows = 0;
   } else if (skinny_final) {
     const int l = kfin_layer - 1;
-    launch_skinny(sa, nb, t_ptr(l), t_ld(l), t_point_rows(l), l);
+    launch_skinny(sfin, nb, t_ptr(l), t_ld(l), t_point_rows(l), l);
     u = w.u;
     ldu = dev::kSkMB;
     u_point_rows = n_pad_;
@@ -1050,12 +1143,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   }
   if (want_j) {
     const int64_t tot = static_cast<int64_t>(nb) * n_;
-    prof_begin(sa, kTagJacOut, 0, 0);
-    dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, sa>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
-                                                                 w.y[kfin_layer], w.ld[kfin_layer],
-                                                                 static_cast<int>(n_), static_cast<int>(m_), nb,
-                                                                 softmax_out ? 1 : 0, o.j);
-    after_launch(sa);
+    prof_begin(sfin, kTagJacOut, 0, 0);
+    dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, sfin>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
+                                                                   w.y[kfin_layer], w.ld[kfin_layer],
+                                                                   static_cast<int>(n_), static_cast<int>(m_), nb,
+                                                                   softmax_out ? 1 : 0, o.j);
+    after_launch(sfin);
+  }
+  if (defer_last) {
+    CK(cudaStreamWaitEvent(sa, adj_done, 0));
+    syrk(L - 2, sa);
   }
   if (want_h) {
     cudaStream_t sh = sb;  // the SYRKs live on sb
@@ -1071,12 +1168,15 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
                                                        static_cast<int>(m_), nb, w.h, n_pad_ * n_pad_, n_pad_);
         after_launch(sh);
       } else {
-        syrk(kfin_layer);
+        syrk(kfin_layer, sh);
       }
     }
     const int64_t tot = static_cast<int64_t>(nb) * n_ * n_;
     prof_begin(sh, kTagSymmetrize, 0, 0);
-    if (o.h_packed)
+    if (gather)
+      dev::syrk_gather_out_kernel<<<dim3(ceil_div(n_, 32), ceil_div(n_, 32), nb), 256, 0, sh>>>(
+          gat, h_direct ? w.h : nullptr, n_pad_ * n_pad_, n_pad_, static_cast<int>(n_), o.h_packed ? 1 : 0, o.h);
+    else if (o.h_packed)
       dev::pack_lower_kernel<<<dim3(ceil_div(n_, 256), static_cast<unsigned>(n_), nb), 256, 0, sh>>>(
           w.h, 1, 0, n_pad_ * n_pad_, n_pad_, static_cast<int>(n_), o.h);
     else
