@@ -159,7 +159,8 @@ class DeviceNet {
   int syrk_split(int points, int k_blocks) const;
   void ensure_transposed();
   void prepare(int nb, const Outputs& o);
-  void launch_skinny(cudaStream_t st, int nb, const double* t, int64_t ldt, int64_t t_point_rows, int l);
+  void launch_skinny(cudaStream_t st, int nb, const double* t, int64_t ldt, int64_t t_point_rows, int l,
+                     double* jac = nullptr);
   void batch_gemm(cudaStream_t st, int nb, const CUtensorMap& ta, const DevLayer& d, bool transposed,
                   const void* epi, double* store);
   void launch_nt(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, const dev::NtParams& p, int grid);

@@ -784,11 +784,21 @@ constexpr int kFwdWarps = 8;
 // WPR warps share a row (split K, fixed-order reduction through shared
 // memory: deterministic) so layers with few rows still fill the GPU; each
 // lane keeps 8 independent 16-byte weight loads in flight.
+// Optional extras of a single point's last forward layer (elementwise
+// output): the y output copy and the adjoint seed gz = lambda sigma',
+// d = lambda sigma'' (adj_seed_kernel) -- two dependent launches fewer.
+struct FwdTail {
+  double* y;          // nullable: y output
+  const double* lam;  // nullable: seed the adjoint
+  double* gz;
+  double* d;
+};
+
 template <int WPR>
 __global__ void __launch_bounds__(kFwdWarps * 32)
     fwd_row1_kernel(const double* __restrict__ w, int64_t ldw, const double* __restrict__ bias, int rows, int k_dim,
                     const double* __restrict__ yin, int act, double* __restrict__ z_out, double* __restrict__ y_out,
-                    double* __restrict__ s1_out, double* __restrict__ s2_out) {
+                    double* __restrict__ s1_out, double* __restrict__ s2_out, FwdTail tail) {
   constexpr int kRowsPerCta = kFwdWarps / WPR;
   __shared__ double part[kFwdWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -845,6 +855,11 @@ __global__ void __launch_bounds__(kFwdWarps * 32)
     y_out[row] = yy;
     s1_out[row] = d1;
     s2_out[row] = d2;
+    if (tail.y) tail.y[row] = yy;
+    if (tail.lam) {  // adj_seed_kernel's elementwise seed, same products
+      tail.gz[row] = tail.lam[row] * d1;
+      tail.d[row] = tail.lam[row] * d2;
+    }
   }
 }
 
@@ -1348,14 +1363,22 @@ __global__ void __launch_bounds__(256)
 }
 
 // U[b][j][i] = sum_c partial[c][b][j][i]   (deterministic order)
+// jac != nullptr (elementwise final activation): also J[b][i][j] = s1_i U_ji,
+// jacobian_out_kernel's product, folded in (one launch less on the J path).
 __global__ void skinny_reduce_kernel(const double* __restrict__ partial, int chunks, int nb, int rows_pad, int m,
-                                     double* __restrict__ u) {
+                                     double* __restrict__ u, double* __restrict__ jac, const double* __restrict__ s1,
+                                     int64_t ld, int n) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t per_point = static_cast<int64_t>(rows_pad) * kSkMB;
   if (e >= per_point * nb) return;
   double sum = 0.0;
   for (int c = 0; c < chunks; ++c) sum += partial[static_cast<int64_t>(c) * nb * per_point + e];
   u[e] = sum;
+  if (jac) {
+    const int b = static_cast<int>(e / per_point);
+    const int j = static_cast<int>((e % per_point) / kSkMB), i = static_cast<int>(e % kSkMB);
+    if (i < m && j < n) jac[(static_cast<int64_t>(b) * m + i) * n + j] = s1[ld * b + i] * sum;
+  }
 }
 
 // J[b][i][j] from U = dz_L/dx^T (rows j, cols i, pitch ldu):

@@ -560,7 +560,8 @@ void DeviceNet::profile(int nb, const double* dx, const double* dlam, std::vecto
 
 // Final layer with m <= 16 outputs: U = T_l diag(sigma'_l) W_{l+1}^T into
 // w.u ([nb][n_pad][16]) by the skinny split-K kernel + fixed-order reduce.
-void DeviceNet::launch_skinny(cudaStream_t st, int nb, const double* t, int64_t ldt, int64_t t_point_rows, int l) {
+void DeviceNet::launch_skinny(cudaStream_t st, int nb, const double* t, int64_t ldt, int64_t t_point_rows, int l,
+                              double* jac) {
   Workspace& w = ws_;
   const DevLayer& df = layers_[static_cast<size_t>(l + 1)];
   dim3 grid(static_cast<unsigned>(n_pad_ / dev::kSkRows), w.sk_chunks, nb);
@@ -580,7 +581,8 @@ void DeviceNet::launch_skinny(cudaStream_t st, int nb, const double* t, int64_t 
   const int64_t tot = static_cast<int64_t>(nb) * n_pad_ * dev::kSkMB;
   prof_begin(st, kTagSkinnyReduce, 0, 0);
   dev::skinny_reduce_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(w.sk_part, w.sk_chunks, nb, static_cast<int>(n_pad_),
-                                                                static_cast<int>(m_), w.u);
+                                                                static_cast<int>(m_), w.u, jac, w.s1[l + 1], w.ld[l + 1],
+                                                                static_cast<int>(n_));
   after_launch(st);
 }
 
@@ -644,6 +646,9 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   // Layer 0 runs on sa (GEMM_1 needs only sigma'_0); layers >= 1 run on sb,
   // beside the tangent GEMMs, each recording fwd_done[l] for GEMM_{l+1}.
   std::vector<cudaEvent_t> fwd_done(static_cast<size_t>(L), nullptr);
+  // a single point with an elementwise output: the last layer's GEMV also
+  // writes y out and seeds the adjoint (no copy node, no seed launch)
+  const bool tail_fused = nb == 1 && !batched && !softmax_out;
   for (int l = 0; l < L; ++l) {
     const DevLayer& d = layers_[static_cast<size_t>(l)];
     if (l == 1) link(sa, sb);
@@ -671,6 +676,15 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     const int act = d.act == kSoftmax ? kLinear : d.act;
     prof_begin(sa, kTagFwd, 2.0 * d.rows * d.cols * nb, 8.0 * d.rows * d.cols * ceil_div(nb, nbpass));
     if (nb == 1) {
+      dev::FwdTail tail{};
+      if (l == L - 1 && tail_fused) {
+        tail.y = o.y;
+        if (need_adj) {
+          tail.lam = w.lam;
+          tail.gz = w.gz[L - 1];
+          tail.d = w.d[L - 1];
+        }
+      }
       // warps per row so that short layers (the 10-row output) still spread
       // over the GPU: aim at >= 16 warps per SM
       const int64_t target = static_cast<int64_t>(sm_count_) * 16;
@@ -678,16 +692,16 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       const dim3 g1(ceil_div(d.rows * wpr, dev::kFwdWarps));
       if (wpr == 1)
         dev::fwd_row1_kernel<1><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
-                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l], tail);
       else if (wpr == 2)
         dev::fwd_row1_kernel<2><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
-                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l], tail);
       else if (wpr == 4)
         dev::fwd_row1_kernel<4><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
-                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l], tail);
       else
         dev::fwd_row1_kernel<8><<<g1, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, act,
-                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l]);
+                                                                    w.z[l], w.y[l], w.s1[l], w.s2[l], tail);
     } else if (nbpass == 8)
       dev::fwd_rows_kernel<8><<<grid, dev::kFwdWarps * 32, 0, sa>>>(d.w, d.ldw, d.b, d.rows, d.cols, yin, ld_in, nb,
                                                                      act, w.z[l], w.y[l], w.s1[l], w.s2[l], w.ld[l]);
@@ -713,7 +727,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
                                                          nb);
     after_launch(sf);
   }
-  if (o.y) {
+  if (o.y && !tail_fused) {
     CK(cudaMemcpy2DAsync(o.y, sizeof(double) * m_, w.y[L - 1], sizeof(double) * w.ld[L - 1], sizeof(double) * m_, nb,
                          cudaMemcpyDeviceToDevice, sf));
   }
@@ -835,11 +849,13 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
   cudaEvent_t adj_done = nullptr;  // the adjoint chain (d_l of every layer) on sb
   if (need_adj) {
     link(sa, sb);  // the adjoint needs the forward chain
-    prof_begin(sb, kTagAdjSeed, 0, 0);
-    dev::adj_seed_kernel<<<ceil_div(nb, 4), 128, 0, sb>>>(
-        w.lam, w.ld_lam, w.y[L - 1], w.s1[L - 1], w.s2[L - 1], w.ld[L - 1], static_cast<int>(m_), nb,
-        softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
-    after_launch(sb);
+    if (!tail_fused) {
+      prof_begin(sb, kTagAdjSeed, 0, 0);
+      dev::adj_seed_kernel<<<ceil_div(nb, 4), 128, 0, sb>>>(
+          w.lam, w.ld_lam, w.y[L - 1], w.s1[L - 1], w.s2[L - 1], w.ld[L - 1], static_cast<int>(m_), nb,
+          softmax_out ? 1 : 0, w.gz[L - 1], w.d[L - 1], w.mid, m_ * m_);
+      after_launch(sb);
+    }
     adjoint_chain(nb, 1, o.g ? 0 : 1, true);
     if (two) {
       adj_done = next_event();
@@ -1132,7 +1148,8 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     u_point_rows = 0;
   } else if (skinny_final) {
     const int l = kfin_layer - 1;
-    launch_skinny(sfin, nb, t_ptr(l), t_ld(l), t_point_rows(l), l);
+    // elementwise final activation: J written by the skinny reduction
+    launch_skinny(sfin, nb, t_ptr(l), t_ld(l), t_point_rows(l), l, want_j && !softmax_out ? o.j : nullptr);
     u = w.u;
     ldu = dev::kSkMB;
     u_point_rows = n_pad_;
@@ -1141,7 +1158,7 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
     ldu = ldt_;
     u_point_rows = n_pad_;
   }
-  if (want_j) {
+  if (want_j && !(skinny_final && kfin_layer > 0 && !softmax_out)) {
     const int64_t tot = static_cast<int64_t>(nb) * n_;
     prof_begin(sfin, kTagJacOut, 0, 0);
     dev::jacobian_out_kernel<<<ceil_div(tot, 128), 128, 0, sfin>>>(u, ldu, u_point_rows, w.s1[kfin_layer],
