@@ -245,6 +245,7 @@ class DeviceNet {
   bool adj_mma_ = true;  // multi-vector adjoints on DMMA (GBOPT_ADJ_MMA=0: CUDA-core sweeps)
   bool adj_fuse_ = true;  // chunk reduction in the adjoint sweep's last CTA (GBOPT_ADJ_FUSE=0: separate launch)
   bool syrk_fuse_ = true;
+  int s0_mode_ = -1;  // S_0 = T_0 diag(sigma'_0) materialised: -1 by the rule, 0 / 1 forced (GBOPT_S0_PASS)
   bool syrk_gather_ = true;  // small batches: per-layer SYRK partials, one gather (GBOPT_SYRK_GATHER=0: per-layer reduce)  // one-tile points: all layers' curvature in one launch (GBOPT_SYRK_FUSE=0: per layer)
 };
 

@@ -1507,14 +1507,16 @@ __global__ void __launch_bounds__(256) syrk_gather_out_kernel(SyrkGather g, cons
 
 // dst[b][r][c] = src[b * src_point_rows + r][c] * scale[b * s_stride + c]
 // for b < nb, r < rows, c < cols (S_0 = T_0 diag(sigma'_0) per point).
-// Grid: x over columns, y = b * rows + r.
+// Grid: x over columns, y strides over b * rows + r (gridDim.y <= 65535).
 __global__ void scale_cols_kernel(const double* __restrict__ src, int64_t lds, int64_t src_point_rows, int rows,
                                   int cols, const double* __restrict__ scale, int64_t s_stride,
                                   double* __restrict__ dst, int64_t ldd, int64_t dst_point_rows, int nb) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int b = blockIdx.y / rows, r = blockIdx.y % rows;
-  if (c >= cols || b >= nb) return;
-  dst[(dst_point_rows * b + r) * ldd + c] = src[(src_point_rows * b + r) * lds + c] * scale[s_stride * b + c];
+  if (c >= cols) return;
+  for (int64_t y = blockIdx.y; y < static_cast<int64_t>(nb) * rows; y += gridDim.y) {
+    const int b = static_cast<int>(y / rows), r = static_cast<int>(y % rows);
+    dst[(dst_point_rows * b + r) * ldd + c] = src[(src_point_rows * b + r) * lds + c] * scale[s_stride * b + c];
+  }
 }
 
 // Strided copy of a [rows][cols] block (pitch src -> pitch dst).

@@ -131,6 +131,7 @@ DeviceNet::DeviceNet(const Net& net, int ordinal) : net_(net), ordinal_(ordinal)
   if (const char* e = std::getenv("GBOPT_SYRK_FUSE")) syrk_fuse_ = e[0] != '0';
   if (const char* e = std::getenv("GBOPT_ADJ_FUSE")) adj_fuse_ = e[0] != '0';
   if (const char* e = std::getenv("GBOPT_SYRK_GATHER")) syrk_gather_ = e[0] != '0';
+  if (const char* e = std::getenv("GBOPT_S0_PASS")) s0_mode_ = e[0] == '1' ? 1 : 0;
   CK(cudaFuncSetAttribute(dev::nt_syrk_segs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kSmemBytes));
   if (const char* e = std::getenv("GBOPT_DATAFLOW"))
     dataflow_mode_ = e[0] == '0' ? 0 : (e[0] == '-' && e[1] == '2') ? -2 : 1;
@@ -1049,11 +1050,12 @@ void DeviceNet::enqueue(cudaStream_t st, int nb, const Outputs& o) {
       // ~4% of 2 nb n n_1 n_2 flops against 8 nb n n_1 bytes written, i.e.
       // n_2 >~ 1400 (c2/c3: 5120 yes; c4/c5: 1024 no -- the first GEMM then
       // keeps the per-fragment scale on the shared T_0).
-      const bool s0_pass = layers_[1].rows >= 2048;
+      const bool s0_pass = s0_mode_ >= 0 ? s0_mode_ == 1 : layers_[1].rows >= 2048;
       if (l == 0 && s0_pass) {
         const int cols0 = static_cast<int>(layers_[0].rows);
         prof_begin(sa, kTagRowEpi, 0, 0);
-        dev::scale_cols_kernel<<<dim3(ceil_div(cols0, 256), static_cast<unsigned>(nb * n_pad_)), 256, 0, sa>>>(
+        dev::scale_cols_kernel<<<dim3(ceil_div(cols0, 256), static_cast<unsigned>(std::min<int64_t>(nb * n_pad_, 65535))),
+                                 256, 0, sa>>>(
             t0_, ldt0_, 0, static_cast<int>(n_pad_), cols0, w.s1[0], w.ld[0], w.s0, ldt0_, n_pad_, nb);
         after_launch(sa);
         ta = &w.tm_s0;

@@ -362,3 +362,54 @@ def test_multi_segment_syrk_matches_per_layer():
         assert r.returncode == 0, r.stderr
         outs.append(np.array(json.loads(r.stdout.strip().splitlines()[-1])))
     assert orc.rel_err(outs[0], outs[1]) <= 1e-13
+
+
+def test_fused_reductions_are_bitwise_identical():
+    """The single-point launch savings -- per-layer SYRK partials gathered in
+    one launch (GBOPT_SYRK_GATHER), the adjoint chunk reduction in the sweep's
+    last CTA (GBOPT_ADJ_FUSE) -- add in the same order as the separate
+    reductions: Y, J, H (full and packed) bit for bit, separate processes."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import json, sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_2509_22462_b200 as gb\n"
+        "out = []\n"
+        "for widths, hid, fin, B in (([784, 512, 512, 10], 'tanh', 'linear', 1),\n"
+        "                            ([130, 200, 150, 12], 'softplus', 'sigmoid', 3),\n"
+        "                            ([40, 64, 64, 64, 20], 'sigmoid', 'softmax', 2)):\n"
+        "    net = gb.random_net(widths, hid, fin, 5).bind_device(0)\n"
+        "    rng = np.random.default_rng(6)\n"
+        "    X = rng.uniform(-1, 1, (B, widths[0])); L = rng.normal(size=(B, widths[-1]))\n"
+        "    Y, J, H = net.oracle_batched(X, L)\n"
+        "    out += [Y.tolist(), J.tolist(), H.tolist()]\n"
+        "    out.append(net.oracle_lower(X[0], L[0])[2].tolist())\n"
+        "print(json.dumps(out))\n" % root)
+    outs = []
+    for env in ({}, {"GBOPT_SYRK_GATHER": "0"}, {"GBOPT_ADJ_FUSE": "0"}, {"GBOPT_SYRK_GATHER": "0", "GBOPT_ADJ_FUSE": "0"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, **env))
+        assert r.returncode == 0, r.stderr
+        outs.append([np.array(a) for a in json.loads(r.stdout.strip().splitlines()[-1])])
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+
+
+def test_s0_pass_batch_beyond_grid_y_limit():
+    """S_0 = T_0 diag(sigma'_0) materialised for a wide second layer with
+    points x n_pad > 65535 rows (the grid-y limit of one launch)."""
+    net = gb.random_net([784, 2048, 2048, 10], "softplus", "linear", 31).bind_device(0)
+    ref = to_oracle(net)
+    rng = np.random.default_rng(31)
+    B = 90  # 90 x 784 = 70560 rows
+    X = rng.uniform(0, 1, (B, 784))
+    L = rng.normal(size=(B, 10))
+    Y, J, H = net.oracle_batched(X, L)
+    for k in (0, 89):
+        assert orc.rel_err(Y[k], ref.forward(X[k])) <= TOL
+        assert orc.rel_err(J[k], ref.jacobian(X[k])) <= TOL
+        assert orc.rel_err(H[k], ref.lagrangian_hessian(X[k], L[k])) <= TOL
