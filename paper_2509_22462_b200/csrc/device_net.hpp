@@ -144,8 +144,15 @@ class DeviceNet {
   // Device buffers, ordered on `user` stream, asynchronous.
   void evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
                        cudaStream_t user);
+  // Batches above kMaxChunk points run as consecutive sub-batches (grid
+  // dimensions y / z of the per-point launches stay <= 65535).
+  static constexpr int kMaxChunk = 32768;
 
  private:
+  void evaluate_host_chunk(int nb, const double* x, const double* lam, double* y, double* jac, double* hess,
+                           double* grad, bool hess_packed);
+  void evaluate_device_chunk(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
+                             cudaStream_t user);
   using GraphKey = std::tuple<int, double*, double*, double*, double*, bool, bool>;
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;

@@ -1389,6 +1389,28 @@ void DeviceNet::launch_fwd_stream(cudaStream_t st) {
 // Host-buffer entry: copy in, evaluate, copy out, synchronise.
 void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double* y, double* jac, double* hess,
                               double* grad, bool hess_packed) {
+  const int64_t n = n_, m = m_, hsz = hess_packed ? n_ * (n_ + 1) / 2 : n_ * n_;
+  for (int p0 = 0; p0 < nb || p0 == 0; p0 += kMaxChunk) {
+    const int c = std::min(kMaxChunk, nb - p0);
+    auto at = [p0](auto* ptr, int64_t per) { return ptr ? ptr + per * p0 : ptr; };
+    evaluate_host_chunk(c, at(x, n), at(lam, m), at(y, m), at(jac, m * n), at(hess, hsz), at(grad, n), hess_packed);
+    if (nb <= 0) break;
+  }
+}
+
+void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
+                                cudaStream_t user) {
+  const int64_t n = n_, m = m_;
+  for (int p0 = 0; p0 < nb || p0 == 0; p0 += kMaxChunk) {
+    const int c = std::min(kMaxChunk, nb - p0);
+    auto at = [p0](auto* ptr, int64_t per) { return ptr ? ptr + per * p0 : ptr; };
+    evaluate_device_chunk(c, at(dx, n), at(dlam, m), at(dy, m), at(dj, m * n), at(dh, n * n), user);
+    if (nb <= 0) break;
+  }
+}
+
+void DeviceNet::evaluate_host_chunk(int nb, const double* x, const double* lam, double* y, double* jac, double* hess,
+                                    double* grad, bool hess_packed) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
   Workspace& w = ws_;
@@ -1539,8 +1561,8 @@ void DeviceNet::evaluate_host(int nb, const double* x, const double* lam, double
 }
 
 // Device-buffer entry: ordered after / before `user` stream, no host sync.
-void DeviceNet::evaluate_device(int nb, const double* dx, const double* dlam, double* dy, double* dj, double* dh,
-                                cudaStream_t user) {
+void DeviceNet::evaluate_device_chunk(int nb, const double* dx, const double* dlam, double* dy, double* dj,
+                                      double* dh, cudaStream_t user) {
   DeviceGuard g(ordinal_);
   ensure_workspace(nb);
   Workspace& w = ws_;

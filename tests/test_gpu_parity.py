@@ -413,3 +413,20 @@ def test_s0_pass_batch_beyond_grid_y_limit():
         assert orc.rel_err(Y[k], ref.forward(X[k])) <= TOL
         assert orc.rel_err(J[k], ref.jacobian(X[k])) <= TOL
         assert orc.rel_err(H[k], ref.lagrangian_hessian(X[k], L[k])) <= TOL
+
+
+def test_batch_above_chunk_limit():
+    """70000 contingency-style points in one call (> DeviceNet::kMaxChunk and
+    > the 65535 grid-y/z limit of the per-point launches): consecutive
+    sub-batches, every point still matches the oracle."""
+    net = gb.random_net([8, 16, 16, 1], "tanh", "sigmoid", 37).bind_device(0)
+    ref = to_oracle(net)
+    rng = np.random.default_rng(37)
+    B = 70000
+    X = rng.normal(1.0, 0.1, (B, 8))
+    L = rng.uniform(0, 1, (B, 1))
+    Y, J, H = net.oracle_batched(X, L)
+    for k in (0, 32767, 32768, 65535, 65536, B - 1):
+        assert orc.rel_err(Y[k], ref.forward(X[k])) <= TOL
+        assert orc.rel_err(J[k], ref.jacobian(X[k])) <= TOL
+        assert orc.rel_err(H[k], ref.lagrangian_hessian(X[k], L[k])) <= TOL
