@@ -1475,27 +1475,56 @@ __global__ void __launch_bounds__(256) syrk_gather_out_kernel(SyrkGather g, cons
   __shared__ double tile[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t nn = static_cast<int64_t>(n) * n;
-  for (int ry = ty; ry < 32; ry += 8) {
-    const int r = by * 32 + ry, c = bx * 32 + tx;
-    double v = 0.0;
-    const bool live = r < n && c <= r;
-    if (live) {
-      const int tm = r / kBM, tn = c / kBM;
-      const int64_t off = (static_cast<int64_t>(b) * g.n_tiles + tm * (tm + 1) / 2 + tn) * (kBM * kBN) +
-                          (r % kBM) * kBN + (c % kBM);
-      const int64_t slice = static_cast<int64_t>(g.points) * g.n_tiles * (kBM * kBN);
-      for (int q = 0; q < g.nseg; ++q) {
-        double t = 0.0;
-        for (int s = 0; s < g.split[q]; ++s) t += __ldcg(g.part[q] + slice * s + off);
-        v += t;
-      }
-      if (hws) v += hws[h_point_stride * b + static_cast<int64_t>(r) * ldh + c];
-      if (packed)
-        out[static_cast<int64_t>(b) * n * (n + 1) / 2 + static_cast<int64_t>(r) * (r + 1) / 2 + c] = v;
-      else
-        out[nn * b + static_cast<int64_t>(r) * n + c] = v;
+  const int64_t slice = static_cast<int64_t>(g.points) * g.n_tiles * (kBM * kBN);
+  // this thread's four elements (rows ty, ty + 8, ...): all loads of a
+  // split chunk for the four rows in flight before their adds (each
+  // element's additions keep the ascending layer / slice order)
+  int64_t off[4];
+  bool live[4];
+  double v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = by * 32 + ty + 8 * i, c = bx * 32 + tx;
+    live[i] = r < n && c <= r;
+    const int tm = live[i] ? r / kBM : 0, tn = live[i] ? c / kBM : 0;
+    off[i] = live[i] ? (static_cast<int64_t>(b) * g.n_tiles + tm * (tm + 1) / 2 + tn) * (kBM * kBN) +
+                           (r % kBM) * kBN + (c % kBM)
+                     : 0;
+    v[i] = 0.0;
+  }
+  for (int q = 0; q < g.nseg; ++q) {
+    const double* base = g.part[q];
+    const int sp = g.split[q];
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    int s = 0;
+    for (; s + 4 <= sp; s += 4) {
+      double a[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[u][i] = live[i] ? __ldcg(base + slice * (s + u) + off[i]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] += a[u][i];
     }
-    tile[ry][tx] = v;
+    for (; s < sp; ++s)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[i] += live[i] ? __ldcg(base + slice * s + off[i]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] += t[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ry = ty + 8 * i, r = by * 32 + ry, c = bx * 32 + tx;
+    if (live[i]) {
+      if (hws) v[i] += hws[h_point_stride * b + static_cast<int64_t>(r) * ldh + c];
+      if (packed)
+        out[static_cast<int64_t>(b) * n * (n + 1) / 2 + static_cast<int64_t>(r) * (r + 1) / 2 + c] = v[i];
+      else
+        out[nn * b + static_cast<int64_t>(r) * n + c] = v[i];
+    }
+    tile[ry][tx] = v[i];
   }
   if (packed) return;
   __syncthreads();
