@@ -681,7 +681,16 @@ def run_b200(args):
         e2e = {"value": total_points * args.steps / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "api": api, "timer": "wall clock around the synchronous calls, max over ranks"}
         if world == 1:
-            ok = ok and bool(np.array_equal(Hh, Hd.cpu().numpy()))
+            # the host-buffer call may evaluate the batch in chunks (c4: 4, so
+            # its copy-out overlaps the next chunk), and split-K factors follow
+            # the batch size: equal to rounding then, bit for bit otherwise
+            Hdn = Hd.cpu().numpy()
+            if np.array_equal(Hh, Hdn):
+                e2e["matches_device"] = "bitwise"
+            else:
+                rel = float(np.abs(Hh - Hdn).max() / max(np.abs(Hdn).max(), 1e-300))
+                e2e["matches_device"] = f"max rel {rel:.1e} (host path in sub-batches)"
+                ok = ok and rel <= 1e-12
         elif rank == 0:
             Yh, Jh, Hh = out
 
