@@ -1717,7 +1717,6 @@ DfPlan& DeviceNet::dataflow_plan(int nb) {
   const int L = static_cast<int>(L_);
   const int tiles_m = static_cast<int>(n_pad_ / kBM);
   auto rows = [&](int l) { return layers_[static_cast<size_t>(l)].rows; };
-  auto cols = [&](int l) { return layers_[static_cast<size_t>(l)].cols; };
   auto kbs = [&](int64_t k) { return ceil_div(k, kBK); };
   const int ring = static_cast<int>(w.t.size());
   auto t_buf = [&](int l) -> double* { return w.t[static_cast<size_t>((l - 1) % ring)]; };
