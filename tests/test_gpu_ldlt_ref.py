@@ -187,3 +187,38 @@ def test_cluster_panel_four_rows_per_thread_known_inertia(monkeypatch):
     b = rng.uniform(-1, 1, n1 + m)
     x = f.solve(b)
     assert np.abs(K @ x - b).max() <= 1e-10 * (np.abs(K).max() * np.abs(x).max() + 1.0)
+
+
+@pytest.mark.parametrize("dim,kernel", [(2048, "panel"), (2049, "cpanel"), (8500, "cpanel"), (8501, "grid")])
+def test_default_kernel_ranges_at_their_edges(dim, kernel):
+    """The default factorisation kernel at the edges of its size ranges
+    (one-CTA panel n <= 2048, cluster panel 2048 < n <= 8500, grid beyond;
+    read from the GBOPT_LDLT_TIMING trace), each with the exact inertia of a
+    saddle point [[D, J^T], [J, 0]] (D > 0, J of full row rank) and a refined
+    solve at the residual bar.  Separate process: the trace goes to stderr."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, paper_2509_22462_b200 as gb\n"
+        "dim = %d; m = dim // 10; n1 = dim - m\n"
+        "rng = np.random.default_rng(dim)\n"
+        "K = np.zeros((dim, dim))\n"
+        "K[np.arange(n1), np.arange(n1)] = rng.uniform(1.0, 4.0, n1)\n"
+        "for i in range(m):\n"
+        "    K[n1 + i, 7 * i:7 * i + 7] = rng.uniform(0.5, 1.5, 7)\n"
+        "    K[n1 + i, n1 - 1 - i] += 1.0\n"
+        "K[:n1, n1:] = K[n1:, :n1].T\n"
+        "f = gb.ldlt_factor(K)\n"
+        "b = rng.uniform(-1, 1, dim); x = f.solve(b)\n"
+        "res = np.abs(K @ x - b).max() / (np.abs(K).max() * np.abs(x).max() + 1.0)\n"
+        "print('RESULT', f.inertia == (n1, m, 0), res)\n" % (root, dim))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, GBOPT_LDLT_TIMING="1"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")][-1].split()
+    assert line[1] == "True" and float(line[2]) <= 1e-10
+    used = "panel" if "bkp_factor_kernel" in r.stderr else "cpanel" if "cpanel nb" in r.stderr else "grid"
+    assert used == kernel, r.stderr[-1500:]
