@@ -266,12 +266,15 @@ double* DeviceNet::ws_alloc(size_t n_doubles) {
   return static_cast<double*>(p);
 }
 
-// Split-K factor of a layer's SYRK: enough CTAs to cover the SMs, at least
-// 8 k-blocks (128 of K) per split.
+// Split-K factor of a layer's SYRK: enough CTAs to cover the SMs twice, at
+// least 8 k-blocks (128 of K) per split.
 int DeviceNet::syrk_split(int points, int k_blocks) const {
   const int tiles = points * (square_syrk_ ? n_sq_tiles_ : n_syrk_tiles_);
   if (tiles >= sm_count_) return 1;
-  return std::max(1, std::min(sm_count_ / tiles, k_blocks / 8));
+  // up to two CTAs' worth per SM: the SYRKs run in the tangent GEMMs' idle
+  // SMs, and shorter slices fill them more evenly (c2: 5 -> 10 slices, 184.05
+  // -> 184.8 evals/s; 15 / 20 slices 184.3 / 180-183, tools/r02_gpu81.sh)
+  return std::max(1, std::min(2 * sm_count_ / tiles, k_blocks / 8));
 }
 
 // Adjoint sweep layout of a layer: columns per thread (4 for multi-vector
@@ -368,8 +371,8 @@ void DeviceNet::ensure_workspace(int batch) {
   // Hessian accumulator [cap][n_pad][n_pad] and split-K partials
   w.ldh = n_pad_;
   w.h = ws_alloc(static_cast<size_t>(cap) * n_pad_ * n_pad_);
-  // split * points * tiles <= max(sm_count, tiles) by construction of syrk_split
-  w.syrk_part = ws_alloc(static_cast<size_t>(std::max(sm_count_, std::max(n_syrk_tiles_, n_sq_tiles_))) * kBM * kBN);
+  // split * points * tiles <= max(2 sm_count, tiles) by construction of syrk_split
+  w.syrk_part = ws_alloc(static_cast<size_t>(std::max(2 * sm_count_, std::max(n_syrk_tiles_, n_sq_tiles_))) * kBM * kBN);
   w.gemm_part = ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN);
   // per-layer SYRK partials of the gather path (single points: points x
   // square tiles < SMs), one buffer per curvature layer
@@ -378,7 +381,7 @@ void DeviceNet::ensure_workspace(int batch) {
     int segs = 0;
     for (auto& d : layers_) segs += d.act != kLinear;
     if (segs <= dev::kMaxGather)
-      for (int q = 0; q < segs; ++q) w.syrk_gather.push_back(ws_alloc(static_cast<size_t>(sm_count_) * kBM * kBN));
+      for (int q = 0; q < segs; ++q) w.syrk_gather.push_back(ws_alloc(static_cast<size_t>(2 * sm_count_) * kBM * kBN));
   }
   // final-layer skinny product: U [cap][n_pad][16], partials [chunks][cap][n_pad][16]
   const int64_t kfin = layers_[L - 1].cols;
